@@ -1,0 +1,229 @@
+/*
+ * tilerun_b200 — C ABI of the B200-native out-of-core tiled GEMM runtime.
+ *
+ * This is the drop-in boundary for the reference package `tilerun`
+ * (/root/reference/pkg/src/tilerun).  The reference is pure Python; its
+ * "FFI" for this path is its public Python API, so every entry point below
+ * names the reference symbol it replaces (file:line under pkg/src/tilerun/).
+ * The Python mirror (paper_1511_04348_b200/) binds these with ctypes; the
+ * binding a maintainer of the reference would add is shown in INTEGRATION.md.
+ *
+ * Conventions
+ *   - Every function returns int status (tr_status).  On failure the
+ *     thread-local message is available from tr_last_error().
+ *   - Plain pointers and sizes only; no torch / numpy types.
+ *   - Matrices are row-major, described by tr_matrix.  Host matrices should be
+ *     pinned (cudaHostAlloc / cudaHostRegister) for full H2D/D2H bandwidth; the
+ *     runtime registers unpinned host ranges for the duration of a call.
+ *   - Tile identity is (matrix uid, tile row, tile col) in STORED coordinates,
+ *     as in scheduler.py:99-138 (Operand).  A uid must name immutable content
+ *     for the lifetime of the session (ann.py:138-140,247).
+ */
+#ifndef TILERUN_B200_H
+#define TILERUN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TR_ABI_VERSION 1
+
+/* ---------------------------------------------------------------- status */
+typedef enum {
+  TR_OK = 0,
+  TR_ERR_CONFIG = 1,     /* devices.py:26-27  ConfigError(ValueError)            */
+  TR_ERR_SHAPE = 2,      /* ValueError: shape / tile / mode (tiles.py:57-58,165-168; scheduler.py:173-180) */
+  TR_ERR_CAPACITY = 3,   /* coherence.py:33-34 CapacityError(RuntimeError)       */
+  TR_ERR_RUNTIME = 4,    /* RuntimeError: incomplete run / double execution (scheduler.py:80-81,587-590) */
+  TR_ERR_CUDA = 5,       /* CUDA runtime / driver failure (RuntimeError)        */
+  TR_ERR_VALUE = 6,      /* other ValueError (pin/unpin misuse, duplicate admit, bad enum) */
+  TR_ERR_INTERNAL = 7,   /* invariant violation (AssertionError in coherence.py:300-313) */
+  TR_ERR_NODEVICE = 8    /* no CUDA device / driver: the product path cannot run */
+} tr_status;
+
+typedef enum { TR_DTYPE_F32 = 0, TR_DTYPE_F64 = 1 } tr_dtype;
+typedef enum { TR_LOC_HOST = 0, TR_LOC_DEVICE = 1 } tr_location;
+
+/* Arithmetic of the tile kernel.  FP32ACC: each fp32/f64 tile is split once at
+ * admission into bf16 hi + lo planes and every k-block issues hi*lo + lo*hi +
+ * hi*hi tcgen05 MMAs into an fp32 TMEM accumulator.  BF16: one plane, one MMA. */
+typedef enum { TR_PREC_BF16 = 0, TR_PREC_FP32ACC = 1 } tr_precision;
+
+typedef enum { TR_POLICY_LRU = 0, TR_POLICY_FIFO = 1 } tr_policy; /* coherence.py:95-99 */
+typedef enum { TR_HIT_L1 = 0, TR_HIT_L2 = 1, TR_HIT_MISS = 2 } tr_hit_level; /* coherence.py:37-40 */
+#define TR_SOURCE_HOST (-1)                                              /* devices.py:20 HOST */
+typedef enum { TR_KIND_ACCELERATOR = 0, TR_KIND_HOST_WORKER = 1 } tr_device_kind; /* devices.py:17-18 */
+
+/* -------------------------------------------------------------- library */
+const char* tr_last_error(void);
+int tr_abi_version(void);
+/* Number of visible CUDA devices (0 on a host without a GPU). */
+int tr_cuda_device_count(int32_t* out);
+
+/* ------------------------------------------------ task queue (msqueue.py:28-67)
+ * Lock-free Michael–Scott MPMC FIFO of uint64 values (counted-pointer CAS).
+ * Replaces MichaelScottQueue.{enqueue,dequeue,is_empty} (msqueue.py:36-58). */
+typedef struct tr_queue tr_queue;
+int tr_queue_create(tr_queue** out);
+int tr_queue_destroy(tr_queue* q);
+int tr_queue_enqueue(tr_queue* q, uint64_t value);
+/* *got = 1 and *value set when an element was dequeued, *got = 0 when empty. */
+int tr_queue_dequeue(tr_queue* q, uint64_t* value, int32_t* got);
+int tr_queue_is_empty(tr_queue* q, int32_t* empty);
+
+/* ------------------------------------- machine description (devices.py:30-216) */
+typedef struct {
+  int32_t device_id;      /* DeviceSpec.device_id (devices.py:43)                       */
+  int32_t kind;           /* tr_device_kind; host workers are rejected by sessions       */
+  int64_t capacity_tiles; /* DeviceSpec.capacity_tiles; -1 = unbounded (HBM-budget bound)  */
+  int32_t slots;          /* reservation-station width (devices.py:49), = CUDA streams   */
+  int32_t gpu;            /* physical CUDA ordinal; -1 = device_id % visible GPUs        */
+  double flops_per_unit;  /* kept for config round-trip; unused on hardware            */
+  double host_bandwidth;  /* idem                                                      */
+} tr_device_spec;
+
+typedef struct {
+  int32_t n_devices;
+  const tr_device_spec* devices;
+  const int64_t* hops;    /* n x n ProximityMatrix.hops (devices.py:78-118)             */
+  int32_t element_bytes;  /* Machine.element_bytes (devices.py:145-154): byte accounting */
+} tr_machine;
+
+/* ----------------------------------- cache directory (coherence.py:86-313) */
+typedef struct {
+  uint64_t matrix; /* interned uid */
+  int64_t row;
+  int64_t col;
+} tr_tile_key; /* tiles.py:29-34 TileKey */
+
+typedef struct {
+  int64_t l1_hits, l2_hits, host_fetches, bytes_host, bytes_peer, evictions, writebacks, bytes_writeback;
+} tr_cache_stats; /* coherence.py:59-83 CacheStats, field for field */
+
+typedef struct {
+  int32_t level;  /* tr_hit_level */
+  int32_t source; /* device id or TR_SOURCE_HOST */
+  int64_t nbytes_moved;
+  int32_t n_evicted;
+} tr_acquire_result; /* coherence.py:49-56 AcquireResult */
+
+typedef struct tr_directory tr_directory;
+/* CacheDirectory(machine, enabled, policy, debug)  coherence.py:95-114 */
+int tr_dir_create(const tr_machine* m, int32_t enabled, int32_t policy, int32_t debug, tr_directory** out);
+int tr_dir_destroy(tr_directory* d);
+/* lookup  coherence.py:118-134 (owner = -1 unless L2) */
+int tr_dir_lookup(tr_directory* d, int32_t requester, const tr_tile_key* key, int32_t* level, int32_t* owner);
+/* admit  coherence.py:136-174; evicted keys copied to `evicted` (capacity `cap`) */
+int tr_dir_admit(tr_directory* d, int32_t device, const tr_tile_key* key, tr_tile_key* evicted, int32_t cap,
+                 int32_t* n_evicted);
+int tr_dir_pin(tr_directory* d, int32_t device, const tr_tile_key* key);   /* 176-180 */
+int tr_dir_unpin(tr_directory* d, int32_t device, const tr_tile_key* key); /* 182-192 */
+int tr_dir_is_pinned(tr_directory* d, int32_t device, const tr_tile_key* key, int32_t* pinned);
+int tr_dir_residents(tr_directory* d, int32_t device, tr_tile_key* out, int64_t cap, int64_t* n);
+int tr_dir_used_tiles(tr_directory* d, int32_t device, int64_t* n);
+/* acquire_input  coherence.py:210-246 */
+int tr_dir_acquire_input(tr_directory* d, int32_t requester, const tr_tile_key* key, int64_t nbytes,
+                         tr_acquire_result* res, tr_tile_key* evicted, int32_t cap);
+int tr_dir_release_input(tr_directory* d, int32_t device, const tr_tile_key* key);           /* 248-252 */
+int tr_dir_admit_output(tr_directory* d, int32_t device, const tr_tile_key* key, tr_tile_key* evicted,
+                        int32_t cap, int32_t* n_evicted);                                        /* 254-261 */
+int tr_dir_release_output(tr_directory* d, int32_t device, const tr_tile_key* key, int64_t nbytes); /* 263-280 */
+int tr_dir_stats(tr_directory* d, tr_cache_stats* global, tr_cache_stats* per_device /* n_devices */);
+int tr_dir_check_invariants(tr_directory* d); /* 296-313 */
+
+/* ------------------- reservation stations + stealing (scheduler.py:200-249) */
+typedef struct tr_station tr_station;
+int tr_station_create(int32_t owner, int32_t width, tr_station** out);
+int tr_station_destroy(tr_station* s);
+/* refill from `q` until full; pulled ids copied out (scheduler.py:214-224) */
+int tr_station_refill(tr_station* s, tr_queue* q, uint64_t* pulled, int32_t cap, int32_t* n);
+int tr_station_pop_for_run(tr_station* s, uint64_t* tid, int32_t* got); /* front, 226-228 */
+int tr_station_try_steal(tr_station* s, uint64_t* tid, int32_t* got);   /* back, 230-232 */
+int tr_station_reserved_count(tr_station* s, int32_t* n);
+/* steal_task  scheduler.py:239-249: victim = most reserved, ties to lowest id. */
+int tr_steal_task(int32_t thief, tr_station* const* stations, int32_t n, uint64_t* tid, int32_t* victim,
+                  int32_t* got);
+
+/* ------------------------------------------ session (scheduler.py:522-621) */
+typedef struct tr_session tr_session;
+
+enum {
+  TR_FLAG_STEAL = 1u << 0,     /* Runtime(steal=True)                                  */
+  TR_FLAG_COHERENCE = 1u << 1, /* Runtime(coherence=True); off = bypass (2g^3 host)     */
+  TR_FLAG_DEBUG = 1u << 2,     /* Runtime(directory_debug=True): invariants per mutation */
+  TR_FLAG_DRYRUN = 1u << 3,    /* schedule-only test mode: no CUDA, no arithmetic, C untouched */
+  TR_FLAG_FIFO = 1u << 4       /* FIFO eviction instead of LRU                          */
+};
+
+typedef struct {
+  const void* ptr; /* host or device base pointer                          */
+  int64_t rows, cols;
+  int64_t ld;      /* elements between rows (>= cols)                         */
+  int32_t dtype;   /* tr_dtype                                                */
+  int32_t location;/* tr_location                                             */
+} tr_matrix;
+
+typedef struct {
+  int64_t tasks_completed, steals_performed, steals_suffered; /* scheduler.py:261-267 */
+} tr_device_stats;
+
+typedef struct {
+  int32_t thief, victim;
+  int64_t task_id;
+} tr_steal_event; /* scheduler.py:252-258 (queue_empty_observed is always true) */
+
+typedef struct {
+  /* outputs filled by tr_gemm */
+  int64_t grid_rows, grid_cols, k_steps, total_tasks;
+  double wall_seconds;
+  tr_cache_stats cache;            /* per-call delta (scheduler.py:576-607) */
+  int64_t n_steals;                /* total steal events (may exceed steals_cap) */
+  int64_t gpu_launches;            /* kernels launched by this call                 */
+  /* caller-provided arrays (may be NULL) */
+  tr_cache_stats* cache_per_device; /* n_devices */
+  tr_device_stats* devices;         /* n_devices */
+  tr_steal_event* steals;           /* steals_cap entries */
+  int64_t steals_cap;
+  uint8_t* completion;              /* total_tasks bytes: exactly-once bitmap snapshot */
+  int64_t completion_cap;
+} tr_gemm_report;
+
+/* Runtime(machine, tile_size, mode, steal, coherence, seed, directory_debug)
+ * (scheduler.py:531-546).  hbm_budget_bytes: per-GPU bytes the tile cache may
+ * occupy (0 = 80% of free memory at creation). */
+int tr_session_create(const tr_machine* m, int32_t tile_size, int32_t precision, uint32_t flags,
+                      int64_t hbm_budget_bytes, tr_session** out);
+int tr_session_destroy(tr_session* s);
+/* Borrowed pointer to the session's directory (Runtime.directory). */
+int tr_session_directory(tr_session* s, tr_directory** out);
+/* Runtime.multiply(a, b, transpose_a, transpose_b, a_uid, b_uid, c_uid)  scheduler.py:559-612:
+ * plans one task per C tile (row-major ids, plan() scheduler.py:165-197), runs one
+ * pinned worker thread per device (_run_threaded scheduler.py:467-516) whose
+ * reservation-station slots are CUDA streams, and blocks until every task executed
+ * exactly once.  `c` must be zero-initialised storage of a.rows x b.cols (after
+ * transposition) of c->dtype; it is fully overwritten. */
+int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t transpose_a, const tr_matrix* b,
+            uint64_t b_uid, int32_t transpose_b, const tr_matrix* c, uint64_t c_uid, tr_gemm_report* report);
+/* Partial product for static multi-process sharding: only tasks t with
+ * t % task_stride == task_offset are planned (all others are left untouched). */
+int tr_gemm_shard(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t transpose_a, const tr_matrix* b,
+                  uint64_t b_uid, int32_t transpose_b, const tr_matrix* c, uint64_t c_uid, int64_t task_offset,
+                  int64_t task_stride, tr_gemm_report* report);
+/* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
+ * measured with CUDA events on the launching streams (sum over launches). */
+int tr_session_kernel_ms(tr_session* s, double* per_device_ms /* n_devices */);
+
+/* ------------------------------- dense in-core product (ann.py:62-75 DenseBackend)
+ * One K1 launch over whole matrices on the current CUDA device, no scheduler and
+ * no tile cache: a, b, c are DEVICE matrices.  accumulate: c += a@b.  `stream`
+ * is a cudaStream_t (NULL = legacy default stream). */
+int tr_dense_gemm(const tr_matrix* a, int32_t transpose_a, const tr_matrix* b, int32_t transpose_b,
+                  const tr_matrix* c, int32_t precision, int32_t accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TILERUN_B200_H */

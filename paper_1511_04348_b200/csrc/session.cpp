@@ -1,0 +1,698 @@
+// GPU runtime session; see session.h for the mapping onto the reference.
+#include "session.h"
+
+#include <pthread.h>
+#include <sched.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "common.h"
+
+namespace tr {
+
+namespace {
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+void pin_thread_to_core(int index) {
+  cpu_set_t allowed;
+  CPU_ZERO(&allowed);
+  if (sched_getaffinity(0, sizeof(allowed), &allowed) != 0) return;
+  std::vector<int> cores;
+  for (int c = 0; c < CPU_SETSIZE; ++c)
+    if (CPU_ISSET(c, &allowed)) cores.push_back(c);
+  if (cores.size() < 2) return;
+  // core 0 of the allowed set stays with the calling (Python) thread
+  const int core = cores[1 + index % static_cast<int>(cores.size() - 1)];
+  cpu_set_t one;
+  CPU_ZERO(&one);
+  CPU_SET(core, &one);
+  pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
+}
+
+}  // namespace
+
+void Job::mark(int64_t tid) {
+  if (done[static_cast<size_t>(tid)].exchange(1) != 0) fail(TR_ERR_RUNTIME, "task %lld executed twice", (long long)tid);
+  done_count.fetch_add(1);
+}
+
+void Job::set_error(int status, const std::string& msg) {
+  std::lock_guard<std::mutex> g(mu);
+  if (err_status == 0) {
+    err_status = status;
+    err_msg = msg;
+  }
+  abort.store(true);
+}
+
+// ---------------------------------------------------------------- construction
+Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t flags, int64_t hbm_budget)
+    : tile_(tile), precision_(precision), flags_(flags), hbm_budget_(hbm_budget) {
+  if (tile < 1) fail(TR_ERR_SHAPE, "tile_size must be >= 1, got %d", tile);
+  if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC) fail(TR_ERR_VALUE, "unknown precision %d", precision);
+  if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
+  dryrun_ = flags & TR_FLAG_DRYRUN;
+  steal_ = flags & TR_FLAG_STEAL;
+  coherence_ = flags & TR_FLAG_COHERENCE;
+  element_bytes_ = m.element_bytes > 0 ? m.element_bytes : 8;
+  planes_ = precision == TR_PREC_FP32ACC ? 2 : 1;
+  ld_ = ceil_div(tile, 8) * 8;
+  plane_elems_ = static_cast<int64_t>(tile) * ld_;
+  slot_elems_ = planes_ * plane_elems_;
+
+  const int n = m.n_devices;
+  std::vector<int64_t> caps(n), hops(static_cast<size_t>(n) * n);
+  std::vector<bool> hw(n, false);
+  for (int d = 0; d < n; ++d) {
+    const tr_device_spec& ds = m.devices[d];
+    if (ds.device_id != d) fail(TR_ERR_CONFIG, "device ids must be 0..%d in order", n - 1);
+    if (ds.kind != TR_KIND_ACCELERATOR)
+      fail(TR_ERR_CONFIG, "device %d is a host-worker: the B200 runtime has no CPU compute path", d);
+    if (ds.slots < 1 || ds.slots > 32) fail(TR_ERR_CONFIG, "device %d: slots must be in 1..32", d);
+    caps[d] = ds.capacity_tiles;
+    if (caps[d] >= 0 && caps[d] < 3) fail(TR_ERR_CONFIG, "capacity_tiles must be >= 3 (A+B+C working set)");
+  }
+  for (int64_t i = 0; i < static_cast<int64_t>(n) * n; ++i) hops[i] = m.hops ? m.hops[i] : (i % (n + 1) ? 1 : 0);
+  dir_ = std::make_unique<Directory>(n, caps, hw, hops, coherence_, (flags & TR_FLAG_FIFO) ? TR_POLICY_FIFO : TR_POLICY_LRU,
+                                     (flags & TR_FLAG_DEBUG) != 0);
+
+  int n_gpus = 0;
+  if (!dryrun_) {
+    cudaError_t e = cudaGetDeviceCount(&n_gpus);
+    if (e != cudaSuccess || n_gpus < 1) {
+      cudaGetLastError();
+      fail(TR_ERR_NODEVICE, "no CUDA device available (%s): the tile GEMM runs only on the GPU",
+           e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    }
+  }
+  devs_.resize(n);
+  std::vector<int> per_gpu(std::max(n_gpus, 1), 0);
+  for (int d = 0; d < n; ++d) {
+    DeviceCtx& dc = devs_[d];
+    dc.id = d;
+    dc.width = m.devices[d].slots;
+    dc.max_inflight = std::min(dc.width, 2);
+    dc.capacity = caps[d];
+    dc.gpu = dryrun_ ? 0 : (m.devices[d].gpu >= 0 ? m.devices[d].gpu : d % n_gpus);
+    if (!dryrun_ && dc.gpu >= n_gpus) fail(TR_ERR_CONFIG, "device %d maps to GPU %d but only %d visible", d, dc.gpu, n_gpus);
+    per_gpu[dc.gpu] += 1;
+    dc.station = std::make_unique<Station>(d, dc.width);
+    station_ptrs_.push_back(dc.station.get());
+  }
+  if (!dryrun_) {
+    for (int d = 0; d < n; ++d) {
+      DeviceCtx& dc = devs_[d];
+      TR_CUDA(cudaSetDevice(dc.gpu));
+      size_t free_b = 0, total_b = 0;
+      TR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      int64_t budget = hbm_budget_ > 0 ? hbm_budget_ : static_cast<int64_t>(0.8 * static_cast<double>(free_b));
+      budget /= per_gpu[dc.gpu];
+      const int64_t tile_bytes = static_cast<int64_t>(tile) * tile * 8;
+      const int64_t slot_bytes = slot_elems_ * 2;
+      int64_t avail = budget - static_cast<int64_t>(dc.width) * 2 * tile_bytes;
+      int64_t slots = avail / slot_bytes - 2 * dc.width;
+      slots = std::min<int64_t>(slots, int64_t(1) << 22);
+      if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
+      if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
+      dc.max_slots = static_cast<int32_t>(slots);
+      dc.streams.resize(dc.width);
+      for (auto& sc : dc.streams) {
+        TR_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+        for (auto& ev : sc.ring) TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
+        TR_CUDA(cudaMalloc(&sc.staging, tile_bytes));
+        TR_CUDA(cudaMalloc(&sc.outbuf, tile_bytes));
+      }
+    }
+    // Peer access between every pair of distinct GPUs in use (NVLink / NVSwitch).
+    for (int d = 0; d < n; ++d) {
+      for (int o = 0; o < n; ++o) {
+        const int g = devs_[d].gpu, h = devs_[o].gpu;
+        if (g == h) continue;
+        int can = 0;
+        TR_CUDA(cudaDeviceCanAccessPeer(&can, g, h));
+        if (!can) continue;
+        TR_CUDA(cudaSetDevice(g));
+        cudaError_t e = cudaDeviceEnablePeerAccess(h, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else TR_CUDA(e);
+      }
+    }
+  }
+  for (int d = 0; d < n; ++d) devs_[d].worker = std::thread(&Session::worker_main, this, d);
+}
+
+Session::~Session() {
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    shutdown_ = true;
+  }
+  cv_.notify_all();
+  for (auto& dc : devs_)
+    if (dc.worker.joinable()) dc.worker.join();
+  if (dryrun_) return;
+  for (auto& dc : devs_) {
+    cudaSetDevice(dc.gpu);
+    cudaDeviceSynchronize();
+    for (auto& sc : dc.streams) {
+      for (auto& ev : sc.ring) cudaEventDestroy(ev);
+      cudaEventDestroy(sc.done);
+      cudaFree(sc.staging);
+      cudaFree(sc.outbuf);
+      cudaStreamDestroy(sc.stream);
+    }
+    for (auto& t : dc.timed) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    for (auto& t : dc.timed_pool) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.end);
+    }
+    if (dc.slab) cudaFree(dc.slab);
+  }
+}
+
+// ---------------------------------------------------------------- HBM slab
+void Session::build_tmaps(int d) {
+  DeviceCtx& dc = devs_[d];
+  PlaneGeom g;
+  g.base = dc.slab;
+  g.cols = tile_;
+  g.rows = tile_;
+  g.nplanes = static_cast<int64_t>(dc.slab_slots + 2 * dc.width) * planes_;
+  g.ld = ld_;
+  g.plane_stride = plane_elems_;
+  for (int b = 0; b < 4; ++b) {
+    const int r = make_plane_tmap(&dc.tmap[b], g, static_cast<BoxKind>(b));
+    if (r != 0) fail(TR_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) for device %d", r, d);
+  }
+}
+
+void Session::ensure_slab(int d, int64_t needed) {
+  DeviceCtx& dc = devs_[d];
+  const int64_t target = std::min<int64_t>(dc.max_slots, std::max<int64_t>(needed, 1));
+  if (target <= dc.slab_slots) return;
+  int64_t grow = std::min<int64_t>(dc.max_slots, std::max<int64_t>(target, 2 * static_cast<int64_t>(dc.slab_slots)));
+  const int64_t scratch = 2 * dc.width;
+  TR_CUDA(cudaSetDevice(dc.gpu));
+  TR_CUDA(cudaDeviceSynchronize());
+  uint16_t* nb = nullptr;
+  cudaError_t e = cudaMalloc(&nb, static_cast<size_t>((grow + scratch) * slot_elems_ * 2));
+  if (e != cudaSuccess && grow > target) {
+    cudaGetLastError();
+    grow = target;
+    e = cudaMalloc(&nb, static_cast<size_t>((grow + scratch) * slot_elems_ * 2));
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(TR_ERR_CAPACITY, "device %d: cannot allocate a %lld-slot tile slab (%s)", d, (long long)grow,
+         cudaGetErrorString(e));
+  }
+  if (dc.slab) {
+    TR_CUDA(cudaMemcpy(nb, dc.slab, static_cast<size_t>((dc.slab_slots + scratch) * slot_elems_ * 2),
+                       cudaMemcpyDeviceToDevice));
+    TR_CUDA(cudaFree(dc.slab));
+  }
+  dc.slab = nb;
+  dc.slab_slots = static_cast<int32_t>(grow);
+  dc.slots.resize(static_cast<size_t>(grow + scratch));
+  {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    dir_->attach_slots(d, dc.slab_slots);
+  }
+  build_tmaps(d);
+}
+
+// ---------------------------------------------------------------- events / ordering
+cudaEvent_t Session::record(int d, int s) {
+  StreamCtx& sc = devs_[d].streams[s];
+  cudaEvent_t ev = sc.ring[sc.next++ % kRing];
+  TR_CUDA(cudaEventRecord(ev, sc.stream));
+  return ev;
+}
+
+void Session::wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev) {
+  if (gs < 0 || gs == gs_of(d, s)) return;  // same stream: already ordered
+  TR_CUDA(cudaStreamWaitEvent(devs_[d].streams[s].stream, ev, 0));
+}
+
+// Before overwriting physical slot `phys` of device d from stream s: every other
+// stream that read it (kernels, peer copies) or is still filling it must be done.
+void Session::wait_slot_free(int d, int s, int32_t phys) {
+  SlotState& st = devs_[d].slots[phys];
+  wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
+  for (auto& u : st.uses) wait_event_if_foreign(d, s, u.first, u.second);
+}
+
+// Miss path: host (pinned) -> staging -> split/convert into the slot, or
+// device matrix -> split/convert directly.
+void Session::fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c) {
+  DeviceCtx& dc = devs_[d];
+  StreamCtx& sc = dc.streams[s];
+  const int64_t T = tile_;
+  const int64_t tr_ = std::min(T, src.rows - r * T);
+  const int64_t tc = std::min(T, src.cols - c * T);
+  const int64_t es = src.esize();
+  const char* base = static_cast<const char*>(src.ptr) + (r * T * src.ld + c * T) * es;
+  const void* conv_src = base;
+  int64_t conv_ld = src.ld;
+  if (src.location == TR_LOC_HOST) {
+    TR_CUDA(cudaMemcpy2DAsync(sc.staging, tc * es, base, src.ld * es, tc * es, tr_, cudaMemcpyHostToDevice, sc.stream));
+    conv_src = sc.staging;
+    conv_ld = tc;
+  }
+  TR_CUDA(launch_split_convert(conv_src, src.dtype == TR_DTYPE_F64, conv_ld, tr_, tc, slot_ptr(d, phys), ld_, T,
+                               plane_elems_, planes_, sc.stream));
+}
+
+// One input tile for device d, task stream s: directory accounting exactly as
+// coherence.py:210-246, then the physical action for the hit level.
+int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r,
+                         int64_t c, int scratch) {
+  // r, c are STORED coordinates of the tile (Operand.key, scheduler.py:132-134)
+  (void)transposed;
+  const int64_t T = tile_;
+  const int64_t nbytes = std::min(T, src.rows - r * T) * std::min(T, src.cols - c * T) * element_bytes_;
+  const TileKey key{uid, r, c};
+  const int32_t gs = gs_of(d, s);
+  std::lock_guard<std::mutex> g(dir_->mu);
+  Acquired a = dir_->acquire_input_locked(d, key, nbytes);
+  if (dryrun_) return a.slot;
+  if (!coherence_) {
+    // bypass (coherence.py:220-225): every request is a host fetch into a per-stream scratch slot
+    const int32_t phys = scratch_phys(s, scratch);
+    fill_slot(d, s, phys, src, r, c);
+    job.launches.fetch_add(1);
+    return phys;
+  }
+  DeviceCtx& dc = devs_[d];
+  const int32_t phys = phys_of(d, a.slot);
+  SlotState& st = dc.slots[phys];
+  if (a.level == HIT_L1) {
+    wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
+    return phys;
+  }
+  wait_slot_free(d, s, phys);
+  StreamCtx& sc = dc.streams[s];
+  if (a.level == HIT_L2) {
+    const int o = a.source;
+    const int32_t src_phys = phys_of(o, dir_->slot_of_locked(o, key));
+    SlotState& ss = devs_[o].slots[src_phys];
+    wait_event_if_foreign(d, s, ss.ready_gs, ss.ready_ev);
+    const size_t bytes = static_cast<size_t>(slot_elems_ * 2);
+    if (devs_[o].gpu == dc.gpu) {
+      TR_CUDA(cudaMemcpyAsync(slot_ptr(d, phys), slot_ptr(o, src_phys), bytes, cudaMemcpyDeviceToDevice, sc.stream));
+    } else {
+      TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, sc.stream));
+    }
+    cudaEvent_t ev = record(d, s);
+    bool found = false;
+    for (auto& u : ss.uses)
+      if (u.first == gs) {
+        u.second = ev;
+        found = true;
+      }
+    if (!found) ss.uses.emplace_back(gs, ev);
+    st.ready_gs = gs;
+    st.ready_ev = ev;
+    st.uses.clear();
+    return phys;
+  }
+  fill_slot(d, s, phys, src, r, c);
+  job.launches.fetch_add(1);
+  st.ready_gs = gs;
+  st.ready_ev = record(d, s);
+  st.uses.clear();
+  return phys;
+}
+
+// ---------------------------------------------------------------- task issue
+// _execute_task (scheduler.py:371-410), asynchronous: the host sequence of
+// directory operations is identical; the arithmetic is enqueued on stream s.
+void Session::issue(int d, Job& job, int64_t tid, int s) {
+  DeviceCtx& dc = devs_[d];
+  const int64_t T = tile_;
+  const int64_t i = tid / job.grid_cols, j = tid % job.grid_cols;
+  const int64_t mt = std::min(T, job.M - i * T);
+  const int64_t nt = std::min(T, job.N - j * T);
+  const TileKey c_key{job.c_uid, i, j};
+  const int64_t ks = job.k_steps;
+  int64_t chunk = ks;
+  if (!coherence_) chunk = 1;
+  else if (dc.capacity >= 0 && dc.capacity < 2 * ks + 1) chunk = std::max<int64_t>(1, (dc.capacity - 1) / 2);
+  chunk = std::min<int64_t>(chunk, kMaxKSteps);
+  {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    dir_->admit_output_locked(d, c_key);  // pinned for the whole task (scheduler.py:390)
+  }
+  StreamCtx* scp = dryrun_ ? nullptr : &dc.streams[s];
+  const int64_t ces = job.c.esize();
+  void* cptr = nullptr;
+  int64_t ldc = 0;
+  if (!dryrun_) {
+    if (job.c.location == TR_LOC_HOST) {
+      cptr = scp->outbuf;
+      ldc = nt;
+    } else {
+      cptr = const_cast<char*>(static_cast<const char*>(job.c.ptr)) + (i * T * job.c.ld + j * T) * ces;
+      ldc = job.c.ld;
+    }
+  }
+  for (int64_t k0 = 0; k0 < ks; k0 += chunk) {
+    const int64_t kc = std::min(chunk, ks - k0);
+    GemmArgs args;
+    std::memset(&args, 0, sizeof(args));
+    args.m_valid = static_cast<int32_t>(mt);
+    args.n_valid = static_cast<int32_t>(nt);
+    args.n_ksteps = static_cast<int32_t>(kc);
+    args.planes = planes_;
+    args.c = cptr;
+    args.ldc = ldc;
+    args.c_f64 = job.c.dtype == TR_DTYPE_F64;
+    args.epilogue = k0 == 0 ? EPI_STORE : EPI_ACCUMULATE;
+    args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+    std::vector<TileKey> used;
+    std::vector<int32_t> used_phys;
+    for (int64_t k = k0; k < k0 + kc; ++k) {
+      // input acquire order per k-step: A then B (scheduler.py:394-396)
+      const int64_t ar = job.ta ? k : i, ac = job.ta ? i : k;
+      const int64_t br = job.tb ? j : k, bc = job.tb ? k : j;
+      const int32_t pa = acquire(d, s, job, job.a, job.a_uid, job.ta, ar, ac, 0);
+      const int32_t pb = acquire(d, s, job, job.b, job.b_uid, job.tb, br, bc, 1);
+      args.a_z[k - k0] = pa * planes_;
+      args.b_z[k - k0] = pb * planes_;
+      args.k_len[k - k0] = static_cast<int32_t>(std::min(T, job.K - k * T));
+      used.push_back(TileKey{job.a_uid, ar, ac});
+      used.push_back(TileKey{job.b_uid, br, bc});
+      used_phys.push_back(pa);
+      used_phys.push_back(pb);
+    }
+    if (!dryrun_) {
+      BoxKind ba, bb;
+      gemm_boxes(job.ta, job.tb, &ba, &bb);
+      TimedLaunch tl;
+      if (!dc.timed_pool.empty()) {
+        tl = dc.timed_pool.back();
+        dc.timed_pool.pop_back();
+      } else {
+        TR_CUDA(cudaEventCreate(&tl.start));
+        TR_CUDA(cudaEventCreate(&tl.end));
+      }
+      TR_CUDA(cudaEventRecord(tl.start, scp->stream));
+      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, job.ta, job.tb, scp->stream));
+      TR_CUDA(cudaEventRecord(tl.end, scp->stream));
+      dc.timed.push_back(tl);
+      job.launches.fetch_add(1);
+    }
+    {
+      std::lock_guard<std::mutex> g(dir_->mu);
+      if (!dryrun_ && coherence_) {
+        cudaEvent_t ev = record(d, s);
+        const int32_t gs = gs_of(d, s);
+        for (int32_t p : used_phys) {
+          SlotState& st = dc.slots[p];
+          bool found = false;
+          for (auto& u : st.uses)
+            if (u.first == gs) {
+              u.second = ev;
+              found = true;
+            }
+          if (!found) st.uses.emplace_back(gs, ev);
+        }
+      }
+      for (const TileKey& k : used) dir_->release_input_locked(d, k);
+    }
+  }
+  const int64_t wb_bytes = mt * nt * element_bytes_;
+  if (!dryrun_ && job.c.location == TR_LOC_HOST) {
+    char* dst = const_cast<char*>(static_cast<const char*>(job.c.ptr)) + (i * T * job.c.ld + j * T) * ces;
+    TR_CUDA(cudaMemcpy2DAsync(dst, job.c.ld * ces, scp->outbuf, nt * ces, nt * ces, mt, cudaMemcpyDeviceToHost,
+                              scp->stream));
+  }
+  {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    dir_->release_output_locked(d, c_key, wb_bytes);  // coherence.py:263-280
+  }
+  if (dryrun_) {
+    job.mark(tid);
+    dc.stats.tasks_completed += 1;
+    return;
+  }
+  TR_CUDA(cudaEventRecord(scp->done, scp->stream));
+  scp->task = tid;
+}
+
+void Session::reap(int d, Job& job, bool block_oldest) {
+  DeviceCtx& dc = devs_[d];
+  int oldest = -1;
+  for (int s = 0; s < dc.width; ++s) {
+    StreamCtx& sc = dc.streams[s];
+    if (sc.task < 0) continue;
+    if (oldest < 0 || sc.seq < dc.streams[oldest].seq) oldest = s;
+  }
+  if (block_oldest && oldest >= 0) TR_CUDA(cudaEventSynchronize(dc.streams[oldest].done));
+  for (int s = 0; s < dc.width; ++s) {
+    StreamCtx& sc = dc.streams[s];
+    if (sc.task < 0) continue;
+    cudaError_t e = cudaEventQuery(sc.done);
+    if (e == cudaErrorNotReady) continue;
+    TR_CUDA(e);
+    job.mark(sc.task);
+    dc.stats.tasks_completed += 1;
+    sc.task = -1;
+  }
+}
+
+// The device worker (scheduler.py:475-505): refill -> pop -> steal -> issue.
+void Session::run_job(int d, Job& job) {
+  DeviceCtx& dc = devs_[d];
+  Station& st = *dc.station;
+  uint64_t seq = 0;
+  while (!job.abort.load()) {
+    int active = 0;
+    if (!dryrun_) {
+      reap(d, job, false);
+      for (auto& sc : dc.streams) active += sc.task >= 0;
+    }
+    if (active >= dc.max_inflight) {
+      reap(d, job, true);
+      continue;
+    }
+    st.refill(job.queue, dc.width - active);
+    uint64_t tid;
+    int victim = -1;
+    if (!st.pop_for_run(&tid)) {
+      if (!job.queue.is_empty()) continue;  // raced with other refills
+      bool got = false;
+      if (steal_) got = steal_task(d, station_ptrs_.data(), static_cast<int>(station_ptrs_.size()), &tid, &victim);
+      if (!got) {
+        if (active == 0) {
+          if (job.all_done()) return;
+          std::this_thread::sleep_for(std::chrono::microseconds(50));
+        } else {
+          reap(d, job, true);
+        }
+        continue;
+      }
+    }
+    if (victim >= 0) {
+      std::lock_guard<std::mutex> g(job.mu);
+      job.steals.push_back(tr_steal_event{d, victim, static_cast<int64_t>(tid)});
+      dc.stats.steals_performed += 1;
+      devs_[victim].stats.steals_suffered += 1;
+    }
+    int s = 0;
+    if (!dryrun_) {
+      while (dc.streams[s].task >= 0) ++s;
+      dc.streams[s].seq = ++seq;
+    }
+    issue(d, job, static_cast<int64_t>(tid), s);
+  }
+}
+
+void Session::worker_main(int d) {
+  pin_thread_to_core(d);
+  if (!dryrun_) cudaSetDevice(devs_[d].gpu);
+  uint64_t seen = 0;
+  for (;;) {
+    Job* job;
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait(lk, [&] { return shutdown_ || generation_ != seen; });
+      if (shutdown_) return;
+      seen = generation_;
+      job = job_;
+    }
+    try {
+      run_job(d, *job);
+    } catch (const Error& e) {
+      job->set_error(e.status, e.what());
+    } catch (const std::exception& e) {
+      job->set_error(TR_ERR_INTERNAL, e.what());
+    }
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      workers_done_ += 1;
+    }
+    cv_done_.notify_all();
+  }
+}
+
+// ---------------------------------------------------------------- one product
+namespace {
+struct HostReg {
+  std::vector<const void*> regs;
+  void ensure(const Mat& m) {
+    if (m.location != TR_LOC_HOST || !m.ptr) return;
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, m.ptr);
+    if (e == cudaSuccess && attr.type == cudaMemoryTypeHost) return;
+    cudaGetLastError();
+    const size_t bytes = static_cast<size_t>(((m.rows - 1) * m.ld + m.cols) * m.esize());
+    if (cudaHostRegister(const_cast<void*>(m.ptr), bytes, cudaHostRegisterPortable) == cudaSuccess)
+      regs.push_back(m.ptr);
+    else
+      cudaGetLastError();  // fall back to pageable copies
+  }
+  ~HostReg() {
+    for (const void* p : regs) cudaHostUnregister(const_cast<void*>(p));
+  }
+};
+}  // namespace
+
+void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t b_uid, bool tb, const Mat& c,
+                   uint64_t c_uid, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep) {
+  const int64_t M = ta ? a.cols : a.rows, K = ta ? a.rows : a.cols;
+  const int64_t Kb = tb ? b.cols : b.rows, N = tb ? b.rows : b.cols;
+  if (a.rows < 1 || a.cols < 1 || b.rows < 1 || b.cols < 1) fail(TR_ERR_SHAPE, "matrix dimensions must be >= 1");
+  if (K != Kb)
+    fail(TR_ERR_SHAPE, "inner dimensions differ: (%lld, %lld) x (%lld, %lld)", (long long)M, (long long)K,
+         (long long)Kb, (long long)N);
+  if (c.rows != M || c.cols != N) fail(TR_ERR_SHAPE, "output is %lldx%lld, expected %lldx%lld", (long long)c.rows,
+                                       (long long)c.cols, (long long)M, (long long)N);
+  for (const Mat* m : {&a, &b, &c})
+    if (m->ld < m->cols || (!dryrun_ && !m->ptr)) fail(TR_ERR_SHAPE, "bad matrix descriptor (ld < cols or null)");
+  if (task_stride < 1 || task_offset < 0 || task_offset >= task_stride) fail(TR_ERR_VALUE, "bad task shard");
+  const int64_t T = tile_;
+  Job job(ceil_div(M, T) * ceil_div(N, T));
+  job.a = a;
+  job.b = b;
+  job.c = c;
+  job.ta = ta;
+  job.tb = tb;
+  job.a_uid = a_uid;
+  job.b_uid = b_uid;
+  job.c_uid = c_uid;
+  job.M = M;
+  job.N = N;
+  job.K = K;
+  job.grid_rows = ceil_div(M, T);
+  job.grid_cols = ceil_div(N, T);
+  job.k_steps = ceil_div(K, T);
+  job.task_offset = task_offset;
+  job.task_stride = task_stride;
+  // plan(): every task enqueued up front, row-major (scheduler.py:189-192)
+  const int64_t total = job.grid_rows * job.grid_cols;
+  int64_t planned = 0;
+  for (int64_t t = task_offset; t < total; t += task_stride) {
+    job.queue.enqueue(static_cast<uint64_t>(t));
+    ++planned;
+  }
+  job.n_tasks = planned;
+  for (auto& dc : devs_) {
+    dc.station->clear();
+    dc.stats = tr_device_stats{};
+  }
+
+  int prev_dev = 0;
+  if (!dryrun_) cudaGetDevice(&prev_dev);
+  struct RestoreDev {
+    bool on;
+    int dev;
+    ~RestoreDev() {
+      if (on) cudaSetDevice(dev);
+    }
+  } restore{!dryrun_, prev_dev};
+  HostReg reg;
+  if (!dryrun_) {
+    reg.ensure(a);
+    reg.ensure(b);
+    reg.ensure(c);
+    const int64_t a_tiles = ceil_div(a.rows, T) * ceil_div(a.cols, T);
+    const int64_t b_tiles = ceil_div(b.rows, T) * ceil_div(b.cols, T);
+    for (int d = 0; d < n_devices(); ++d) ensure_slab(d, dir_->used_tiles(d) + a_tiles + b_tiles);
+  }
+  const tr_cache_stats before = dir_->stats();
+  const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    job_ = &job;
+    workers_done_ = 0;
+    generation_ += 1;
+  }
+  cv_.notify_all();
+  {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_done_.wait(lk, [&] { return workers_done_ == n_devices(); });
+    job_ = nullptr;
+  }
+  if (!dryrun_) {
+    for (auto& dc : devs_) {
+      cudaSetDevice(dc.gpu);
+      for (auto& sc : dc.streams) {
+        cudaError_t e = cudaStreamSynchronize(sc.stream);
+        if (e != cudaSuccess) job.set_error(TR_ERR_CUDA, std::string("stream sync: ") + cudaGetErrorString(e));
+        sc.task = -1;
+      }
+    }
+  }
+  const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // kernel timings
+  for (auto& dc : devs_) {
+    double ms = 0;
+    for (auto& tl : dc.timed) {
+      float x = 0;
+      if (cudaEventElapsedTime(&x, tl.start, tl.end) == cudaSuccess) ms += x;
+      else cudaGetLastError();
+      dc.timed_pool.push_back(tl);
+    }
+    dc.timed.clear();
+    dc.last_kernel_ms = ms;
+  }
+  if (job.err_status) throw Error(job.err_status, job.err_msg);
+  if (!job.all_done())
+    fail(TR_ERR_RUNTIME, "run incomplete: %lld/%lld tasks", (long long)job.done_count.load(), (long long)job.n_tasks);
+
+  if (rep) {
+    rep->grid_rows = job.grid_rows;
+    rep->grid_cols = job.grid_cols;
+    rep->k_steps = job.k_steps;
+    rep->total_tasks = job.n_tasks;
+    rep->wall_seconds = wall;
+    rep->cache = sub_stats(dir_->stats(), before);
+    rep->n_steals = static_cast<int64_t>(job.steals.size());
+    rep->gpu_launches = job.launches.load();
+    const auto after_dev = dir_->stats_per_device();
+    for (int d = 0; d < n_devices(); ++d) {
+      if (rep->cache_per_device) rep->cache_per_device[d] = sub_stats(after_dev[d], before_dev[d]);
+      if (rep->devices) rep->devices[d] = devs_[d].stats;
+    }
+    if (rep->steals)
+      for (int64_t k = 0; k < std::min<int64_t>(rep->steals_cap, rep->n_steals); ++k) rep->steals[k] = job.steals[k];
+    if (rep->completion)
+      for (int64_t t = 0; t < std::min<int64_t>(rep->completion_cap, total); ++t)
+        rep->completion[t] = job.done[static_cast<size_t>(t)].load();
+  }
+}
+
+void Session::kernel_ms(double* out) const {
+  for (int d = 0; d < static_cast<int>(devs_.size()); ++d) out[d] = devs_[d].last_kernel_ms;
+}
+
+}  // namespace tr

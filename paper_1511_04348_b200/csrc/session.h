@@ -1,0 +1,167 @@
+// The GPU runtime session: Runtime (scheduler.py:522-621) re-designed for B200.
+//
+//   reference (Python, simulated devices)        this build
+//   ------------------------------------------   ------------------------------------------------
+//   one Python thread per device (467-516)       one pinned C++ thread per logical device
+//   ReservationStation width 4 (200-236)         station entries feed CUDA streams (one per entry)
+//   _execute_task k-loop (371-410)               async issue: acquire tiles -> fills on the
+//                                                task's stream -> ONE tcgen05 GEMM launch over
+//                                                all k-steps -> D2H writeback of C
+//   CacheDirectory (coherence.py)                same directory + physical HBM slab slots;
+//                                                L2 hit = cudaMemcpyPeerAsync from the owner,
+//                                                miss = pinned-host H2D + split/convert (K2)
+//   instantaneous copies under one lock          copies are async; ordering is enforced with
+//                                                CUDA events: a slot is refilled only after every
+//                                                stream that read it has passed its last use
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <exception>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "directory.h"
+#include "msqueue.h"
+#include "station.h"
+#include "tile_gemm.h"
+
+namespace tr {
+
+struct Mat {
+  const void* ptr = nullptr;
+  int64_t rows = 0, cols = 0, ld = 0;
+  int32_t dtype = TR_DTYPE_F32;
+  int32_t location = TR_LOC_HOST;
+  int64_t esize() const { return dtype == TR_DTYPE_F64 ? 8 : 4; }
+};
+
+class Session;
+
+struct Job {
+  Mat a, b, c;
+  bool ta = false, tb = false;
+  uint64_t a_uid = 0, b_uid = 0, c_uid = 0;
+  int64_t M = 0, N = 0, K = 0;
+  int64_t grid_rows = 0, grid_cols = 0, k_steps = 0;
+  int64_t task_offset = 0, task_stride = 1;
+  int64_t n_tasks = 0;  // planned tasks (shard)
+  MSQueue queue;
+  std::vector<std::atomic<uint8_t>> done;  // exactly-once bitmap over ALL task ids
+  std::atomic<int64_t> done_count{0};
+  std::atomic<bool> abort{false};
+  std::mutex mu;  // errors + steal log
+  int err_status = 0;
+  std::string err_msg;
+  std::vector<tr_steal_event> steals;
+  std::atomic<int64_t> launches{0};
+
+  explicit Job(int64_t total) : done(static_cast<size_t>(total)) {
+    for (auto& d : done) d.store(0);
+  }
+  void mark(int64_t tid);  // scheduler.py:78-83
+  bool all_done() const { return done_count.load() == n_tasks; }
+  void set_error(int status, const std::string& msg);
+};
+
+class Session {
+ public:
+  Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t flags, int64_t hbm_budget);
+  ~Session();
+
+  Directory& directory() { return *dir_; }
+  int n_devices() const { return static_cast<int>(devs_.size()); }
+  // Runs one product (scheduler.py:559-612); fills `rep`.
+  void gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t b_uid, bool tb, const Mat& c,
+            uint64_t c_uid, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep);
+  void kernel_ms(double* out) const;
+
+ private:
+  static constexpr int kRing = 64;
+
+  struct SlotState {
+    int32_t ready_gs = -1;
+    cudaEvent_t ready_ev = nullptr;
+    std::vector<std::pair<int32_t, cudaEvent_t>> uses;  // (global stream, event of last use)
+  };
+  struct StreamCtx {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ring[kRing] = {};
+    uint32_t next = 0;
+    cudaEvent_t done = nullptr;
+    int64_t task = -1;      // in-flight task id, -1 idle
+    uint64_t seq = 0;       // issue order
+    void* staging = nullptr;  // host-tile landing zone (T*T*8 bytes)
+    void* outbuf = nullptr;   // C tile for host outputs (T*T*8 bytes)
+  };
+  struct TimedLaunch {
+    cudaEvent_t start, end;
+  };
+  struct DeviceCtx {
+    int id = 0, gpu = 0, width = 4, max_inflight = 2;
+    int64_t capacity = -1;
+    uint16_t* slab = nullptr;
+    int32_t slab_slots = 0;  // directory slots allocated (physical = slab_slots + scratch)
+    int32_t max_slots = 0;
+    CUtensorMap tmap[4];
+    std::vector<SlotState> slots;  // indexed by physical slot
+    std::vector<StreamCtx> streams;
+    std::unique_ptr<Station> station;
+    tr_device_stats stats{};
+    std::vector<TimedLaunch> timed, timed_pool;
+    double last_kernel_ms = 0;
+    std::thread worker;
+  };
+
+  // worker-side
+  void worker_main(int d);
+  void run_job(int d, Job& job);
+  void issue(int d, Job& job, int64_t tid, int s);
+  int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
+                  int scratch);
+  void fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c);
+  void wait_slot_free(int d, int s, int32_t phys);
+  void wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev);
+  cudaEvent_t record(int d, int s);
+  int32_t gs_of(int d, int s) const { return d * 64 + s; }
+  void reap(int d, Job& job, bool block_oldest);
+
+  // session-side
+  void ensure_slab(int d, int64_t needed);
+  void build_tmaps(int d);
+  uint16_t* slot_ptr(int d, int32_t phys) const {
+    return devs_[d].slab + static_cast<int64_t>(phys) * slot_elems_;
+  }
+  int32_t scratch_phys(int s, int which) const { return 2 * s + which; }
+  int32_t phys_of(int d, int32_t dir_slot) const { return dir_slot + 2 * devs_[d].width; }
+
+  int32_t tile_;
+  int32_t precision_;
+  int planes_;
+  int64_t ld_, plane_elems_, slot_elems_;
+  uint32_t flags_;
+  bool dryrun_, steal_, coherence_;
+  int32_t element_bytes_;
+  int64_t hbm_budget_;
+  std::unique_ptr<Directory> dir_;
+  std::vector<DeviceCtx> devs_;
+  std::vector<Station*> station_ptrs_;
+
+  // worker coordination
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::condition_variable cv_done_;
+  uint64_t generation_ = 0;
+  int workers_done_ = 0;
+  bool shutdown_ = false;
+  Job* job_ = nullptr;
+};
+
+}  // namespace tr

@@ -1,0 +1,372 @@
+// K1 tile GEMM and K2 split/convert for sm_100a.  See tile_gemm.h for the contract.
+//
+// Kernel anatomy (one CTA per 128 x 256 output block, 352 threads):
+//   warp 0       TMA producer  (one elected lane; STAGES-deep smem ring, mbarrier full/empty)
+//   warp 1       MMA issuer    (one lane issues tcgen05.mma; commits free smem stages)
+//   warp 2       TMEM allocator (512 columns = two 128 x 256 fp32 partial-sum buffers)
+//   warps 3..10  epilogue      (every seg_kb k-blocks: tcgen05.ld TMEM -> fp32 registers,
+//                               round-to-nearest add; at the end: registers -> global)
+// All k-steps of a task (each a separate tile-cache slot, i.e. a different TMA
+// dim-2 coordinate) stream through the same ring; C is written exactly once.
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+
+#include "sm100_ptx.cuh"
+#include "tile_gemm.h"
+
+namespace tr {
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BN = 256;
+constexpr int BK = 64;                    // bf16 elements = 128 B = one SW128 row
+constexpr int A_BYTES = BM * BK * 2;      // 16 KiB per plane
+constexpr int B_BYTES = BN * BK * 2;      // 32 KiB per plane
+constexpr int MN_GROUP_BYTES = 64 * BK * 2;  // one 64-wide MN-major TMA box (8 KiB)
+constexpr int EPI_WARP0 = 3;                 // warps 3..10: epilogue (2 per TMEM lane quadrant)
+constexpr int EPI_WARPS = 8;
+constexpr int NUM_THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
+constexpr int TMEM_COLS = 2 * BN;             // double-buffered 128 x 256 fp32 partial sums
+constexpr int SMEM_BUDGET = 227 * 1024;
+
+template <int PLANES>
+struct Cfg {
+  static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
+  static constexpr int STAGES = std::min(6, (SMEM_BUDGET - 2048) / STAGE_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <bool A_MN, bool B_K, int PLANES>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    tile_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ GemmArgs args) {
+  using C = Cfg<PLANES>;
+  constexpr int STAGES = C::STAGES;
+  constexpr int STAGE_BYTES = C::STAGE_BYTES;
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: partial sum ready in TMEM buffer b
+  uint64_t* acc_empty = acc_full + 2;   // [2] epilogue -> MMA: TMEM buffer b drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+
+  // total k-blocks and TMEM segments (identical on every role)
+  int total_kb = 0;
+  for (int ks = 0; ks < args.n_ksteps; ++ks) total_kb += (args.k_len[ks] + BK - 1) / BK;
+  const int seg_kb = args.seg_kb > 0 ? args.seg_kb : total_kb;
+  const int n_seg = (total_kb + seg_kb - 1) / seg_kb;
+
+  if (warp == 0 && lane == 0) {
+    ptx::tma_prefetch_desc(&tmA);
+    ptx::tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&acc_full[b], 1);
+      ptx::mbar_init(&acc_empty[b], EPI_WARPS);
+    }
+    ptx::fence_mbar_init();
+    ptx::fence_proxy_async();
+  }
+  if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int ks = 0; ks < args.n_ksteps; ++ks) {
+        const int nkb = (args.k_len[ks] + BK - 1) / BK;
+        const int az = args.a_z[ks];
+        const int bz = args.b_z[ks];
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sb = sa + PLANES * A_BYTES;
+          const int k0 = kb * BK;
+#pragma unroll
+          for (int p = 0; p < PLANES; ++p) {
+            if (!A_MN) {
+              ptx::tma_load_3d(sa + p * A_BYTES, &tmA, &full[stage], k0, m0, az + p);
+            } else {
+#pragma unroll
+              for (int g = 0; g < BM / 64; ++g)
+                ptx::tma_load_3d(sa + p * A_BYTES + g * MN_GROUP_BYTES, &tmA, &full[stage], m0 + 64 * g, k0,
+                                 az + p);
+            }
+            if (B_K) {
+              ptx::tma_load_3d(sb + p * B_BYTES, &tmB, &full[stage], k0, n0, bz + p);
+            } else {
+#pragma unroll
+              for (int g = 0; g < BN / 64; ++g)
+                ptx::tma_load_3d(sb + p * B_BYTES + g * MN_GROUP_BYTES, &tmB, &full[stage], n0 + 64 * g, k0,
+                                 bz + p);
+            }
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, !B_K);
+      int stage = 0;
+      uint32_t phase = 0;
+      int kb_in_seg = 0, seg = 0;
+      uint32_t tmem_d = tmem_base;
+      uint32_t accumulate = 0;
+      for (int ks = 0; ks < args.n_ksteps; ++ks) {
+        const int nkb = (args.k_len[ks] + BK - 1) / BK;
+        for (int kb = 0; kb < nkb; ++kb) {
+          if (kb_in_seg == 0) {
+            // new partial sum: wait until the epilogue drained this TMEM buffer
+            const int buf = seg & 1;
+            ptx::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+            ptx::tc_fence_after();
+            tmem_d = tmem_base + static_cast<uint32_t>(buf * BN);
+            accumulate = 0;
+          }
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t b_base = a_base + PLANES * A_BYTES;
+          // PLANES == 2: small cross terms first, then hi*hi.
+#pragma unroll
+          for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
+            const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
+            const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
+#pragma unroll
+            for (int k16 = 0; k16 < BK / 16; ++k16) {
+              const uint64_t adesc =
+                  A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024)
+                       : ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 32, 16, 1024);
+              const uint64_t bdesc =
+                  B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 32, 16, 1024)
+                      : ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024);
+              ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
+              accumulate = 1;
+            }
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+          if (++kb_in_seg == seg_kb) {
+            ptx::mma_commit(&acc_full[seg & 1]);
+            kb_in_seg = 0;
+            ++seg;
+          }
+        }
+      }
+      if (kb_in_seg != 0) ptx::mma_commit(&acc_full[seg & 1]);
+    }
+  } else if (warp >= EPI_WARP0) {
+    // ---------------- epilogue: TMEM partial sums -> fp32 registers (RNE) -> global
+    const int q = warp & 3;                      // TMEM lane quadrant this warp may access
+    const int half = (warp - EPI_WARP0) >> 2;    // column half of the 256-wide tile
+    const int row = q * 32 + lane;
+    const uint32_t tlane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 128);
+    float acc[128];
+#pragma unroll
+    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+    for (int seg = 0; seg < n_seg; ++seg) {
+      const int buf = seg & 1;
+      ptx::mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+      ptx::tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        uint32_t r[16];
+        ptx::tmem_ld_32x32b_x16(tlane + static_cast<uint32_t>(buf * BN + c * 16), r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(r[j]);
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&acc_empty[buf]);
+    }
+    const int grow = m0 + row;
+    const int gcol0 = n0 + half * 128;
+    if (grow < args.m_valid && gcol0 < args.n_valid) {
+      const int ncols = min(128, args.n_valid - gcol0);
+      const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
+      const bool acc_mode = args.epilogue == EPI_ACCUMULATE;
+      if (args.c_f64) {
+        double* dst = static_cast<double*>(args.c) + off;
+#pragma unroll
+        for (int j = 0; j < 128; ++j)
+          if (j < ncols) dst[j] = acc_mode ? dst[j] + static_cast<double>(acc[j]) : static_cast<double>(acc[j]);
+      } else {
+        float* dst = static_cast<float*>(args.c) + off;
+        if (ncols == 128 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            float4 v = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+            if (acc_mode) {
+              const float4 o = d4[j];
+              v.x += o.x;
+              v.y += o.y;
+              v.z += o.z;
+              v.w += o.w;
+            }
+            d4[j] = v;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 128; ++j)
+            if (j < ncols) dst[j] = acc_mode ? dst[j] + acc[j] : acc[j];
+        }
+      }
+    }
+  }
+
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+template <bool A_MN, bool B_K, int PLANES>
+cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args,
+                           cudaStream_t stream) {
+  using C = Cfg<PLANES>;
+  static std::once_flag once;
+  static cudaError_t attr_err = cudaSuccess;
+  std::call_once(once, [] {
+    attr_err = cudaFuncSetAttribute(tile_gemm_kernel<A_MN, B_K, PLANES>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+  });
+  if (attr_err != cudaSuccess) return attr_err;
+  dim3 grid((args.m_valid + BM - 1) / BM, (args.n_valid + BN - 1) / BN);
+  tile_gemm_kernel<A_MN, B_K, PLANES><<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, args);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- K2 split/convert
+template <typename T>
+__global__ void split_convert_kernel(const T* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
+                                     uint16_t* __restrict__ dst, int64_t ld_dst, int64_t rows_cap,
+                                     int64_t plane_stride, int planes) {
+  const int64_t chunks_per_row = ld_dst / 8;
+  const int64_t total = rows_cap * chunks_per_row;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / chunks_per_row;
+    const int64_t c = (idx - r * chunks_per_row) * 8;
+    uint16_t hi[8], lo[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t cc = c + j;
+      const double v = (r < rows && cc < cols) ? static_cast<double>(src[r * ld_src + cc]) : 0.0;
+      const __nv_bfloat16 h = __float2bfloat16_rn(static_cast<float>(v));
+      const __nv_bfloat16 l = __float2bfloat16_rn(static_cast<float>(v - static_cast<double>(__bfloat162float(h))));
+      hi[j] = __bfloat16_as_ushort(h);
+      lo[j] = __bfloat16_as_ushort(l);
+    }
+    uint16_t* d = dst + r * ld_dst + c;
+    *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(hi);
+    if (planes == 2) *reinterpret_cast<uint4*>(d + plane_stride) = *reinterpret_cast<const uint4*>(lo);
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+}  // namespace
+
+int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box) {
+  auto fn = encode_fn();
+  if (!fn) return -1;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(g.cols), static_cast<cuuint64_t>(g.rows),
+                        static_cast<cuuint64_t>(g.nplanes)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(g.ld * 2), static_cast<cuuint64_t>(g.plane_stride * 2)};
+  cuuint32_t boxd[3] = {64, 128, 1};
+  if (box == BOX_MN64) boxd[1] = 64;
+  if (box == BOX_K256) boxd[1] = 256;
+  if (box == BOX_K64) boxd[1] = 64;
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, g.base, dims, strides, boxd, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
+}
+
+void gemm_boxes(bool a_mn, bool b_kmajor, BoxKind* box_a, BoxKind* box_b) {
+  *box_a = a_mn ? BOX_MN64 : BOX_K128;
+  *box_b = b_kmajor ? BOX_K256 : BOX_MN64;
+}
+
+cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
+                             bool b_kmajor, cudaStream_t stream) {
+  if (args.m_valid <= 0 || args.n_valid <= 0 || args.n_ksteps <= 0 || args.n_ksteps > kMaxKSteps)
+    return cudaErrorInvalidValue;
+  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (args.planes == 2 ? 1 : 0);
+  switch (variant) {
+    case 0: return launch_variant<false, false, 1>(tmA, tmB, args, stream);
+    case 1: return launch_variant<false, false, 2>(tmA, tmB, args, stream);
+    case 2: return launch_variant<false, true, 1>(tmA, tmB, args, stream);
+    case 3: return launch_variant<false, true, 2>(tmA, tmB, args, stream);
+    case 4: return launch_variant<true, false, 1>(tmA, tmB, args, stream);
+    case 5: return launch_variant<true, false, 2>(tmA, tmB, args, stream);
+    case 6: return launch_variant<true, true, 1>(tmA, tmB, args, stream);
+    default: return launch_variant<true, true, 2>(tmA, tmB, args, stream);
+  }
+}
+
+cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols,
+                                 uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,
+                                 int planes, cudaStream_t stream) {
+  if (ld_dst % 8 != 0 || plane_stride % 8 != 0) return cudaErrorInvalidValue;
+  const int64_t total = rows_cap * (ld_dst / 8);
+  const int threads = 256;
+  int64_t blocks = (total + threads - 1) / threads;
+  blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
+  if (src_f64)
+    split_convert_kernel<double><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+        static_cast<const double*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, plane_stride, planes);
+  else
+    split_convert_kernel<float><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
+        static_cast<const float*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, plane_stride, planes);
+  return cudaGetLastError();
+}
+
+}  // namespace tr

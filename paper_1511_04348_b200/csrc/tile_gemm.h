@@ -1,0 +1,80 @@
+// K1: the per-task tile GEMM  C[i,j] (+)= sum_k A[i,k] . B[k,j]  on sm_100a.
+//
+// Replaces the reference's per-k-step numpy kernel
+//   tiles.py:154-179  accumulate_product  (called per k-step, scheduler.py:393-404)
+// with ONE launch per task (or per chunk of k-steps when the tile cache is too
+// small to pin all of a task's inputs).  The k-loop runs inside the kernel and the
+// accumulator stays in TMEM across every k-step, so C is written exactly once.
+//
+// Operands are read by TMA out of tile-cache slots ("planes" of bf16).  In the
+// FP32-accurate mode every fp32/f64 tile was split once at admission (K2,
+// convert.cu) into hi = bf16(x) and lo = bf16(x - hi); each 64-wide k-block then
+// issues three MMAs  hi*lo + lo*hi + hi*hi  into the same fp32 accumulator.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace tr {
+
+constexpr int kMaxKSteps = 64;  // k-steps per launch; longer tasks are chunked (accumulate=1)
+
+enum Epilogue : int32_t {
+  EPI_STORE = 0,        // C = acc
+  EPI_ACCUMULATE = 1,   // C += acc
+};
+
+struct GemmArgs {
+  int32_t m_valid;               // output rows actually stored
+  int32_t n_valid;               // output cols actually stored
+  int32_t n_ksteps;              // number of k-steps in this launch
+  int32_t planes;                // 1 = bf16, 2 = hi/lo split (fp32-accurate)
+  int32_t a_z[kMaxKSteps];       // TMA dim-2 index of A's hi plane per k-step (lo = +1)
+  int32_t b_z[kMaxKSteps];       // same for B
+  int32_t k_len[kMaxKSteps];     // contraction extent of each k-step
+  void* c;                       // output (row-major, ldc elements)
+  int64_t ldc;
+  int32_t c_f64;                 // 0: float32 output, 1: float64 output
+  int32_t epilogue;              // Epilogue
+  int32_t seg_kb;                // k-blocks (of 64) per TMEM partial sum; see below
+};
+
+// Accumulation-precision note (measured on B200, tools/probe_accum.py): the
+// tcgen05 fp32 accumulator rounds toward zero, so a long K accumulated in TMEM
+// drifts linearly in K (-1e-4 relative at K=32768).  The kernel therefore
+// accumulates at most `seg_kb` k-blocks in TMEM, then the epilogue warps add
+// the partial sum into fp32 registers with round-to-nearest (double-buffered
+// TMEM, so the tensor pipe never waits).  FP32-accurate mode uses seg_kb = 4.
+constexpr int kSegKbFp32Acc = 4;
+
+// Geometry of a 3-D bf16 tensor map: dim0 = columns (contiguous), dim1 = rows,
+// dim2 = plane index.  Used for both tile-cache slabs and dense matrices.
+struct PlaneGeom {
+  void* base;
+  int64_t cols, rows, nplanes;
+  int64_t ld;            // elements between rows
+  int64_t plane_stride;  // elements between planes
+};
+
+// Box shapes the kernel family needs; one tensor map per (geometry, box).
+enum BoxKind : int32_t { BOX_K128 = 0, BOX_MN64 = 1, BOX_K256 = 2, BOX_K64 = 3 };
+
+// Encodes a tensor map for `g` with the given box; returns 0 on success.
+int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box);
+
+// Launches the tile GEMM.  a_mn: A stored K x M (transposed operand, MN-major);
+// b_kmajor: B stored N x K (transposed operand, K-major).
+// tmA/tmB must have been made with the boxes reported by gemm_boxes().
+cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
+                             bool b_kmajor, cudaStream_t stream);
+void gemm_boxes(bool a_mn, bool b_kmajor, BoxKind* box_a, BoxKind* box_b);
+
+// K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
+// into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything
+// outside the valid region so ragged tiles contribute nothing in K.
+cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols,
+                                 uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,
+                                 int planes, cudaStream_t stream);
+
+}  // namespace tr

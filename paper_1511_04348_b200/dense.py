@@ -1,0 +1,44 @@
+"""Dense in-core product on one GPU: one K1 launch over whole device matrices.
+
+This is the B200 counterpart of the reference's ``DenseBackend`` product
+(ann.py:62-75 -> tiles.py:197-212 ``reference_gemm``): no tiling, no
+scheduler, no tile cache.  The paper's "in-core GPU" comparison point.
+"""
+
+from __future__ import annotations
+
+from . import _native as N
+from .matrix import describe, is_device_tensor
+
+PRECISIONS = {"bf16": N.TR_PREC_BF16, "fp32acc": N.TR_PREC_FP32ACC}
+
+
+def precision_code(p) -> int:
+    if isinstance(p, int):
+        return p
+    try:
+        return PRECISIONS[p]
+    except KeyError:
+        raise ValueError(f"unknown precision {p!r}; expected one of {sorted(PRECISIONS)}") from None
+
+
+def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,
+               stream=None):
+    """``out (+)= op(a) @ op(b)`` for torch CUDA tensors (float32/float64).
+
+    Launches the sm_100a tile kernel directly on ``stream`` (default: torch's
+    current stream).  Returns ``out``.
+    """
+    import torch
+
+    if not (is_device_tensor(a) and is_device_tensor(b)):
+        raise ValueError("dense_gemm takes CUDA tensors")
+    m = a.shape[1] if transpose_a else a.shape[0]
+    n = b.shape[0] if transpose_b else b.shape[1]
+    if out is None:
+        out = torch.zeros((m, n), dtype=a.dtype, device=a.device)
+    if stream is None:
+        stream = torch.cuda.current_stream(a.device)
+    N.call("tr_dense_gemm", describe(a), int(transpose_a), describe(b), int(transpose_b), describe(out),
+           precision_code(precision), int(accumulate), stream.cuda_stream)
+    return out

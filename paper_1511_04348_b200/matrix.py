@@ -1,0 +1,72 @@
+"""Matrix descriptors for the C ABI and pinned host buffers.
+
+Host matrices are numpy arrays (the reference's type, tiles.py:37-44); device
+matrices are torch CUDA tensors.  torch is used here only as the allocator of
+device memory and page-locked host memory.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as N
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def is_device_tensor(x) -> bool:
+    t = type(x)
+    return t.__module__.startswith("torch") and getattr(x, "is_cuda", False)
+
+
+def dtype_code(dt) -> int:
+    s = str(dt)
+    if s in ("float32", "torch.float32"):
+        return N.TR_DTYPE_F32
+    if s in ("float64", "torch.float64"):
+        return N.TR_DTYPE_F64
+    raise ValueError(f"unsupported element dtype {dt} (float32 / float64 only)")
+
+
+def describe(x) -> N.MatrixC:
+    """MatrixC for a 2-D row-major numpy array (host) or torch CUDA tensor (device)."""
+    if is_device_tensor(x):
+        if x.dim() != 2:
+            raise ValueError(f"expected a 2-D matrix, got shape {tuple(x.shape)}")
+        if x.stride(1) != 1 or x.stride(0) < max(1, x.shape[1]):
+            raise ValueError("device matrix must be row-major with unit column stride")
+        return N.MatrixC(x.data_ptr(), x.shape[0], x.shape[1], x.stride(0), dtype_code(x.dtype), N.TR_LOC_DEVICE)
+    a = np.asarray(x)
+    if a.ndim != 2:
+        raise ValueError(f"expected a 2-D matrix, got shape {a.shape}")
+    if not a.flags.c_contiguous:
+        raise ValueError("host matrix must be C-contiguous")
+    return N.MatrixC(a.ctypes.data, a.shape[0], a.shape[1], max(a.shape[1], 1), dtype_code(a.dtype), N.TR_LOC_HOST)
+
+
+def pinned_empty(shape, dtype=np.float32) -> np.ndarray:
+    """A numpy array backed by page-locked host memory (cudaHostAlloc via torch).
+
+    The array keeps the owning tensor alive through its ``base``.
+    """
+    torch = _torch()
+    tdt = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}[np.dtype(dtype)]
+    t = torch.empty(tuple(shape), dtype=tdt, pin_memory=True)
+    return t.numpy()
+
+
+def pinned_zeros(shape, dtype=np.float32) -> np.ndarray:
+    a = pinned_empty(shape, dtype)
+    a.fill(0)
+    return a
+
+
+def host_pinning_available() -> bool:
+    try:
+        return N.cuda_device_count() > 0
+    except Exception:
+        return False

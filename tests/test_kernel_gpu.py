@@ -1,0 +1,74 @@
+"""K1 tile kernel (tcgen05/TMEM/TMA) vs a float64 torch reference.
+
+Replaces the reference's per-tile numpy kernel (tiles.py:154-179); numerics
+are checked with the north-star tolerances (relative Frobenius error <= 1e-5
+for the FP32-accurate split-bf16 mode, <= 1e-2 for bf16) on zero-mean normal
+inputs, and bit-exactly on small-integer inputs (exact in bf16 and fp32).
+"""
+
+import pytest
+import torch
+
+from paper_1511_04348_b200 import dense_gemm
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32acc": 1e-5, "bf16": 1e-2}
+
+
+def rel_fro(c, ref):
+    return float(torch.linalg.norm(c.double() - ref) / torch.linalg.norm(ref))
+
+
+def make(m, k, n, ta, tb, dtype, gen, kind="normal"):
+    def mk(r, c):
+        if kind == "int":
+            return torch.randint(-4, 5, (r, c), generator=gen, dtype=torch.int64).to(dtype)
+        return torch.randn((r, c), generator=gen, dtype=torch.float64).to(dtype)
+
+    a = mk(k, m) if ta else mk(m, k)
+    b = mk(n, k) if tb else mk(k, n)
+    return a.cuda(), b.cuda()
+
+
+def ref_product(a, b, ta, tb):
+    a64, b64 = a.double(), b.double()
+    return (a64.T if ta else a64) @ (b64.T if tb else b64)
+
+
+SHAPES = [(128, 256, 64), (1, 1, 1), (5, 7, 3), (200, 300, 130), (257, 513, 1000), (1024, 768, 4096)]
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_dense_kernel_normal(shape, ta, tb, precision):
+    m, n, k = shape
+    gen = torch.Generator().manual_seed(hash((shape, ta, tb)) & 0xFFFF)
+    a, b = make(m, k, n, ta, tb, torch.float32, gen)
+    c = dense_gemm(a, b, ta, tb, precision=precision)
+    torch.cuda.synchronize()
+    err = rel_fro(c, ref_product(a, b, ta, tb))
+    assert err <= TOL[precision], f"{shape} ta={ta} tb={tb} {precision}: rel err {err:.3e}"
+
+
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
+def test_dense_kernel_integers_exact(ta, tb):
+    gen = torch.Generator().manual_seed(7)
+    for (m, n, k) in [(33, 65, 17), (300, 260, 700)]:
+        a, b = make(m, k, n, ta, tb, torch.float64, gen, kind="int")
+        for precision in ("bf16", "fp32acc"):
+            c = dense_gemm(a, b, ta, tb, precision=precision)
+            torch.cuda.synchronize()
+            assert torch.equal(c, ref_product(a, b, ta, tb)), precision
+
+
+def test_dense_kernel_accumulate_and_f64_out():
+    gen = torch.Generator().manual_seed(3)
+    a, b = make(130, 70, 300, False, False, torch.float64, gen)
+    c0 = torch.randn((130, 300), dtype=torch.float64, generator=gen).cuda()
+    c = c0.clone()
+    dense_gemm(a, b, out=c, accumulate=True)
+    torch.cuda.synchronize()
+    ref = c0 + ref_product(a, b, False, False)
+    assert rel_fro(c, ref) <= 1e-5
