@@ -1,0 +1,519 @@
+"""Planning, reservation stations, the GPU session (Runtime) and run reports.
+
+Python face of the native runtime (csrc/session.cpp), API-compatible with the
+reference scheduler (pkg/src/tilerun/scheduler.py):
+
+* ``plan`` builds one task per output tile with row-major ids and every task
+  enqueued up front (scheduler.py:165-197).
+* ``Runtime(machine, tile_size, ...)`` is a session whose tile cache and uid
+  identities persist across ``multiply`` calls (scheduler.py:522-612).  Each
+  product runs on one pinned C++ worker thread per logical device; a device's
+  reservation-station entries feed its CUDA streams; each task is ONE
+  tcgen05 GEMM launch over all its k-steps with inputs resolved L1 (own HBM)
+  -> L2 (peer HBM over NVLink) -> host (pinned DRAM).
+* ``mode``: "gpu" (default) and "threaded" (its alias: one real worker thread
+  per device) run on B200s; "dryrun" runs the scheduler and directory only
+  (no CUDA, result is None) for schedule-parity tests.  The reference's
+  discrete-event "sim" engine is not part of the hardware build.
+"""
+
+from __future__ import annotations
+
+import csv
+import ctypes as C
+import json
+import threading
+import time
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _native as N
+from .coherence import CacheDirectory, CacheStats, UidTable
+from .dense import precision_code
+from .devices import Machine
+from .matrix import describe, is_device_tensor, pinned_zeros
+from .msqueue import MichaelScottQueue
+from .tiles import TiledMatrix, TileKey, decode_task, partition
+
+SCHEMA_VERSION = 1
+MODES = ("gpu", "threaded", "dryrun")
+
+
+class TaskState(Enum):
+    QUEUED = "queued"
+    RESERVED = "reserved"
+    RUNNING = "running"
+    DONE = "done"
+
+
+@dataclass
+class Task:
+    task_id: int
+    row: int
+    col: int
+    k_steps: int
+    state: TaskState = TaskState.QUEUED
+
+
+class Completion:
+    """Exactly-once bitmap; a second mark raises (scheduler.py:70-96).
+
+    The native runtime keeps the same bitmap with an atomic exchange per task;
+    its snapshot is copied here after every product.
+    """
+
+    def __init__(self, n_tasks: int):
+        self._done = [False] * n_tasks
+        self._count = 0
+        self._lock = threading.Lock()
+
+    def mark(self, task_id: int) -> None:
+        with self._lock:
+            if self._done[task_id]:
+                raise RuntimeError(f"task {task_id} executed twice")
+            self._done[task_id] = True
+            self._count += 1
+
+    def all_done(self) -> bool:
+        with self._lock:
+            return self._count == len(self._done)
+
+    @property
+    def done_count(self) -> int:
+        with self._lock:
+            return self._count
+
+    def snapshot(self) -> list[bool]:
+        with self._lock:
+            return list(self._done)
+
+
+@dataclass
+class Operand:
+    """A tiled matrix as seen by the planner, optionally transposed (scheduler.py:99-138).
+
+    Tile (i, k) of the transposed operand is stored tile (k, i); the cache key
+    names STORED coordinates so both readings share tile identity.  On the
+    GPU the transposition is a TMA/UMMA layout choice (MN-major operand), never
+    a copy.
+    """
+
+    tiled: TiledMatrix
+    uid: str
+    transposed: bool = False
+
+    @property
+    def grid_rows(self) -> int:
+        return self.tiled.grid_cols if self.transposed else self.tiled.grid_rows
+
+    @property
+    def grid_cols(self) -> int:
+        return self.tiled.grid_rows if self.transposed else self.tiled.grid_cols
+
+    @property
+    def element_shape(self) -> tuple[int, int]:
+        r, c = self.tiled.shape
+        return (c, r) if self.transposed else (r, c)
+
+    def tile_view(self, i: int, j: int):
+        return self.tiled.tile(j, i).T if self.transposed else self.tiled.tile(i, j)
+
+    def key(self, i: int, j: int) -> TileKey:
+        return TileKey(self.uid, j, i) if self.transposed else TileKey(self.uid, i, j)
+
+    def tile_nbytes(self, i: int, j: int, element_bytes: int) -> int:
+        r, c = self.tiled.tile_shape(j, i) if self.transposed else self.tiled.tile_shape(i, j)
+        return r * c * element_bytes
+
+
+def _as_operand(x, uid: str) -> Operand:
+    return x if isinstance(x, Operand) else Operand(x, uid)
+
+
+@dataclass
+class Plan:
+    a: Operand
+    b: Operand
+    c: Operand
+    tile_size: int
+    grid_rows: int
+    grid_cols: int
+    k_steps: int
+    tasks: list[Task]
+    queue: MichaelScottQueue
+    completion: Completion
+
+    @property
+    def total_tasks(self) -> int:
+        return len(self.tasks)
+
+
+def _zeros_like_output(a: Operand, rows: int, cols: int, pinned: bool):
+    base = a.tiled.base
+    if is_device_tensor(base):
+        import torch
+
+        return torch.zeros((rows, cols), dtype=base.dtype, device=base.device)
+    dt = np.asarray(base).dtype
+    if pinned and dt in (np.float32, np.float64):
+        return pinned_zeros((rows, cols), dt)
+    return np.zeros((rows, cols), dtype=dt)
+
+
+def plan(a, b, a_uid: str = "A", b_uid: str = "B", c_uid: str = "C", *, _pinned_output: bool = False) -> Plan:
+    """One task per output tile, all enqueued row-major (scheduler.py:165-197)."""
+    a = _as_operand(a, a_uid)
+    b = _as_operand(b, b_uid)
+    if a.tiled.tile_size != b.tiled.tile_size:
+        raise ValueError(f"tile sizes differ: {a.tiled.tile_size} vs {b.tiled.tile_size}")
+    am, ak = a.element_shape
+    bk, bn = b.element_shape
+    if ak != bk:
+        raise ValueError(f"inner dimensions differ: {a.element_shape} x {b.element_shape}")
+    t = a.tiled.tile_size
+    c = Operand(partition(_zeros_like_output(a, am, bn, _pinned_output), t), c_uid)
+    gr, gc = c.grid_rows, c.grid_cols
+    k_steps = a.grid_cols
+    queue = MichaelScottQueue()
+    tasks = []
+    for tid in range(gr * gc):
+        i, j = decode_task(tid, gc, gr)
+        tasks.append(Task(tid, i, j, k_steps))
+        queue.enqueue(tid)
+    return Plan(a=a, b=b, c=c, tile_size=t, grid_rows=gr, grid_cols=gc, k_steps=k_steps, tasks=tasks, queue=queue,
+                completion=Completion(len(tasks)))
+
+
+# ----------------------------------------------------------------- stations
+
+
+class ReservationStation:
+    """Fixed-width buffer of reserved task ids (scheduler.py:200-236), native.
+
+    The owner pops the front, a thief the back; one lock per station.
+    """
+
+    def __init__(self, owner: int, width: int):
+        self.owner = owner
+        self.width = width
+        h = C.c_void_p()
+        N.call("tr_station_create", int(owner), int(width), C.byref(h))
+        self._h = h
+        self._buf = (N.u64 * max(1, width))()
+        self._held: dict = {}  # native handle -> the reserved value
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None:
+            N.lib.tr_station_destroy(self._h)
+            self._h = None
+
+    def refill(self, queue: MichaelScottQueue) -> list:
+        """Pull from the global queue until full; returns the values taken."""
+        # The native station stores queue handles; translate back to the objects.
+        n = N.i32()
+        N.call("tr_station_refill", self._h, queue.handle, self._buf, self.width, C.byref(n))
+        pulled = []
+        for i in range(n.value):
+            hid = int(self._buf[i])
+            val = queue._objs.pop(hid)
+            self._held[hid] = val
+            pulled.append(val)
+        return pulled
+
+    def _one(self, fn) -> object | None:
+        v, got = N.u64(), N.i32()
+        N.call(fn, self._h, C.byref(v), C.byref(got))
+        return self._held.pop(int(v.value)) if got.value else None
+
+    def pop_for_run(self):
+        return self._one("tr_station_pop_for_run")
+
+    def try_steal(self):
+        return self._one("tr_station_try_steal")
+
+    def reserved_count(self) -> int:
+        n = N.i32()
+        N.call("tr_station_reserved_count", self._h, C.byref(n))
+        return n.value
+
+
+def steal_task(thief: int, stations: dict) -> tuple:
+    """Steal one reserved task from the most-loaded peer, ties to the lowest id
+    (scheduler.py:239-249).  Returns (task_id, victim) or (None, None)."""
+    ids = sorted(stations)
+    arr = (C.c_void_p * len(ids))(*[stations[d]._h.value for d in ids])
+    v, victim, got = N.u64(), N.i32(), N.i32()
+    N.call("tr_steal_task", int(thief), arr, len(ids), C.byref(v), C.byref(victim), C.byref(got))
+    if not got.value:
+        return None, None
+    return stations[victim.value]._held.pop(int(v.value)), victim.value
+
+
+# ----------------------------------------------------------------- stats
+
+
+@dataclass
+class StealEvent:
+    thief: int
+    victim: int
+    task_id: int
+    queue_empty_observed: bool = True
+    time: float | None = None
+
+
+@dataclass
+class DeviceStats:
+    device_id: int
+    kind: str
+    tasks_completed: int = 0
+    steals_performed: int = 0
+    steals_suffered: int = 0
+
+
+@dataclass
+class RunStats:
+    """Per-product report (scheduler.py:270-325) plus GPU measurements."""
+
+    mode: str
+    tile_size: int
+    grid_rows: int
+    grid_cols: int
+    k_steps: int
+    total_tasks: int
+    steal_enabled: bool
+    coherence_enabled: bool
+    seed: int | None
+    devices: dict[int, DeviceStats]
+    cache: CacheStats
+    cache_per_device: dict[int, CacheStats]
+    makespan: float | None
+    wall_elapsed: float
+    steal_events: list[StealEvent] = field(default_factory=list)
+    precision: str = "fp32acc"
+    gpu_launches: int = 0
+    kernel_ms: dict[int, float] = field(default_factory=dict)
+
+    @property
+    def tasks_by_device(self) -> dict[int, int]:
+        return {d: s.tasks_completed for d, s in self.devices.items()}
+
+    def to_report_dict(self) -> dict:
+        return {
+            "schema_version": SCHEMA_VERSION,
+            "mode": self.mode,
+            "tile_size": self.tile_size,
+            "grid": {"rows": self.grid_rows, "cols": self.grid_cols, "k_steps": self.k_steps},
+            "total_tasks": self.total_tasks,
+            "steal": self.steal_enabled,
+            "coherence": self.coherence_enabled,
+            "seed": self.seed,
+            "makespan": self.makespan,
+            "wall_elapsed": self.wall_elapsed,
+            "steals": len(self.steal_events),
+            "devices": [
+                {"device_id": s.device_id, "kind": s.kind, "tasks_completed": s.tasks_completed,
+                 "steals_performed": s.steals_performed, "steals_suffered": s.steals_suffered}
+                for s in self.devices.values()
+            ],
+            "cache": {**self.cache.as_dict(),
+                      "per_device": {str(d): s.as_dict() for d, s in self.cache_per_device.items()}},
+            "gpu": {"precision": self.precision, "launches": self.gpu_launches,
+                    "kernel_ms": {str(d): v for d, v in self.kernel_ms.items()}},
+        }
+
+
+def write_report_json(stats: RunStats, path) -> None:
+    with open(path, "w") as f:
+        json.dump(stats.to_report_dict(), f, indent=2)
+        f.write("\n")
+
+
+_CSV_FIELDS = ["device_id", "kind", "tasks_completed", "steals_performed", "steals_suffered", "l1_hits", "l2_hits",
+               "host_fetches", "bytes_host", "bytes_peer", "evictions", "writebacks", "bytes_writeback"]
+
+
+def write_report_csv(stats: RunStats, path) -> None:
+    """One row per device plus a total row (scheduler.py:341-361)."""
+    with open(path, "w", newline="") as f:
+        w = csv.DictWriter(f, fieldnames=_CSV_FIELDS)
+        w.writeheader()
+        for did, ds in sorted(stats.devices.items()):
+            cs = stats.cache_per_device.get(did, CacheStats())
+            w.writerow({"device_id": did, "kind": ds.kind, "tasks_completed": ds.tasks_completed,
+                        "steals_performed": ds.steals_performed, "steals_suffered": ds.steals_suffered,
+                        **{k: v for k, v in cs.as_dict().items() if k in _CSV_FIELDS}})
+        w.writerow({"device_id": "total", "kind": "",
+                    "tasks_completed": sum(d.tasks_completed for d in stats.devices.values()),
+                    "steals_performed": sum(d.steals_performed for d in stats.devices.values()),
+                    "steals_suffered": sum(d.steals_suffered for d in stats.devices.values()),
+                    **{k: v for k, v in stats.cache.as_dict().items() if k in _CSV_FIELDS}})
+
+
+# ----------------------------------------------------------------- the session
+
+
+def _host_matrix(x):
+    """Host operand as a C-contiguous float32/float64 array (ints widen to f64)."""
+    a = np.asarray(x)
+    if a.dtype not in (np.float32, np.float64):
+        a = a.astype(np.float64)
+    return np.ascontiguousarray(a)
+
+
+class Runtime:
+    """A session: one machine, one HBM tile cache, any number of products.
+
+    Signature follows scheduler.py:531-533, plus ``precision`` ("fp32acc" |
+    "bf16") and ``hbm_budget_bytes`` (per GPU; 0 = 80% of free HBM).
+    """
+
+    def __init__(self, machine: Machine, tile_size: int, mode: str = "gpu", steal: bool = True,
+                 coherence: bool = True, seed: int | None = None, directory_debug: bool = False,
+                 precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru"):
+        if mode not in MODES:
+            if mode == "sim":
+                raise ValueError("mode 'sim' is the reference's simulated engine; the B200 runtime executes on "
+                                 "hardware: use mode='gpu' (or 'threaded'), or 'dryrun' for schedule-only runs")
+            raise ValueError(f"unknown mode {mode!r}")
+        if tile_size < 1:
+            raise ValueError(f"tile_size must be >= 1, got {tile_size}")
+        self.machine = machine
+        self.tile_size = tile_size
+        self.mode = mode
+        self.steal = steal
+        self.coherence = coherence
+        self.seed = seed
+        self.precision = precision
+        flags = (N.TR_FLAG_STEAL if steal else 0) | (N.TR_FLAG_COHERENCE if coherence else 0)
+        flags |= N.TR_FLAG_DEBUG if directory_debug else 0
+        flags |= N.TR_FLAG_DRYRUN if mode == "dryrun" else 0
+        flags |= N.TR_FLAG_FIFO if policy == "fifo" else 0
+        mc, keep = machine._as_c()
+        h = C.c_void_p()
+        N.call("tr_session_create", C.byref(mc), int(tile_size), precision_code(precision), flags,
+               int(hbm_budget_bytes), C.byref(h))
+        self._h = h
+        self._uids = UidTable()
+        dh = C.c_void_p()
+        N.call("tr_session_directory", h, C.byref(dh))
+        self.directory = CacheDirectory(machine, enabled=coherence, policy=policy, debug=directory_debug,
+                                        _native_handle=dh, _uids=self._uids, _owner=self)
+        self._uid_n = 0
+        self._lock = threading.Lock()  # one product at a time per session
+
+    def close(self) -> None:
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib.tr_session_destroy(h)
+        self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def fresh_uid(self, prefix: str = "m") -> str:
+        self._uid_n += 1
+        return f"{prefix}#{self._uid_n}"
+
+    def sim_now(self) -> float:
+        """No simulated clocks on hardware: always 0.0 (scheduler.py:552-553)."""
+        return 0.0
+
+    def operand(self, m, uid: str | None = None, transposed: bool = False) -> Operand:
+        tiled = m if isinstance(m, TiledMatrix) else partition(m, self.tile_size)
+        return Operand(tiled, uid or self.fresh_uid(), transposed)
+
+    def multiply(self, a, b, transpose_a: bool = False, transpose_b: bool = False, a_uid: str | None = None,
+                 b_uid: str | None = None, c_uid: str | None = None, *, out=None, task_offset: int = 0,
+                 task_stride: int = 1):
+        """Full scheduled product; returns ``(result, RunStats)`` (scheduler.py:559-612).
+
+        Host operands (numpy) are read tile by tile from (pinned) host memory;
+        CUDA-tensor operands are read from HBM.  The result lives where A lives.
+        ``task_offset``/``task_stride`` run only the tasks t with
+        t % stride == offset (static multi-process sharding).
+        """
+        if (isinstance(a, Operand) and transpose_a) or (isinstance(b, Operand) and transpose_b):
+            raise ValueError("transposition of an Operand is fixed at construction")
+        a_op = a if isinstance(a, Operand) else self.operand(self._prep(a), a_uid, transpose_a)
+        b_op = b if isinstance(b, Operand) else self.operand(self._prep(b), b_uid, transpose_b)
+        if a_op.tiled.tile_size != b_op.tiled.tile_size or a_op.tiled.tile_size != self.tile_size:
+            raise ValueError(f"tile sizes differ: {a_op.tiled.tile_size} vs {b_op.tiled.tile_size}")
+        am, ak = a_op.element_shape
+        bk, bn = b_op.element_shape
+        if ak != bk:
+            raise ValueError(f"inner dimensions differ: {a_op.element_shape} x {b_op.element_shape}")
+        c_uid = c_uid or self.fresh_uid("c")
+        dry = self.mode == "dryrun"
+        if out is None:
+            out = None if dry else _zeros_like_output(a_op, am, bn, pinned=True)
+        n = self.machine.n_devices
+        rep = N.GemmReportC()
+        per_cache = (N.CacheStatsC * n)()
+        per_dev = (N.DeviceStatsC * n)()
+        total = -(-am // self.tile_size) * -(-bn // self.tile_size)
+        steals = (N.StealEventC * max(1, total))()
+        completion = (N.u8 * max(1, total))()
+        rep.cache_per_device, rep.devices = per_cache, per_dev
+        rep.steals, rep.steals_cap = steals, total
+        rep.completion, rep.completion_cap = completion, total
+        ma = self._desc(a_op.tiled.base, dry)
+        mb = self._desc(b_op.tiled.base, dry)
+        mc = self._desc(out, dry, shape=(am, bn), dtype=a_op.tiled.base.dtype)
+        with self._lock:
+            N.call("tr_gemm_shard", self._h, C.byref(ma), self._uids.id(a_op.uid), int(a_op.transposed), C.byref(mb),
+                   self._uids.id(b_op.uid), int(b_op.transposed), C.byref(mc), self._uids.id(c_uid),
+                   int(task_offset), int(task_stride), C.byref(rep))
+            kms = (N.f64 * n)()
+            N.call("tr_session_kernel_ms", self._h, kms)
+        done = [bool(completion[t]) for t in range(total)]
+        want = [t % task_stride == task_offset for t in range(total)]
+        if done != want:
+            raise RuntimeError(f"run incomplete: {sum(done)}/{sum(want)} tasks")
+        stats = RunStats(
+            mode=self.mode, tile_size=self.tile_size, grid_rows=int(rep.grid_rows), grid_cols=int(rep.grid_cols),
+            k_steps=int(rep.k_steps), total_tasks=int(rep.total_tasks), steal_enabled=self.steal,
+            coherence_enabled=self.coherence, seed=self.seed,
+            devices={d: DeviceStats(d, self.machine.devices[d].kind, int(per_dev[d].tasks_completed),
+                                    int(per_dev[d].steals_performed), int(per_dev[d].steals_suffered))
+                     for d in range(n)},
+            cache=CacheStats.from_c(rep.cache),
+            cache_per_device={d: CacheStats.from_c(per_cache[d]) for d in range(n)},
+            makespan=None, wall_elapsed=float(rep.wall_seconds),
+            steal_events=[StealEvent(int(steals[i].thief), int(steals[i].victim), int(steals[i].task_id), True)
+                          for i in range(min(int(rep.n_steals), total))],
+            precision=self.precision, gpu_launches=int(rep.gpu_launches),
+            kernel_ms={d: float(kms[d]) for d in range(n)},
+        )
+        return out, stats
+
+    @staticmethod
+    def _prep(x):
+        return x if is_device_tensor(x) else _host_matrix(x)
+
+    @staticmethod
+    def _desc(x, dry, shape=None, dtype=None) -> N.MatrixC:
+        if x is None:  # dry run: shape-only descriptor
+            from .matrix import dtype_code
+
+            r, c = shape
+            return N.MatrixC(None, r, c, c, dtype_code(dtype), N.TR_LOC_HOST)
+        return describe(x)
+
+
+def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool = True, coherence: bool = True,
+        seed: int | None = None, directory_debug: bool = False, precision: str = "fp32acc"):
+    """One-shot product through a fresh session with uids "A","B","C" (scheduler.py:615-621)."""
+    rt = Runtime(machine, tile_size, mode=mode, steal=steal, coherence=coherence, seed=seed,
+                 directory_debug=directory_debug, precision=precision)
+    try:
+        return rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C")
+    finally:
+        rt.close()

@@ -1,0 +1,86 @@
+"""The C-ABI boundary: the in-tree library loads on any host and exports every
+function include/tilerun_b200.h declares; config objects round-trip."""
+
+import ctypes
+import json
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import paper_1511_04348_b200 as tr
+from paper_1511_04348_b200 import _native as N
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_functions():
+    text = (ROOT / "include" / "tilerun_b200.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\**\s+\**(tr_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_runtime_surface():
+    names = declared_functions()
+    for must in ("tr_gemm", "tr_session_create", "tr_queue_dequeue", "tr_dir_acquire_input", "tr_steal_task",
+                 "tr_dense_gemm", "tr_last_error"):
+        assert must in names
+    assert len(names) >= 35
+
+
+def test_library_exports_every_declared_symbol():
+    lib = ctypes.CDLL(str(N._LIB_PATH))
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_every_declared_symbol_has_a_python_prototype():
+    protos = set(N._PROTOS) | {"tr_last_error", "tr_abi_version"}
+    assert set(declared_functions()) <= protos
+
+
+def test_abi_version_and_error_channel():
+    assert N.ABI_VERSION == 1
+    h = ctypes.c_void_p()
+    st = N.lib.tr_station_create(0, 0, ctypes.byref(h))  # width 0 is a config error
+    assert st == N.TR_ERR_CONFIG
+    assert b"width" in N.lib.tr_last_error()
+
+
+def test_no_gpu_means_loud_failure_not_fallback():
+    if N.cuda_device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(tr.NoDeviceError):
+        tr.Runtime(tr.homogeneous_machine(1), 4)
+
+
+def test_machine_config_roundtrip(tmp_path):
+    m = tr.Machine([tr.DeviceSpec(0, capacity_tiles=5, slots=2, gpu=0), tr.DeviceSpec(1, flops_per_unit=3.0)],
+                   tr.ProximityMatrix([[0, 2], [2, 0]], [[0, 5.0], [5.0, 0]]), dtype=np.float32)
+    tr.save_machine(tmp_path / "m.json", m)
+    m2 = tr.load_machine(tmp_path / "m.json")
+    assert m2.to_dict() == m.to_dict() and m2.element_bytes == 4
+    assert json.loads((tmp_path / "m.json").read_text())["devices"][0]["gpu"] == 0
+
+
+@pytest.mark.parametrize("bad", [
+    dict(device_id=-1), dict(device_id=0, kind="fpga"), dict(device_id=0, capacity_tiles=2),
+    dict(device_id=0, slots=0), dict(device_id=0, kind="host-worker", capacity_tiles=4),
+])
+def test_device_spec_validation(bad):
+    with pytest.raises(tr.ConfigError):
+        tr.DeviceSpec(**bad)
+
+
+def test_proximity_and_machine_validation():
+    with pytest.raises(tr.ConfigError):
+        tr.ProximityMatrix([[0, 1], [2, 0]], np.ones((2, 2)))
+    with pytest.raises(tr.ConfigError):
+        tr.Machine([tr.DeviceSpec(1)], tr.ProximityMatrix.uniform(1))
+    with pytest.raises(tr.ConfigError):
+        tr.Machine.from_dict({"nodevices": []})
+    m = tr.homogeneous_machine(3)
+    assert tr.closest_owner(0, {1, 2}, m.proximity) == 1
+    assert tr.compute_cost(m.device(0), (2, 3), (3, 4)) == 2 * 2 * 3 * 4 / 1000.0
+    assert tr.transfer_cost(m, tr.HOST, 0, 8192) == 1.0

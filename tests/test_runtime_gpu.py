@@ -1,0 +1,175 @@
+"""The scheduled GPU product (tr_gemm through Runtime/run) against the oracle
+and the reference's golden runs.
+
+Tolerances (north star): integer-valued inputs are exact (they are exactly
+representable in bf16 and the sums in fp32); float inputs <= 1e-5 relative
+Frobenius error in the fp32-accurate mode, <= 1e-2 in bf16 mode.
+"""
+
+import json
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tilerun_oracle as O
+from paper_1511_04348_b200 import DeviceSpec, Machine, ProximityMatrix, Runtime, homogeneous_machine, run
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+TOL = {"fp32acc": 1e-5, "bf16": 1e-2}
+
+
+def rel(c, ref):
+    ref = np.asarray(ref, np.float64)
+    den = np.linalg.norm(ref)
+    return float(np.linalg.norm(np.asarray(c, np.float64) - ref) / (den if den else 1.0))
+
+
+def int_matrix(rng, r, c):
+    return rng.integers(-4, 5, size=(r, c)).astype(np.float64)
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return json.loads((G / "runs.json").read_text()), np.load(G / "runs.npz")
+
+
+def test_golden_runs(golden):
+    meta, arr = golden
+    for name, m in meta.items():
+        if name in ("session_reuse", "transpose"):
+            continue
+        a, b, cref = arr[name + "_a"], arr[name + "_b"], arr[name + "_c"]
+        c, s = run(homogeneous_machine(m["devices"], capacity_tiles=m["capacity"]), a, b, m["tile"],
+                   coherence=m["coherence"], directory_debug=True)
+        if m["kind"] == "int":
+            assert np.array_equal(c, cref), name
+        else:
+            assert rel(c, cref) <= TOL["fp32acc"], (name, rel(c, cref))
+        assert c.dtype == cref.dtype
+        ref_cache = m["stats"]["cache"]
+        assert s.total_tasks == m["stats"]["total_tasks"] == sum(s.tasks_by_device.values())
+        assert s.cache.input_requests == ref_cache["l1_hits"] + ref_cache["l2_hits"] + ref_cache["host_fetches"]
+        assert s.cache.writebacks == ref_cache["writebacks"]
+        if m["devices"] == 1:
+            assert s.cache.as_dict() == ref_cache, name  # deterministic one-device schedule
+        elif m["capacity"] is None:
+            assert s.cache.host_fetches == ref_cache["host_fetches"], name
+        assert s.gpu_launches > 0
+
+
+def test_session_reuse_and_transpose(golden):
+    meta, arr = golden
+    a, b = arr["session_reuse_a"], arr["session_reuse_b"]
+    rt = Runtime(homogeneous_machine(1), 4)
+    c1, s1 = rt.multiply(a, b, a_uid="X", b_uid="W")
+    c2, s2 = rt.multiply(a, b, a_uid="X", b_uid="W")
+    assert s1.cache.as_dict() == meta["session_reuse"]["first"]["cache"]
+    assert s2.cache.as_dict() == meta["session_reuse"]["second"]["cache"]
+    assert np.array_equal(c1, O.reference_gemm(a, b)) and np.array_equal(c1, c2)
+    x, w, y = arr["transpose_x"], arr["transpose_w"], arr["transpose_y"]
+    rt = Runtime(homogeneous_machine(1), 4)
+    rt.multiply(x, w, a_uid="X", b_uid="W")
+    before = rt.directory.stats()
+    c, _ = rt.multiply(x, y, transpose_a=True, a_uid="X", b_uid="Y2")
+    assert rt.directory.stats().host_fetches - before.host_fetches == meta["transpose"]["host_fetch_delta"]
+    assert rel(c, arr["transpose_c"]) <= 1e-5
+
+
+def test_c1_randomized_cases():
+    """Acceptance C1 (reference test_acceptance.py:56-92), checked against the oracle."""
+    rng = np.random.default_rng(20240601)
+    dim_hi = {1: 24, 7: 256, 16: 512, 64: 512}
+    for case in range(30):
+        t = int(rng.choice([1, 7, 16, 64]))
+        m, k, n = (int(rng.integers(1, dim_hi[t] + 1)) for _ in range(3))
+        ndev = int(rng.choice([1, 2, 4]))
+        kind = "int" if case % 2 else "float"
+        if kind == "int":
+            a, b = int_matrix(rng, m, k), int_matrix(rng, k, n)
+        else:
+            a, b = rng.uniform(0.0, 1.0, size=(m, k)), rng.uniform(0.0, 1.0, size=(k, n))
+        c, s = run(homogeneous_machine(ndev), a, b, t)
+        ref = O.c_oracle().gemm(a, b)
+        label = f"{m}x{k}x{n} T={t} dev={ndev} {kind}"
+        if kind == "int":
+            assert np.array_equal(c, ref), label
+        else:
+            assert rel(c, ref) <= 1e-5, label
+        assert sum(s.tasks_by_device.values()) == s.total_tasks
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
+def test_transposed_operands_normal_data(precision, ta, tb):
+    rng = np.random.default_rng(3)
+    m, k, n, t = 300, 520, 270, 128
+    a = rng.standard_normal((k, m) if ta else (m, k))
+    b = rng.standard_normal((n, k) if tb else (k, n))
+    rt = Runtime(homogeneous_machine(2), t, precision=precision)
+    c, s = rt.multiply(a, b, transpose_a=ta, transpose_b=tb)
+    ref = O.reference_gemm(a.T if ta else a, b.T if tb else b)
+    assert rel(c, ref) <= TOL[precision]
+
+
+def test_float32_machine_and_device_resident_operands():
+    rng = np.random.default_rng(4)
+    a = rng.standard_normal((700, 900)).astype(np.float32)
+    b = rng.standard_normal((900, 500)).astype(np.float32)
+    m = homogeneous_machine(2, dtype=np.float32)
+    c_host, s = run(m, a, b, 256)
+    assert c_host.dtype == np.float32
+    assert s.cache.bytes_host == (700 * 900 + 900 * 500) * 4  # each distinct tile crosses PCIe once
+    ref = O.c_oracle().gemm(a.astype(np.float64), b.astype(np.float64))
+    assert rel(c_host, ref) <= 1e-5
+    rt = Runtime(m, 256)
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c_dev, _ = rt.multiply(ta, tb)
+    assert c_dev.is_cuda and c_dev.dtype == torch.float32
+    assert np.array_equal(c_dev.cpu().numpy(), c_host)  # same tiles, same kernel, same order
+
+
+def test_capacity_three_exact_with_evictions():
+    rng = np.random.default_rng(8)
+    a, b = int_matrix(rng, 40, 40), int_matrix(rng, 40, 40)
+    c, s = run(homogeneous_machine(2, capacity_tiles=3), a, b, 5, directory_debug=True)
+    assert np.array_equal(c, O.reference_gemm(a, b))
+    assert s.cache.evictions > 0 and s.cache.input_requests == 2 * s.total_tasks * s.k_steps
+
+
+def test_exactly_once_threaded_stress():
+    rng = np.random.default_rng(7)
+    for _ in range(20):
+        t, g = int(rng.integers(3, 6)), int(rng.integers(2, 5))
+        ndev = int(rng.integers(2, 5))
+        a, b = int_matrix(rng, t * g, t * g), int_matrix(rng, t * g, t * g)
+        c, s = run(homogeneous_machine(ndev), a, b, t, directory_debug=True)
+        assert np.array_equal(c, O.reference_gemm(a, b))
+        assert sum(s.tasks_by_device.values()) == s.total_tasks == g * g
+
+
+def test_peer_hits_and_heterogeneous_slots():
+    rng = np.random.default_rng(9)
+    a, b = int_matrix(rng, 96, 96), int_matrix(rng, 96, 96)
+    devs = [DeviceSpec(0, slots=1), DeviceSpec(1, slots=4), DeviceSpec(2, slots=2)]
+    m = Machine(devs, ProximityMatrix.uniform(3))
+    c, s = run(m, a, b, 16)
+    assert np.array_equal(c, O.reference_gemm(a, b))
+    assert s.cache.host_fetches == 2 * 6 * 6 and s.cache.l2_hits > 0
+    assert s.cache.bytes_peer == s.cache.l2_hits * 16 * 16 * 8
+
+
+def test_bypass_mode_counts_and_result():
+    rng = np.random.default_rng(10)
+    a, b = int_matrix(rng, 24, 24), int_matrix(rng, 24, 24)
+    c, s = run(homogeneous_machine(2), a, b, 4, coherence=False)
+    assert np.array_equal(c, O.reference_gemm(a, b)) and s.cache.host_fetches == 2 * 6 ** 3
+
+
+def test_reports_kernel_time():
+    rng = np.random.default_rng(11)
+    a, b = rng.standard_normal((1024, 1024)), rng.standard_normal((1024, 1024))
+    _, s = run(homogeneous_machine(1), a, b, 512)
+    assert s.kernel_ms[0] > 0 and s.wall_elapsed > 0
