@@ -214,6 +214,13 @@ int tr_gemm_shard(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t tra
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
  * measured with CUDA events on the launching streams (sum over launches). */
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms /* n_devices */);
+/* Device-side span (ms) of the last tr_gemm on each device: CUDA events recorded
+ * before the first and after the last operation of every worker stream. */
+int tr_session_span_ms(tr_session* s, double* per_device_ms /* n_devices */);
+/* Tasks a device keeps executing concurrently (default min(2, slots)); the rest
+ * of its reservation-station entries stay reserved (stealable).  1 serialises
+ * a device's tasks, which the roofline measurement uses. */
+int tr_session_set_inflight(tr_session* s, int32_t max_inflight);
 
 /* ------------------------------- dense in-core product (ann.py:62-75 DenseBackend)
  * One K1 launch over whole matrices on the current CUDA device, no scheduler and

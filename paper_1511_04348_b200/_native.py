@@ -112,6 +112,8 @@ _PROTOS = {
     "tr_gemm_shard": [vp, P(MatrixC), u64, i32, P(MatrixC), u64, i32, P(MatrixC), u64, i64, i64,
                       P(GemmReportC)],
     "tr_session_kernel_ms": [vp, P(f64)],
+    "tr_session_span_ms": [vp, P(f64)],
+    "tr_session_set_inflight": [vp, i32],
     "tr_dense_gemm": [P(MatrixC), i32, P(MatrixC), i32, P(MatrixC), i32, i32, vp],
 }
 

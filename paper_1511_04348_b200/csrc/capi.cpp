@@ -313,6 +313,15 @@ int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t ta, const
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms) {
   return guarded([&] { s->s->kernel_ms(per_device_ms); });
 }
+int tr_session_span_ms(tr_session* s, double* per_device_ms) {
+  return guarded([&] { s->s->span_ms(per_device_ms); });
+}
+int tr_session_set_inflight(tr_session* s, int32_t max_inflight) {
+  return guarded([&] {
+    if (max_inflight < 1) tr::fail(TR_ERR_VALUE, "max_inflight must be >= 1");
+    s->s->set_inflight(max_inflight);
+  });
+}
 
 // ---- dense in-core product
 int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb, const tr_matrix* c,

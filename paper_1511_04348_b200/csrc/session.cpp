@@ -120,6 +120,8 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
       dc.max_slots = static_cast<int32_t>(slots);
       dc.streams.resize(dc.width);
+      TR_CUDA(cudaEventCreate(&dc.span_start));
+      TR_CUDA(cudaEventCreate(&dc.span_end));
       for (auto& sc : dc.streams) {
         TR_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
         for (auto& ev : sc.ring) TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -174,6 +176,8 @@ Session::~Session() {
       cudaEventDestroy(t.end);
     }
     if (dc.slab) cudaFree(dc.slab);
+    cudaEventDestroy(dc.span_start);
+    cudaEventDestroy(dc.span_end);
   }
 }
 
@@ -629,6 +633,15 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   }
   const tr_cache_stats before = dir_->stats();
   const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();
+  if (!dryrun_) {
+    // device-side span of the product: every stream starts after span_start,
+    // span_end is recorded after every stream's last operation
+    for (auto& dc : devs_) {
+      TR_CUDA(cudaSetDevice(dc.gpu));
+      TR_CUDA(cudaEventRecord(dc.span_start, dc.streams[0].stream));
+      for (int s = 1; s < dc.width; ++s) TR_CUDA(cudaStreamWaitEvent(dc.streams[s].stream, dc.span_start, 0));
+    }
+  }
   const auto t0 = std::chrono::steady_clock::now();
   {
     std::lock_guard<std::mutex> lk(mu_);
@@ -645,6 +658,11 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   if (!dryrun_) {
     for (auto& dc : devs_) {
       cudaSetDevice(dc.gpu);
+      for (int s = 1; s < dc.width; ++s) {
+        cudaEvent_t ev = record(dc.id, s);
+        cudaStreamWaitEvent(dc.streams[0].stream, ev, 0);
+      }
+      cudaEventRecord(dc.span_end, dc.streams[0].stream);
       for (auto& sc : dc.streams) {
         cudaError_t e = cudaStreamSynchronize(sc.stream);
         if (e != cudaSuccess) job.set_error(TR_ERR_CUDA, std::string("stream sync: ") + cudaGetErrorString(e));
@@ -662,8 +680,12 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
       else cudaGetLastError();
       dc.timed_pool.push_back(tl);
     }
+    dc.last_launches = static_cast<int64_t>(dc.timed.size());
     dc.timed.clear();
     dc.last_kernel_ms = ms;
+    float span = 0;
+    if (!dryrun_ && cudaEventElapsedTime(&span, dc.span_start, dc.span_end) != cudaSuccess) cudaGetLastError();
+    dc.last_span_ms = span;
   }
   if (job.err_status) throw Error(job.err_status, job.err_msg);
   if (!job.all_done())
@@ -689,6 +711,14 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
       for (int64_t t = 0; t < std::min<int64_t>(rep->completion_cap, total); ++t)
         rep->completion[t] = job.done[static_cast<size_t>(t)].load();
   }
+}
+
+void Session::span_ms(double* out) const {
+  for (int d = 0; d < static_cast<int>(devs_.size()); ++d) out[d] = devs_[d].last_span_ms;
+}
+
+void Session::set_inflight(int n) {
+  for (auto& dc : devs_) dc.max_inflight = std::max(1, std::min(n, dc.width));
 }
 
 void Session::kernel_ms(double* out) const {

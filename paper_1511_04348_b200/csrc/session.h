@@ -82,6 +82,8 @@ class Session {
   void gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t b_uid, bool tb, const Mat& c,
             uint64_t c_uid, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep);
   void kernel_ms(double* out) const;
+  void span_ms(double* out) const;
+  void set_inflight(int n);
 
  private:
   static constexpr int kRing = 64;
@@ -117,6 +119,9 @@ class Session {
     tr_device_stats stats{};
     std::vector<TimedLaunch> timed, timed_pool;
     double last_kernel_ms = 0;
+    int64_t last_launches = 0;
+    double last_span_ms = 0;
+    cudaEvent_t span_start = nullptr, span_end = nullptr;
     std::thread worker;
   };
 

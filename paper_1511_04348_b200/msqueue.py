@@ -13,8 +13,11 @@ from __future__ import annotations
 
 import ctypes as C
 import itertools
+import threading
 
 from . import _native as N
+
+_tls = threading.local()
 
 
 class MichaelScottQueue:
@@ -38,13 +41,21 @@ class MichaelScottQueue:
             raise ValueError("None is the empty sentinel and cannot be enqueued")
         hid = next(self._ids)
         self._objs[hid] = value  # published before the handle becomes visible
-        N.check(self._enq(self._h, hid))
+        st = self._enq(self._h, hid)
+        if st:
+            N.check(st)
 
     def dequeue(self):
         """Pop the oldest value, or None when the queue is empty."""
-        v = N.u64()
-        got = N.i32()
-        N.check(self._deq(self._h, C.byref(v), C.byref(got)))
+        tl = _tls.__dict__
+        bufs = tl.get("bufs")
+        if bufs is None:  # per-thread out-parameters, created once
+            v, got = N.u64(), N.i32()
+            bufs = tl["bufs"] = (v, got, C.byref(v), C.byref(got))
+        v, got, pv, pgot = bufs
+        st = self._deq(self._h, pv, pgot)
+        if st:
+            N.check(st)
         if not got.value:
             return None
         return self._objs.pop(v.value)

@@ -33,7 +33,7 @@ from . import _native as N
 from .coherence import CacheDirectory, CacheStats, UidTable
 from .dense import precision_code
 from .devices import Machine
-from .matrix import describe, is_device_tensor, pinned_zeros
+from .matrix import describe, is_device_tensor, pinned_empty, pinned_zeros
 from .msqueue import MichaelScottQueue
 from .tiles import TiledMatrix, TileKey, decode_task, partition
 
@@ -150,15 +150,18 @@ class Plan:
         return len(self.tasks)
 
 
-def _zeros_like_output(a: Operand, rows: int, cols: int, pinned: bool):
+def _zeros_like_output(a: Operand, rows: int, cols: int, pinned: bool, zero: bool = True):
+    """Output storage where A lives.  The runtime overwrites every element
+    (first k-chunk stores, later chunks accumulate), so it skips zeroing."""
     base = a.tiled.base
     if is_device_tensor(base):
         import torch
 
-        return torch.zeros((rows, cols), dtype=base.dtype, device=base.device)
+        alloc = torch.zeros if zero else torch.empty
+        return alloc((rows, cols), dtype=base.dtype, device=base.device)
     dt = np.asarray(base).dtype
     if pinned and dt in (np.float32, np.float64):
-        return pinned_zeros((rows, cols), dt)
+        return pinned_zeros((rows, cols), dt) if zero else pinned_empty((rows, cols), dt)
     return np.zeros((rows, cols), dtype=dt)
 
 
@@ -293,7 +296,8 @@ class RunStats:
     steal_events: list[StealEvent] = field(default_factory=list)
     precision: str = "fp32acc"
     gpu_launches: int = 0
-    kernel_ms: dict[int, float] = field(default_factory=dict)
+    kernel_ms: dict[int, float] = field(default_factory=dict)  # sum of tile-GEMM kernel durations
+    span_ms: dict[int, float] = field(default_factory=dict)  # device-side span of the product
 
     @property
     def tasks_by_device(self) -> dict[int, int]:
@@ -418,6 +422,10 @@ class Runtime:
     def __exit__(self, *exc):
         self.close()
 
+    def set_inflight(self, max_inflight: int) -> None:
+        """Tasks each device executes concurrently (default 2; 1 serialises)."""
+        N.call("tr_session_set_inflight", self._h, int(max_inflight))
+
     def fresh_uid(self, prefix: str = "m") -> str:
         self._uid_n += 1
         return f"{prefix}#{self._uid_n}"
@@ -453,7 +461,7 @@ class Runtime:
         c_uid = c_uid or self.fresh_uid("c")
         dry = self.mode == "dryrun"
         if out is None:
-            out = None if dry else _zeros_like_output(a_op, am, bn, pinned=True)
+            out = None if dry else _zeros_like_output(a_op, am, bn, pinned=True, zero=False)
         n = self.machine.n_devices
         rep = N.GemmReportC()
         per_cache = (N.CacheStatsC * n)()
@@ -473,6 +481,8 @@ class Runtime:
                    int(task_offset), int(task_stride), C.byref(rep))
             kms = (N.f64 * n)()
             N.call("tr_session_kernel_ms", self._h, kms)
+            span = (N.f64 * n)()
+            N.call("tr_session_span_ms", self._h, span)
         done = [bool(completion[t]) for t in range(total)]
         want = [t % task_stride == task_offset for t in range(total)]
         if done != want:
@@ -491,6 +501,7 @@ class Runtime:
                           for i in range(min(int(rep.n_steals), total))],
             precision=self.precision, gpu_launches=int(rep.gpu_launches),
             kernel_ms={d: float(kms[d]) for d in range(n)},
+            span_ms={d: float(span[d]) for d in range(n)},
         )
         return out, stats
 
