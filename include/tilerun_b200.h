@@ -221,6 +221,15 @@ int tr_session_span_ms(tr_session* s, double* per_device_ms /* n_devices */);
  * of its reservation-station entries stay reserved (stealable).  1 serialises
  * a device's tasks, which the roofline measurement uses. */
 int tr_session_set_inflight(tr_session* s, int32_t max_inflight);
+/* Order in which tr_gemm enqueues task ids: 0 = row-major (the reference's,
+ * scheduler.py:189-192), 1 = banded (pairs of task rows walked column by
+ * column: first-touch host traffic spread over the run), -1 = auto (default:
+ * banded unless some device has a bounded capacity, where LRU eviction
+ * sequences -- and so the counters -- depend on the order). */
+int tr_session_set_order(tr_session* s, int32_t order);
+/* Sessions return HBM slabs/staging buffers to a process-wide cache reused by
+ * later sessions; this frees every cached block. */
+int tr_release_cached_memory(void);
 
 /* ------------------------------- dense in-core product (ann.py:62-75 DenseBackend)
  * One K1 launch over whole matrices on the current CUDA device, no scheduler and
@@ -228,6 +237,32 @@ int tr_session_set_inflight(tr_session* s, int32_t max_inflight);
  * is a cudaStream_t (NULL = legacy default stream). */
 int tr_dense_gemm(const tr_matrix* a, int32_t transpose_a, const tr_matrix* b, int32_t transpose_b,
                   const tr_matrix* c, int32_t precision, int32_t accumulate, void* stream);
+
+/* ------------------------------ MLP elementwise kernels (ann.py:30-56,151-248)
+ * Device float32 arrays, launched on `stream` (cudaStream_t).  These replace the
+ * reference's host float64 numpy steps around the products. */
+typedef enum { TR_ACT_IDENTITY = 0, TR_ACT_SIGMOID = 1, TR_ACT_RELU = 2 } tr_activation; /* ann.py:27 */
+/* y += bias (per column; bias may be NULL); a = act(y)      ann.py:155-158 */
+int tr_mlp_bias_act(float* y, float* a, const float* bias, int64_t rows, int64_t cols, int32_t act, void* stream);
+/* dy = dout * act'(y, a)                                     ann.py:222, 40-48 */
+int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a, int64_t n, int32_t act,
+                    void* stream);
+/* dout = 2 (pred - target) / n; *loss_sum (device double) = sum (pred - target)^2   ann.py:51-56 */
+int tr_mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
+                    void* stream);
+/* out[c] = sum_r m[r, c]                                     ann.py:173 */
+int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream);
+/* w -= lr * g                                                ann.py:243-247 */
+int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
+
+/* Order every product of the session after the work already queued on `stream`
+ * (cudaStream_t, e.g. the caller's framework stream); NULL clears it. */
+int tr_session_set_external_stream(tr_session* s, void* stream);
+
+/* Kernel variant switch (process-wide): 1 = CTA pairs (tcgen05 cta_group::2,
+ * 256 x 256 per pair) for tiles taller than 128 rows, 0 = single CTAs
+ * (128 x 256, default).  Also settable with TR_GEMM_PAIRS=1 in the environment. */
+int tr_set_gemm_pairs(int32_t on);
 
 #ifdef __cplusplus
 }

@@ -114,7 +114,16 @@ _PROTOS = {
     "tr_session_kernel_ms": [vp, P(f64)],
     "tr_session_span_ms": [vp, P(f64)],
     "tr_session_set_inflight": [vp, i32],
+    "tr_session_set_order": [vp, i32],
+    "tr_release_cached_memory": [],
     "tr_dense_gemm": [P(MatrixC), i32, P(MatrixC), i32, P(MatrixC), i32, i32, vp],
+    "tr_set_gemm_pairs": [i32],
+    "tr_mlp_bias_act": [vp, vp, vp, i64, i64, i32, vp],
+    "tr_mlp_act_grad": [vp, vp, vp, vp, i64, i32, vp],
+    "tr_mlp_mse_grad": [vp, vp, vp, i64, vp, vp],
+    "tr_mlp_colsum": [vp, i64, i64, vp, vp],
+    "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
+    "tr_session_set_external_stream": [vp, vp],
 }
 
 

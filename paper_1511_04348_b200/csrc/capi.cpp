@@ -6,7 +6,9 @@
 #include <vector>
 
 #include "common.h"
+#include "devpool.h"
 #include "directory.h"
+#include "mlp_kernels.h"
 #include "msqueue.h"
 #include "session.h"
 #include "station.h"
@@ -356,7 +358,7 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     pack(A, &pa, &ga);
     pack(B, &pb, &gb);
     tr::BoxKind ba, bb;
-    tr::gemm_boxes(ta != 0, tb != 0, &ba, &bb);
+    tr::gemm_boxes(ta != 0, tb != 0, static_cast<int>(M), &ba, &bb);
     CUtensorMap tma, tmb;
     if (tr::make_plane_tmap(&tma, ga, ba) || tr::make_plane_tmap(&tmb, gb, bb))
       tr::fail(TR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -378,6 +380,40 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     TR_CUDA(cudaFreeAsync(pa, st));
     TR_CUDA(cudaFreeAsync(pb, st));
   });
+}
+
+int tr_session_set_order(tr_session* s, int32_t order) {
+  return guarded([&] {
+    if (order < -1 || order > 1) tr::fail(TR_ERR_VALUE, "order must be -1 (auto), 0 (row-major) or 1 (banded)");
+    s->s->set_order(order);
+  });
+}
+int tr_release_cached_memory(void) {
+  return guarded([&] { tr::DevPool::get().trim(); });
+}
+int tr_mlp_bias_act(float* y, float* a, const float* bias, int64_t rows, int64_t cols, int32_t act, void* stream) {
+  return guarded([&] { TR_CUDA(tr::mlp_bias_act(y, a, bias, rows, cols, act, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a, int64_t n, int32_t act,
+                    void* stream) {
+  return guarded([&] { TR_CUDA(tr::mlp_act_grad(dy, dout, y, a, n, act, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
+                    void* stream) {
+  return guarded(
+      [&] { TR_CUDA(tr::mlp_mse_grad(dout, pred, target, n, loss_sum, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream) {
+  return guarded([&] { TR_CUDA(tr::mlp_colsum(m, rows, cols, out, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
+  return guarded([&] { TR_CUDA(tr::mlp_sgd(w, g, n, lr, static_cast<cudaStream_t>(stream))); });
+}
+int tr_session_set_external_stream(tr_session* s, void* stream) {
+  return guarded([&] { s->s->set_external_stream(static_cast<cudaStream_t>(stream)); });
+}
+int tr_set_gemm_pairs(int32_t on) {
+  return guarded([&] { tr::set_gemm_pairs(on != 0); });
 }
 
 }  // extern "C"

@@ -109,7 +109,8 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       TR_CUDA(cudaSetDevice(dc.gpu));
       size_t free_b = 0, total_b = 0;
       TR_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      int64_t budget = hbm_budget_ > 0 ? hbm_budget_ : static_cast<int64_t>(0.8 * static_cast<double>(free_b));
+      const double reusable = static_cast<double>(free_b) + static_cast<double>(DevPool::get().cached_bytes());
+      int64_t budget = hbm_budget_ > 0 ? hbm_budget_ : static_cast<int64_t>(0.8 * reusable);
       budget /= per_gpu[dc.gpu];
       const int64_t tile_bytes = static_cast<int64_t>(tile) * tile * 8;
       const int64_t slot_bytes = slot_elems_ * 2;
@@ -126,8 +127,8 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
         TR_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
         for (auto& ev : sc.ring) TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
-        TR_CUDA(cudaMalloc(&sc.staging, tile_bytes));
-        TR_CUDA(cudaMalloc(&sc.outbuf, tile_bytes));
+        TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
+        TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
       }
     }
     // Peer access between every pair of distinct GPUs in use (NVLink / NVSwitch).
@@ -163,8 +164,8 @@ Session::~Session() {
     for (auto& sc : dc.streams) {
       for (auto& ev : sc.ring) cudaEventDestroy(ev);
       cudaEventDestroy(sc.done);
-      cudaFree(sc.staging);
-      cudaFree(sc.outbuf);
+      DevPool::get().release(dc.gpu, sc.staging, sc.staging_cap);
+      DevPool::get().release(dc.gpu, sc.outbuf, sc.outbuf_cap);
       cudaStreamDestroy(sc.stream);
     }
     for (auto& t : dc.timed) {
@@ -175,10 +176,11 @@ Session::~Session() {
       cudaEventDestroy(t.start);
       cudaEventDestroy(t.end);
     }
-    if (dc.slab) cudaFree(dc.slab);
+    DevPool::get().release(dc.gpu, dc.slab, dc.slab_cap);
     cudaEventDestroy(dc.span_start);
     cudaEventDestroy(dc.span_end);
   }
+  if (ext_ready_) cudaEventDestroy(ext_ready_);
 }
 
 // ---------------------------------------------------------------- HBM slab
@@ -206,11 +208,13 @@ void Session::ensure_slab(int d, int64_t needed) {
   TR_CUDA(cudaSetDevice(dc.gpu));
   TR_CUDA(cudaDeviceSynchronize());
   uint16_t* nb = nullptr;
-  cudaError_t e = cudaMalloc(&nb, static_cast<size_t>((grow + scratch) * slot_elems_ * 2));
+  size_t cap = 0;
+  cudaError_t e = DevPool::get().alloc(dc.gpu, static_cast<size_t>((grow + scratch) * slot_elems_ * 2),
+                                       reinterpret_cast<void**>(&nb), &cap);
   if (e != cudaSuccess && grow > target) {
-    cudaGetLastError();
     grow = target;
-    e = cudaMalloc(&nb, static_cast<size_t>((grow + scratch) * slot_elems_ * 2));
+    e = DevPool::get().alloc(dc.gpu, static_cast<size_t>((grow + scratch) * slot_elems_ * 2),
+                             reinterpret_cast<void**>(&nb), &cap);
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -220,8 +224,9 @@ void Session::ensure_slab(int d, int64_t needed) {
   if (dc.slab) {
     TR_CUDA(cudaMemcpy(nb, dc.slab, static_cast<size_t>((dc.slab_slots + scratch) * slot_elems_ * 2),
                        cudaMemcpyDeviceToDevice));
-    TR_CUDA(cudaFree(dc.slab));
+    DevPool::get().release(dc.gpu, dc.slab, dc.slab_cap);
   }
+  dc.slab_cap = cap;
   dc.slab = nb;
   dc.slab_slots = static_cast<int32_t>(grow);
   dc.slots.resize(static_cast<size_t>(grow + scratch));
@@ -398,7 +403,7 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     }
     if (!dryrun_) {
       BoxKind ba, bb;
-      gemm_boxes(job.ta, job.tb, &ba, &bb);
+      gemm_boxes(job.ta, job.tb, args.m_valid, &ba, &bb);
       TimedLaunch tl;
       if (!dc.timed_pool.empty()) {
         tl = dc.timed_pool.back();
@@ -600,10 +605,30 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   job.k_steps = ceil_div(K, T);
   job.task_offset = task_offset;
   job.task_stride = task_stride;
-  // plan(): every task enqueued up front, row-major (scheduler.py:189-192)
+  // plan(): every task enqueued up front (scheduler.py:189-192).  Row-major as in
+  // the reference, or -- when no device has a bounded capacity, so the hit/miss
+  // counters cannot depend on the order -- banded: rows taken two at a time and
+  // walked column by column, which spreads first-touch host traffic over the run
+  // (each new B tile serves two tasks immediately).
   const int64_t total = job.grid_rows * job.grid_cols;
+  bool banded = order_ == 1;
+  if (order_ < 0) {
+    banded = true;
+    for (auto& dc : devs_) banded = banded && dc.capacity < 0;
+  }
+  std::vector<int64_t> ids;
+  ids.reserve(static_cast<size_t>(total));
+  if (banded) {
+    const int64_t G = 2;
+    for (int64_t b = 0; b < job.grid_rows; b += G)
+      for (int64_t j = 0; j < job.grid_cols; ++j)
+        for (int64_t i = b; i < std::min(b + G, job.grid_rows); ++i) ids.push_back(i * job.grid_cols + j);
+  } else {
+    for (int64_t t = 0; t < total; ++t) ids.push_back(t);
+  }
   int64_t planned = 0;
-  for (int64_t t = task_offset; t < total; t += task_stride) {
+  for (int64_t t : ids) {
+    if (t % task_stride != task_offset) continue;
     job.queue.enqueue(static_cast<uint64_t>(t));
     ++planned;
   }
@@ -634,10 +659,16 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   const tr_cache_stats before = dir_->stats();
   const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();
   if (!dryrun_) {
+    if (ext_stream_) {
+      // inputs produced on the caller's stream (e.g. torch) must be complete first
+      if (!ext_ready_) TR_CUDA(cudaEventCreateWithFlags(&ext_ready_, cudaEventDisableTiming));
+      TR_CUDA(cudaEventRecord(ext_ready_, ext_stream_));
+    }
     // device-side span of the product: every stream starts after span_start,
     // span_end is recorded after every stream's last operation
     for (auto& dc : devs_) {
       TR_CUDA(cudaSetDevice(dc.gpu));
+      if (ext_stream_) TR_CUDA(cudaStreamWaitEvent(dc.streams[0].stream, ext_ready_, 0));
       TR_CUDA(cudaEventRecord(dc.span_start, dc.streams[0].stream));
       for (int s = 1; s < dc.width; ++s) TR_CUDA(cudaStreamWaitEvent(dc.streams[s].stream, dc.span_start, 0));
     }

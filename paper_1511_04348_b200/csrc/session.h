@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include "devpool.h"
 #include "directory.h"
 #include "msqueue.h"
 #include "station.h"
@@ -84,6 +85,8 @@ class Session {
   void kernel_ms(double* out) const;
   void span_ms(double* out) const;
   void set_inflight(int n);
+  void set_order(int order) { order_ = order; }
+  void set_external_stream(cudaStream_t s) { ext_stream_ = s; }
 
  private:
   static constexpr int kRing = 64;
@@ -102,6 +105,7 @@ class Session {
     uint64_t seq = 0;       // issue order
     void* staging = nullptr;  // host-tile landing zone (T*T*8 bytes)
     void* outbuf = nullptr;   // C tile for host outputs (T*T*8 bytes)
+    size_t staging_cap = 0, outbuf_cap = 0;
   };
   struct TimedLaunch {
     cudaEvent_t start, end;
@@ -110,6 +114,7 @@ class Session {
     int id = 0, gpu = 0, width = 4, max_inflight = 2;
     int64_t capacity = -1;
     uint16_t* slab = nullptr;
+    size_t slab_cap = 0;
     int32_t slab_slots = 0;  // directory slots allocated (physical = slab_slots + scratch)
     int32_t max_slots = 0;
     CUtensorMap tmap[4];
@@ -155,6 +160,9 @@ class Session {
   bool dryrun_, steal_, coherence_;
   int32_t element_bytes_;
   int64_t hbm_budget_;
+  int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, -1 auto
+  cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
+  cudaEvent_t ext_ready_ = nullptr;
   std::unique_ptr<Directory> dir_;
   std::vector<DeviceCtx> devs_;
   std::vector<Station*> station_ptrs_;

@@ -10,6 +10,8 @@
 // dim-2 coordinate) stream through the same ring; C is written exactly once.
 #include <algorithm>
 #include <cstdio>
+#include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 #include <cuda_bf16.h>
@@ -22,11 +24,10 @@ namespace tr {
 
 namespace {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
+constexpr int BM = 128;                   // output rows per CTA (TMEM lanes)
+constexpr int BN = 256;                   // output cols per CTA / per CTA pair
 constexpr int BK = 64;                    // bf16 elements = 128 B = one SW128 row
 constexpr int A_BYTES = BM * BK * 2;      // 16 KiB per plane
-constexpr int B_BYTES = BN * BK * 2;      // 32 KiB per plane
 constexpr int MN_GROUP_BYTES = 64 * BK * 2;  // one 64-wide MN-major TMA box (8 KiB)
 constexpr int EPI_WARP0 = 3;                 // warps 3..10: epilogue (2 per TMEM lane quadrant)
 constexpr int EPI_WARPS = 8;
@@ -34,20 +35,30 @@ constexpr int NUM_THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;             // double-buffered 128 x 256 fp32 partial sums
 constexpr int SMEM_BUDGET = 227 * 1024;
 
-template <int PLANES>
+// CG = 1: one CTA computes 128 x 256 with tcgen05 cta_group::1.
+// CG = 2: a CTA pair (cluster of 2, one per SM of a TPC) computes 256 x 256 with
+//         cta_group::2: each CTA stages its 128 rows of A and 128 of the 256
+//         columns of B, the leader issues M=256 MMAs over both CTAs' smem, and
+//         each CTA's TMEM holds its 128 x 256 accumulator.  Per SM this halves
+//         the B bytes fetched and the smem bytes the tensor core reads.
+template <int PLANES, int CG>
 struct Cfg {
+  static constexpr int BN_LOCAL = BN / CG;                // B columns staged per CTA
+  static constexpr int B_BYTES = BN_LOCAL * BK * 2;       // per plane
   static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
   static constexpr int STAGES = std::min(6, (SMEM_BUDGET - 2048) / STAGE_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
-template <bool A_MN, bool B_K, int PLANES>
+template <bool A_MN, bool B_K, int PLANES, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tile_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmArgs args) {
-  using C = Cfg<PLANES>;
+  using C = Cfg<PLANES, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int STAGE_BYTES = C::STAGE_BYTES;
+  constexpr int B_BYTES = C::B_BYTES;
+  constexpr int BN_LOCAL = C::BN_LOCAL;
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -59,8 +70,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
+  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;  // 0 = leader of the pair
+  const bool leader = rank == 0;
+  const int m0 = (blockIdx.x / CG) * (BM * CG) + static_cast<int>(rank) * BM;
+  const int n0 = blockIdx.y * BN;                                   // output tile columns
+  const int nb0 = n0 + static_cast<int>(rank) * BN_LOCAL;           // B columns this CTA stages
 
   // total k-blocks and TMEM segments (identical on every role)
   int total_kb = 0;
@@ -79,20 +93,25 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&acc_full[b], 1);
-      ptx::mbar_init(&acc_empty[b], EPI_WARPS);
+      ptx::mbar_init(&acc_empty[b], EPI_WARPS * CG);
     }
     ptx::fence_mbar_init();
     ptx::fence_proxy_async();
   }
-  if (warp == 2) ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) {
+    if (CG == 2) ptx::tmem_alloc_cg2(tmem_slot, TMEM_COLS);
+    else ptx::tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // barrier inits + TMEM address visible pair-wide
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
+      // ---------------- TMA producer (both CTAs of a pair load their halves)
+      const uint32_t full0 = ptx::smem_u32(&full[0]);
       int stage = 0;
       uint32_t phase = 0;
       for (int ks = 0; ks < args.n_ksteps; ++ks) {
@@ -101,27 +120,30 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int bz = args.b_z[ks];
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + PLANES * A_BYTES;
           const int k0 = kb * BK;
+          // completion bytes of both CTAs go to the leader's full barrier
+          const uint32_t bar = (CG == 2) ? ptx::mapa_shared(full0 + stage * 8, 0) : 0u;
+          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE_BYTES);
+          auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1, int c2) {
+            if (CG == 2) ptx::tma_load_3d_cg2(dst, tm, bar, c0, c1, c2);
+            else ptx::tma_load_3d(dst, tm, &full[stage], c0, c1, c2);
+          };
 #pragma unroll
           for (int p = 0; p < PLANES; ++p) {
             if (!A_MN) {
-              ptx::tma_load_3d(sa + p * A_BYTES, &tmA, &full[stage], k0, m0, az + p);
+              load(sa + p * A_BYTES, &tmA, k0, m0, az + p);
             } else {
 #pragma unroll
-              for (int g = 0; g < BM / 64; ++g)
-                ptx::tma_load_3d(sa + p * A_BYTES + g * MN_GROUP_BYTES, &tmA, &full[stage], m0 + 64 * g, k0,
-                                 az + p);
+              for (int g = 0; g < BM / 64; ++g) load(sa + p * A_BYTES + g * MN_GROUP_BYTES, &tmA, m0 + 64 * g, k0, az + p);
             }
             if (B_K) {
-              ptx::tma_load_3d(sb + p * B_BYTES, &tmB, &full[stage], k0, n0, bz + p);
+              load(sb + p * B_BYTES, &tmB, k0, nb0, bz + p);
             } else {
 #pragma unroll
-              for (int g = 0; g < BN / 64; ++g)
-                ptx::tma_load_3d(sb + p * B_BYTES + g * MN_GROUP_BYTES, &tmB, &full[stage], n0 + 64 * g, k0,
-                                 bz + p);
+              for (int g = 0; g < BN_LOCAL / 64; ++g)
+                load(sb + p * B_BYTES + g * MN_GROUP_BYTES, &tmB, nb0 + 64 * g, k0, bz + p);
             }
           }
           if (++stage == STAGES) {
@@ -132,9 +154,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM, BN, A_MN, !B_K);
+    if (lane == 0 && leader) {
+      // ---------------- MMA issuer (the pair's leader issues for both CTAs)
+      constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, BN, A_MN, !B_K);
       int stage = 0;
       uint32_t phase = 0;
       int kb_in_seg = 0, seg = 0;
@@ -144,7 +166,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int nkb = (args.k_len[ks] + BK - 1) / BK;
         for (int kb = 0; kb < nkb; ++kb) {
           if (kb_in_seg == 0) {
-            // new partial sum: wait until the epilogue drained this TMEM buffer
+            // new partial sum: wait until the epilogue(s) drained this TMEM buffer
             const int buf = seg & 1;
             ptx::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
             ptx::tc_fence_after();
@@ -168,23 +190,29 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               const uint64_t bdesc =
                   B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 32, 16, 1024)
                       : ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024);
-              ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
+              if (CG == 2) ptx::mma_bf16_cg2(tmem_d, adesc, bdesc, idesc, accumulate);
+              else ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
               accumulate = 1;
             }
           }
-          ptx::mma_commit(&empty[stage]);
+          if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+          else ptx::mma_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
           if (++kb_in_seg == seg_kb) {
-            ptx::mma_commit(&acc_full[seg & 1]);
+            if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+            else ptx::mma_commit(&acc_full[seg & 1]);
             kb_in_seg = 0;
             ++seg;
           }
         }
       }
-      if (kb_in_seg != 0) ptx::mma_commit(&acc_full[seg & 1]);
+      if (kb_in_seg != 0) {
+        if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+        else ptx::mma_commit(&acc_full[seg & 1]);
+      }
     }
   } else if (warp >= EPI_WARP0) {
     // ---------------- epilogue: TMEM partial sums -> fp32 registers (RNE) -> global
@@ -192,6 +220,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int half = (warp - EPI_WARP0) >> 2;    // column half of the 256-wide tile
     const int row = q * 32 + lane;
     const uint32_t tlane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 128);
+    const uint32_t empty_leader = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0) : 0u;
     float acc[128];
 #pragma unroll
     for (int j = 0; j < 128; ++j) acc[j] = 0.f;
@@ -209,7 +238,10 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&acc_empty[buf]);
+      if (lane == 0) {
+        if (CG == 2) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
+        else ptx::mbar_arrive(&acc_empty[buf]);
+      }
     }
     const int grow = m0 + row;
     const int gcol0 = n0 + half * 128;
@@ -248,27 +280,43 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2) ptx::cluster_sync();  // the peer's TMEM/barriers stay alive until the leader is done
+  else __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2) ptx::tmem_dealloc_cg2(tmem_base, TMEM_COLS);
+    else ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
-template <bool A_MN, bool B_K, int PLANES>
+template <bool A_MN, bool B_K, int PLANES, int CG>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args,
                            cudaStream_t stream) {
-  using C = Cfg<PLANES>;
+  using C = Cfg<PLANES, CG>;
+  auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(tile_gemm_kernel<A_MN, B_K, PLANES>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-  });
+  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
   if (attr_err != cudaSuccess) return attr_err;
-  dim3 grid((args.m_valid + BM - 1) / BM, (args.n_valid + BN - 1) / BN);
-  tile_gemm_kernel<A_MN, B_K, PLANES><<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, args);
-  return cudaGetLastError();
+  const int m_blocks = (args.m_valid + BM * CG - 1) / (BM * CG);
+  dim3 grid(m_blocks * CG, (args.n_valid + BN - 1) / BN);
+  if (CG == 1) {
+    kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, args);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(NUM_THREADS);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, args);
 }
 
 // ---------------------------------------------------------------- K2 split/convert
@@ -330,27 +378,56 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box) {
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
 
-void gemm_boxes(bool a_mn, bool b_kmajor, BoxKind* box_a, BoxKind* box_b) {
+void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b) {
+  const bool pair = m_valid > BM && gemm_pairs_enabled();
   *box_a = a_mn ? BOX_MN64 : BOX_K128;
-  *box_b = b_kmajor ? BOX_K256 : BOX_MN64;
+  *box_b = b_kmajor ? (pair ? BOX_K128 : BOX_K256) : BOX_MN64;
 }
 
 cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
                              bool b_kmajor, cudaStream_t stream) {
   if (args.m_valid <= 0 || args.n_valid <= 0 || args.n_ksteps <= 0 || args.n_ksteps > kMaxKSteps)
     return cudaErrorInvalidValue;
-  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (args.planes == 2 ? 1 : 0);
+  // CTA pairs once a tile has more than one 128-row block; single CTAs otherwise.
+  const bool pair = args.m_valid > BM && gemm_pairs_enabled();
+  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (args.planes == 2 ? 1 : 0) | (pair ? 8 : 0);
   switch (variant) {
-    case 0: return launch_variant<false, false, 1>(tmA, tmB, args, stream);
-    case 1: return launch_variant<false, false, 2>(tmA, tmB, args, stream);
-    case 2: return launch_variant<false, true, 1>(tmA, tmB, args, stream);
-    case 3: return launch_variant<false, true, 2>(tmA, tmB, args, stream);
-    case 4: return launch_variant<true, false, 1>(tmA, tmB, args, stream);
-    case 5: return launch_variant<true, false, 2>(tmA, tmB, args, stream);
-    case 6: return launch_variant<true, true, 1>(tmA, tmB, args, stream);
-    default: return launch_variant<true, true, 2>(tmA, tmB, args, stream);
+    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, args, stream);
+    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, args, stream);
+    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, args, stream);
+    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, args, stream);
+    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, args, stream);
+    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, args, stream);
+    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, args, stream);
+    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, args, stream);
+    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, args, stream);
+    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, args, stream);
+    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, args, stream);
+    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, args, stream);
+    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, args, stream);
+    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, args, stream);
+    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, args, stream);
+    default: return launch_variant<true, true, 2, 2>(tmA, tmB, args, stream);
   }
 }
+
+static std::atomic<int> g_pairs{-1};
+
+bool gemm_pairs_enabled() {
+  int v = g_pairs.load();
+  if (v < 0) {
+    // Default: single CTAs.  Measured on B200 (tools/probe_variants.py): pairs are
+    // ~2% faster for one kernel alone but ~10% slower when two tasks' kernels
+    // share the GPU (cluster placement is less flexible), which is the runtime's
+    // normal state.  TR_GEMM_PAIRS=1 opts in.
+    const char* e = getenv("TR_GEMM_PAIRS");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_pairs.store(v);
+  }
+  return v != 0;
+}
+
+void set_gemm_pairs(bool on) { g_pairs.store(on ? 1 : 0); }
 
 cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols,
                                  uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,

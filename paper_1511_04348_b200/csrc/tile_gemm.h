@@ -65,10 +65,14 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box);
 
 // Launches the tile GEMM.  a_mn: A stored K x M (transposed operand, MN-major);
 // b_kmajor: B stored N x K (transposed operand, K-major).
-// tmA/tmB must have been made with the boxes reported by gemm_boxes().
+// tmA/tmB must have been made with the boxes reported by gemm_boxes(a_mn, b_kmajor, m_valid).
 cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
                              bool b_kmajor, cudaStream_t stream);
-void gemm_boxes(bool a_mn, bool b_kmajor, BoxKind* box_a, BoxKind* box_b);
+void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b);
+// CTA-pair (cta_group::2, 256 x 256) variant for tiles taller than 128 rows.
+// Off by default; TR_GEMM_PAIRS=1 or set_gemm_pairs(true) selects it.
+bool gemm_pairs_enabled();
+void set_gemm_pairs(bool on);
 
 // K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
 // into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything

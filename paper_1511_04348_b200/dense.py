@@ -22,6 +22,11 @@ def precision_code(p) -> int:
         raise ValueError(f"unknown precision {p!r}; expected one of {sorted(PRECISIONS)}") from None
 
 
+def set_gemm_pairs(on: bool) -> None:
+    """Select the CTA-pair (cta_group::2) kernel variant (default) or single CTAs."""
+    N.call("tr_set_gemm_pairs", int(bool(on)))
+
+
 def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,
                stream=None):
     """``out (+)= op(a) @ op(b)`` for torch CUDA tensors (float32/float64).

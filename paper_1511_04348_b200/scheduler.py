@@ -426,6 +426,11 @@ class Runtime:
         """Tasks each device executes concurrently (default 2; 1 serialises)."""
         N.call("tr_session_set_inflight", self._h, int(max_inflight))
 
+    def set_order(self, order: str) -> None:
+        """Task enqueue order: "row-major" (reference), "banded", or "auto"."""
+        code = {"auto": -1, "row-major": 0, "banded": 1}[order]
+        N.call("tr_session_set_order", self._h, code)
+
     def fresh_uid(self, prefix: str = "m") -> str:
         self._uid_n += 1
         return f"{prefix}#{self._uid_n}"

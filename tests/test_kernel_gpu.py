@@ -10,6 +10,7 @@ import pytest
 import torch
 
 from paper_1511_04348_b200 import dense_gemm
+from paper_1511_04348_b200.dense import set_gemm_pairs
 
 pytestmark = pytest.mark.gpu
 
@@ -39,10 +40,17 @@ def ref_product(a, b, ta, tb):
 SHAPES = [(128, 256, 64), (1, 1, 1), (5, 7, 3), (200, 300, 130), (257, 513, 1000), (1024, 768, 4096)]
 
 
+@pytest.fixture(params=[False, True], ids=["cta", "cta_pair"])
+def variant(request):
+    set_gemm_pairs(request.param)
+    yield request.param
+    set_gemm_pairs(False)
+
+
 @pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("shape", SHAPES)
-def test_dense_kernel_normal(shape, ta, tb, precision):
+def test_dense_kernel_normal(shape, ta, tb, precision, variant):
     m, n, k = shape
     gen = torch.Generator().manual_seed(hash((shape, ta, tb)) & 0xFFFF)
     a, b = make(m, k, n, ta, tb, torch.float32, gen)
@@ -53,7 +61,7 @@ def test_dense_kernel_normal(shape, ta, tb, precision):
 
 
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, True)])
-def test_dense_kernel_integers_exact(ta, tb):
+def test_dense_kernel_integers_exact(ta, tb, variant):
     gen = torch.Generator().manual_seed(7)
     for (m, n, k) in [(33, 65, 17), (300, 260, 700)]:
         a, b = make(m, k, n, ta, tb, torch.float64, gen, kind="int")
@@ -63,7 +71,7 @@ def test_dense_kernel_integers_exact(ta, tb):
             assert torch.equal(c, ref_product(a, b, ta, tb)), precision
 
 
-def test_dense_kernel_accumulate_and_f64_out():
+def test_dense_kernel_accumulate_and_f64_out(variant):
     gen = torch.Generator().manual_seed(3)
     a, b = make(130, 70, 300, False, False, torch.float64, gen)
     c0 = torch.randn((130, 300), dtype=torch.float64, generator=gen).cuda()
