@@ -154,7 +154,8 @@ enum {
   TR_FLAG_COHERENCE = 1u << 1, /* Runtime(coherence=True); off = bypass (2g^3 host)     */
   TR_FLAG_DEBUG = 1u << 2,     /* Runtime(directory_debug=True): invariants per mutation */
   TR_FLAG_DRYRUN = 1u << 3,    /* schedule-only test mode: no CUDA, no arithmetic, C untouched */
-  TR_FLAG_FIFO = 1u << 4       /* FIFO eviction instead of LRU                          */
+  TR_FLAG_FIFO = 1u << 4,      /* FIFO eviction instead of LRU                          */
+  TR_FLAG_NO_PREFETCH = 1u << 5 /* disable fetch-ahead of reserved tasks' input tiles   */
 };
 
 typedef struct {
@@ -223,9 +224,10 @@ int tr_session_span_ms(tr_session* s, double* per_device_ms /* n_devices */);
 int tr_session_set_inflight(tr_session* s, int32_t max_inflight);
 /* Order in which tr_gemm enqueues task ids: 0 = row-major (the reference's,
  * scheduler.py:189-192), 1 = banded (pairs of task rows walked column by
- * column: first-touch host traffic spread over the run), -1 = auto (default:
- * banded unless some device has a bounded capacity, where LRU eviction
- * sequences -- and so the counters -- depend on the order). */
+ * column), 2 = shells (tasks with max(i,j) = s before shell s+1: first-touch
+ * host traffic spread over the run), -1 = auto (default: shells unless some
+ * device has a bounded capacity, where LRU eviction sequences -- and so the
+ * counters -- depend on the order). */
 int tr_session_set_order(tr_session* s, int32_t order);
 /* Sessions return HBM slabs/staging buffers to a process-wide cache reused by
  * later sessions; this frees every cached block. */

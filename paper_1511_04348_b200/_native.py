@@ -25,7 +25,8 @@ TR_POLICY_LRU, TR_POLICY_FIFO = 0, 1
 TR_HIT_L1, TR_HIT_L2, TR_HIT_MISS = 0, 1, 2
 TR_SOURCE_HOST = -1
 TR_KIND_ACCELERATOR, TR_KIND_HOST_WORKER = 0, 1
-TR_FLAG_STEAL, TR_FLAG_COHERENCE, TR_FLAG_DEBUG, TR_FLAG_DRYRUN, TR_FLAG_FIFO = 1, 2, 4, 8, 16
+TR_ACT_IDENTITY, TR_ACT_SIGMOID, TR_ACT_RELU = 0, 1, 2
+TR_FLAG_STEAL, TR_FLAG_COHERENCE, TR_FLAG_DEBUG, TR_FLAG_DRYRUN, TR_FLAG_FIFO, TR_FLAG_NO_PREFETCH = 1, 2, 4, 8, 16, 32
 
 i32, i64, u64, u8, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint8, C.c_double
 P = C.POINTER

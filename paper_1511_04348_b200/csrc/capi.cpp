@@ -384,7 +384,7 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
 
 int tr_session_set_order(tr_session* s, int32_t order) {
   return guarded([&] {
-    if (order < -1 || order > 1) tr::fail(TR_ERR_VALUE, "order must be -1 (auto), 0 (row-major) or 1 (banded)");
+    if (order < -1 || order > 2) tr::fail(TR_ERR_VALUE, "order must be -1 (auto), 0 (row-major), 1 (banded) or 2 (shells)");
     s->s->set_order(order);
   });
 }

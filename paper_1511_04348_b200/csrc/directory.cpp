@@ -162,7 +162,7 @@ std::vector<TileKey> Directory::admit_locked(int device, const TileKey& key, boo
     d.free_slots.pop_back();
   }
   d.order.push_back(key);
-  d.entries[key] = Entry{std::prev(d.order.end()), slot};
+  d.entries[key] = Entry{std::prev(d.order.end()), slot, 0};
   residency_[key] |= 1ull << device;
   if (slot_out) *slot_out = slot;
   if (debug_) check_invariants_locked();
@@ -199,12 +199,33 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
   int32_t owner = -1;
   const HitLevel lvl = lookup_locked(requester, key, &owner);
   if (lvl == HIT_L1) {
+    Entry& e = d.entries.at(key);
+    d.pins[key] += 1;
+    r.slot = e.slot;
+    if (e.pending) {
+      // first request of a fetched-ahead tile: count what the fetch was
+      r.prefetched = true;
+      r.nbytes = nbytes;
+      if (e.pending - 1 == HIT_L2) {
+        stats_.l2_hits += 1;
+        ds.l2_hits += 1;
+        stats_.bytes_peer += nbytes;
+        ds.bytes_peer += nbytes;
+        r.level = HIT_L2;
+      } else {
+        stats_.host_fetches += 1;
+        ds.host_fetches += 1;
+        stats_.bytes_host += nbytes;
+        ds.bytes_host += nbytes;
+        r.level = HIT_MISS;
+      }
+      e.pending = 0;
+      return r;
+    }
     stats_.l1_hits += 1;
     ds.l1_hits += 1;
-    d.pins[key] += 1;
     r.level = HIT_L1;
     r.source = requester;
-    r.slot = d.entries.at(key).slot;
     return r;
   }
   if (lvl == HIT_L2) {
@@ -228,6 +249,21 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
   d.pins[key] += 1;
   r.nbytes = nbytes;
   return r;
+}
+
+bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, HitLevel* level, int32_t* source) {
+  if (!enabled_ || host_worker_[device]) return false;
+  Dev& d = dev_[device];
+  if (d.entries.count(key)) return false;
+  if (capacity_[device] >= 0 && static_cast<int64_t>(d.order.size()) >= capacity_[device]) return false;
+  if (slot_total_[device] > 0 && d.free_slots.empty()) return false;
+  auto it = residency_.find(key);
+  const uint64_t owners = it == residency_.end() ? 0 : it->second;
+  *level = owners ? HIT_L2 : HIT_MISS;
+  *source = owners ? closest_owner(device, owners) : TR_SOURCE_HOST;
+  admit_locked(device, key, true, slot);  // cannot evict: checked above
+  d.entries.at(key).pending = static_cast<int8_t>(*level + 1);
+  return true;
 }
 
 // coherence.py:248-252

@@ -46,6 +46,7 @@ struct Acquired {
   int64_t nbytes;
   int32_t slot;    // physical slot on the requester (-1: none / bypass)
   std::vector<TileKey> evicted;
+  bool prefetched = false;  // counted as `level` but already resident (filled ahead of the request)
 };
 
 class Directory {
@@ -79,6 +80,13 @@ class Directory {
   Acquired acquire_input_locked(int requester, const TileKey& key, int64_t nbytes);
   void release_input_locked(int device, const TileKey& key);
   std::vector<TileKey> admit_output_locked(int device, const TileKey& key);
+  // Fetch-ahead: make `key` resident on `device` before any task requests it,
+  // WITHOUT counting anything and without evicting (returns false when the tile
+  // is already resident, the device is full, or coherence is off).  The first
+  // acquire_input of the tile on `device` is then counted exactly as it would
+  // have been without the prefetch (host fetch, or L2 hit), so every counter
+  // keeps the reference's meaning.  *level/*source say where to copy from.
+  bool prefetch_locked(int device, const TileKey& key, int32_t* slot, HitLevel* level, int32_t* source);
   void release_output_locked(int device, const TileKey& key, int64_t nbytes);
   void check_invariants_locked();
   int32_t slot_of_locked(int device, const TileKey& key) const;
@@ -93,6 +101,7 @@ class Directory {
   struct Entry {
     std::list<TileKey>::iterator pos;
     int32_t slot;
+    int8_t pending = 0;  // fetched ahead, not yet requested: HIT_MISS or HIT_L2 + 1
   };
   struct Dev {
     std::list<TileKey> order;  // LRU order, most recent at the back

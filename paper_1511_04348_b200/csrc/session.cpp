@@ -120,7 +120,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
       if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
       dc.max_slots = static_cast<int32_t>(slots);
-      dc.streams.resize(dc.width);
+      dc.streams.resize(dc.width + 1);  // + the fetch-ahead stream (index width)
       TR_CUDA(cudaEventCreate(&dc.span_start));
       TR_CUDA(cudaEventCreate(&dc.span_end));
       for (auto& sc : dc.streams) {
@@ -302,14 +302,27 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
   DeviceCtx& dc = devs_[d];
   const int32_t phys = phys_of(d, a.slot);
   SlotState& st = dc.slots[phys];
-  if (a.level == HIT_L1) {
+  if (a.level == HIT_L1 || a.prefetched) {
+    // resident (possibly still being filled ahead of time on another stream)
     wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
     return phys;
   }
+  load_slot(d, s, phys, a.level, a.source, key, src, r, c, job);
+  return phys;
+}
+
+// Physical side of an L2 hit (peer copy of the converted planes) or a miss
+// (host H2D + split/convert, or device-matrix split/convert) into slot `phys`
+// of device d, on stream s.  Caller holds the directory lock.
+void Session::load_slot(int d, int s, int32_t phys, HitLevel level, int32_t source, const TileKey& key,
+                        const Mat& src, int64_t r, int64_t c, Job& job) {
+  DeviceCtx& dc = devs_[d];
+  SlotState& st = dc.slots[phys];
+  const int32_t gs = gs_of(d, s);
   wait_slot_free(d, s, phys);
   StreamCtx& sc = dc.streams[s];
-  if (a.level == HIT_L2) {
-    const int o = a.source;
+  if (level == HIT_L2) {
+    const int o = source;
     const int32_t src_phys = phys_of(o, dir_->slot_of_locked(o, key));
     SlotState& ss = devs_[o].slots[src_phys];
     wait_event_if_foreign(d, s, ss.ready_gs, ss.ready_ev);
@@ -330,14 +343,43 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
     st.ready_gs = gs;
     st.ready_ev = ev;
     st.uses.clear();
-    return phys;
+    return;
   }
   fill_slot(d, s, phys, src, r, c);
   job.launches.fetch_add(1);
   st.ready_gs = gs;
   st.ready_ev = record(d, s);
   st.uses.clear();
-  return phys;
+}
+
+// Fetch-ahead ("threaded fetch-ahead", absent from the
+// reference's code): the input tiles of tasks already RESERVED by this device
+// are brought in on the device's fetch-ahead stream while earlier tasks compute,
+// overlapping H2D/NVLink traffic with the tensor pipe.  Directory::prefetch_locked
+// never evicts and never counts, so the counters are exactly the reference's.
+void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen) {
+  DeviceCtx& dc = devs_[d];
+  const int s = dc.width;  // fetch-ahead stream
+  for (uint64_t tid : dc.station->peek()) {
+    if (seen[tid]) continue;
+    seen[tid] = 1;
+    const int64_t i = static_cast<int64_t>(tid) / job.grid_cols, j = static_cast<int64_t>(tid) % job.grid_cols;
+    for (int64_t k = 0; k < job.k_steps; ++k) {
+      for (int which = 0; which < 2; ++which) {
+        const Mat& m = which == 0 ? job.a : job.b;
+        const uint64_t uid = which == 0 ? job.a_uid : job.b_uid;
+        const bool t = which == 0 ? job.ta : job.tb;
+        const int64_t r = which == 0 ? (t ? k : i) : (t ? j : k);
+        const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
+        const TileKey key{uid, r, c};
+        std::lock_guard<std::mutex> g(dir_->mu);
+        int32_t slot = -1, source = -1;
+        HitLevel level;
+        if (!dir_->prefetch_locked(d, key, &slot, &level, &source)) continue;
+        load_slot(d, s, phys_of(d, slot), level, source, key, m, r, c, job);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- task issue
@@ -482,6 +524,9 @@ void Session::run_job(int d, Job& job) {
   DeviceCtx& dc = devs_[d];
   Station& st = *dc.station;
   uint64_t seq = 0;
+  bool ahead = !dryrun_ && coherence_ && !(flags_ & TR_FLAG_NO_PREFETCH);
+  for (auto& dv : devs_) ahead = ahead && dv.capacity < 0;  // bounded caches: keep eviction order exact
+  std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.grid_rows * job.grid_cols) : 0, 0);
   while (!job.abort.load()) {
     int active = 0;
     if (!dryrun_) {
@@ -493,6 +538,7 @@ void Session::run_job(int d, Job& job) {
       continue;
     }
     st.refill(job.queue, dc.width - active);
+    if (ahead) fetch_ahead(d, job, seen);
     uint64_t tid;
     int victim = -1;
     if (!st.pop_for_run(&tid)) {
@@ -607,22 +653,33 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   job.task_stride = task_stride;
   // plan(): every task enqueued up front (scheduler.py:189-192).  Row-major as in
   // the reference, or -- when no device has a bounded capacity, so the hit/miss
-  // counters cannot depend on the order -- banded: rows taken two at a time and
-  // walked column by column, which spreads first-touch host traffic over the run
-  // (each new B tile serves two tasks immediately).
+  // counters cannot depend on the order -- in "shells" (all tasks with
+  // max(i, j) = s before shell s + 1), which spreads first-touch host traffic
+  // over the run instead of loading every B panel during the first task row.
   const int64_t total = job.grid_rows * job.grid_cols;
-  bool banded = order_ == 1;
-  if (order_ < 0) {
-    banded = true;
-    for (auto& dc : devs_) banded = banded && dc.capacity < 0;
+  int order = order_;
+  if (order < 0) {
+    order = 2;
+    for (auto& dc : devs_)
+      if (dc.capacity >= 0) order = 0;
   }
   std::vector<int64_t> ids;
   ids.reserve(static_cast<size_t>(total));
-  if (banded) {
+  if (order == 1) {
     const int64_t G = 2;
     for (int64_t b = 0; b < job.grid_rows; b += G)
       for (int64_t j = 0; j < job.grid_cols; ++j)
         for (int64_t i = b; i < std::min(b + G, job.grid_rows); ++i) ids.push_back(i * job.grid_cols + j);
+  } else if (order == 2) {
+    // shells: task (i, j) in shell max(i, j); each shell adds one A row and one
+    // B column of tiles, so compute starts after 2 k-panels instead of a full row
+    const int64_t g = std::max(job.grid_rows, job.grid_cols);
+    for (int64_t sh = 0; sh < g; ++sh) {
+      for (int64_t i = 0; i < std::min(sh, job.grid_rows); ++i)
+        if (sh < job.grid_cols) ids.push_back(i * job.grid_cols + sh);
+      if (sh < job.grid_rows)
+        for (int64_t j = 0; j <= std::min(sh, job.grid_cols - 1); ++j) ids.push_back(sh * job.grid_cols + j);
+    }
   } else {
     for (int64_t t = 0; t < total; ++t) ids.push_back(t);
   }
@@ -670,7 +727,8 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
       TR_CUDA(cudaSetDevice(dc.gpu));
       if (ext_stream_) TR_CUDA(cudaStreamWaitEvent(dc.streams[0].stream, ext_ready_, 0));
       TR_CUDA(cudaEventRecord(dc.span_start, dc.streams[0].stream));
-      for (int s = 1; s < dc.width; ++s) TR_CUDA(cudaStreamWaitEvent(dc.streams[s].stream, dc.span_start, 0));
+      for (size_t s = 1; s < dc.streams.size(); ++s)
+        TR_CUDA(cudaStreamWaitEvent(dc.streams[s].stream, dc.span_start, 0));
     }
   }
   const auto t0 = std::chrono::steady_clock::now();
@@ -689,7 +747,7 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   if (!dryrun_) {
     for (auto& dc : devs_) {
       cudaSetDevice(dc.gpu);
-      for (int s = 1; s < dc.width; ++s) {
+      for (int s = 1; s < static_cast<int>(dc.streams.size()); ++s) {
         cudaEvent_t ev = record(dc.id, s);
         cudaStreamWaitEvent(dc.streams[0].stream, ev, 0);
       }

@@ -137,6 +137,9 @@ class Session {
   int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
                   int scratch);
   void fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c);
+  void load_slot(int d, int s, int32_t phys, HitLevel level, int32_t source, const TileKey& key, const Mat& src,
+                 int64_t r, int64_t c, Job& job);
+  void fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen);
   void wait_slot_free(int d, int s, int32_t phys);
   void wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev);
   cudaEvent_t record(int d, int s);
@@ -160,7 +163,7 @@ class Session {
   bool dryrun_, steal_, coherence_;
   int32_t element_bytes_;
   int64_t hbm_budget_;
-  int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, -1 auto
+  int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, 2 shells, -1 auto
   cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
   cudaEvent_t ext_ready_ = nullptr;
   std::unique_ptr<Directory> dir_;

@@ -56,6 +56,11 @@ class Station {
     std::lock_guard<std::mutex> g(mu_);
     return static_cast<int>(slots_.size());
   }
+  // Snapshot of the reserved ids, front first (for fetch-ahead).
+  std::vector<uint64_t> peek() {
+    std::lock_guard<std::mutex> g(mu_);
+    return std::vector<uint64_t>(slots_.begin(), slots_.end());
+  }
   void clear() {
     std::lock_guard<std::mutex> g(mu_);
     slots_.clear();

@@ -1,0 +1,149 @@
+"""Device-resident MLP training through the tiled GPU runtime (BASELINE cfg3).
+
+Same algebra and the same 3·L products per step as the reference's
+``train_step`` (ann.py:239-248, Eqs. 1-4 of the paper):
+
+    forward   Y_l = X_l W_l (product) ; Y_l += b_l ; X_{l+1} = act(Y_l)   (K3)
+    loss      dOut = 2 (pred - target) / size ; loss = mean (pred - target)^2 (K4b)
+    backward  dY_l = dOut * act'(Y_l, X_{l+1})                             (K4)
+              dW_l = X_l^T dY_l        (product, transposed A: layout, no copy)
+              dX_l = dY_l W_l^T        (product, transposed B; also for l = 0,
+                                        as the reference does)
+              db_l = colsum dY_l                                           (K5)
+    update    W_l -= lr dW_l ; b_l -= lr db_l ; version += 1               (K6)
+
+Every product is ``Runtime.multiply`` on device-resident operands: tiles are
+admitted into the HBM tile cache by uid (activation/gradient uids are fresh
+per step, weight uids are versioned exactly like ``Layer.weight_uid``), so the
+backward products hit the tiles the forward products cached.  Activations and
+parameters are float32 on the device; the products run in the FP32-accurate
+mode; the loss is accumulated in float64.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .devices import Machine, homogeneous_machine
+from .scheduler import Runtime
+
+_ACT = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
+
+
+def _ptr(t) -> int:
+    return t.data_ptr()
+
+
+@dataclass
+class DeviceLayer:
+    w: object  # torch.Tensor fan_in x fan_out (float32, cuda)
+    b: object | None
+    activation: str
+    tag: str
+    version: int = 0
+
+    @property
+    def weight_uid(self) -> str:
+        return f"{self.tag}.w.v{self.version}"
+
+
+class GpuMLP:
+    """A float32 MLP living in HBM, trained through a tiled ``Runtime`` session."""
+
+    def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
+                 device: int = 0, runtime: Runtime | None = None):
+        import torch
+
+        self.torch = torch
+        self.dev = torch.device("cuda", device)
+        self.layers: list[DeviceLayer] = []
+        for i, L in enumerate(layers):
+            w = torch.as_tensor(np.asarray(L.weights), dtype=torch.float32).to(self.dev).contiguous()
+            b = None if L.bias is None else torch.as_tensor(np.asarray(L.bias), dtype=torch.float32).to(self.dev)
+            self.layers.append(DeviceLayer(w, b, L.activation, getattr(L, "tag", f"layer{i}")))
+        if runtime is None:
+            machine = machine or homogeneous_machine(1, dtype=np.float32, gpus=[device])
+            runtime = Runtime(machine, tile_size, precision=precision)
+        self.rt = runtime
+        self._loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self._bufs: dict = {}
+        self.products = 0
+
+    # -- helpers -----------------------------------------------------------
+    def _buf(self, name, shape):
+        t = self._bufs.get(name)
+        if t is None or tuple(t.shape) != tuple(shape):
+            t = self.torch.empty(shape, dtype=self.torch.float32, device=self.dev)
+            self._bufs[name] = t
+        return t
+
+    def _stream(self):
+        return self.torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _mm(self, a, b, out, ta=False, tb=False, a_uid=None, b_uid=None):
+        N.call("tr_session_set_external_stream", self.rt._h, self._stream())
+        self.rt.multiply(a, b, transpose_a=ta, transpose_b=tb, a_uid=a_uid, b_uid=b_uid, out=out)
+        self.products += 1
+        return out
+
+    # -- one pass ------------------------------------------------------------
+    def loss_gradients(self, x, target):
+        """Forward + backward without update; returns (loss, [(dW, db)]) on the device."""
+        torch = self.torch
+        s = self._stream()
+        xs, ys, acts, uids = [], [], [], []
+        cur, cur_uid = x, self.rt.fresh_uid("x")
+        for li, L in enumerate(self.layers):
+            xs.append(cur)
+            uids.append(cur_uid)
+            y = self._buf(f"y{li}", (cur.shape[0], L.w.shape[1]))
+            self._mm(cur, L.w, y, a_uid=cur_uid, b_uid=L.weight_uid)
+            a = self._buf(f"a{li}", y.shape)
+            N.call("tr_mlp_bias_act", _ptr(y), _ptr(a), _ptr(L.b) if L.b is not None else None, y.shape[0],
+                   y.shape[1], _ACT[L.activation], s)
+            ys.append(y)
+            acts.append(a)
+            cur, cur_uid = a, self.rt.fresh_uid("x")
+        pred = acts[-1]
+        d_out = self._buf("dout", pred.shape)
+        N.call("tr_mlp_mse_grad", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(), _ptr(self._loss), s)
+        grads = [None] * len(self.layers)
+        for li in range(len(self.layers) - 1, -1, -1):
+            L = self.layers[li]
+            d_y = self._buf(f"dy{li}", ys[li].shape)
+            N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), _ptr(ys[li]), _ptr(acts[li]), d_y.numel(),
+                   _ACT[L.activation], s)
+            dy_uid = self.rt.fresh_uid("dy")
+            d_w = self._buf(f"dw{li}", L.w.shape)
+            self._mm(xs[li], d_y, d_w, ta=True, a_uid=uids[li], b_uid=dy_uid)
+            d_x = self._buf(f"dx{li}", xs[li].shape)
+            self._mm(d_y, L.w, d_x, tb=True, a_uid=dy_uid, b_uid=L.weight_uid)
+            d_b = None
+            if L.b is not None:
+                d_b = self._buf(f"db{li}", L.b.shape)
+                N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
+            grads[li] = (d_w, d_b)
+            d_out = d_x
+        return pred.numel(), grads
+
+    def train_step(self, x, target, lr: float) -> float:
+        """One SGD step (ann.py:239-248); returns the MSE loss (read back to the host)."""
+        n, grads = self.loss_gradients(x, target)
+        s = self._stream()
+        for L, (d_w, d_b) in zip(self.layers, grads):
+            N.call("tr_mlp_sgd", _ptr(L.w), _ptr(d_w), L.w.numel(), float(lr), s)
+            if L.b is not None:
+                N.call("tr_mlp_sgd", _ptr(L.b), _ptr(d_b), L.b.numel(), float(lr), s)
+            L.version += 1
+        return float(self._loss.item()) / n
+
+    def to_host(self):
+        """[(W, b)] as float64 numpy arrays."""
+        return [(L.w.double().cpu().numpy(), None if L.b is None else L.b.double().cpu().numpy())
+                for L in self.layers]
+
+    def close(self):
+        self.rt.close()

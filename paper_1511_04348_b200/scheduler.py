@@ -375,7 +375,8 @@ class Runtime:
 
     def __init__(self, machine: Machine, tile_size: int, mode: str = "gpu", steal: bool = True,
                  coherence: bool = True, seed: int | None = None, directory_debug: bool = False,
-                 precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru"):
+                 precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru",
+                 fetch_ahead: bool = True):
         if mode not in MODES:
             if mode == "sim":
                 raise ValueError("mode 'sim' is the reference's simulated engine; the B200 runtime executes on "
@@ -394,6 +395,7 @@ class Runtime:
         flags |= N.TR_FLAG_DEBUG if directory_debug else 0
         flags |= N.TR_FLAG_DRYRUN if mode == "dryrun" else 0
         flags |= N.TR_FLAG_FIFO if policy == "fifo" else 0
+        flags |= 0 if fetch_ahead else N.TR_FLAG_NO_PREFETCH
         mc, keep = machine._as_c()
         h = C.c_void_p()
         N.call("tr_session_create", C.byref(mc), int(tile_size), precision_code(precision), flags,
@@ -427,8 +429,8 @@ class Runtime:
         N.call("tr_session_set_inflight", self._h, int(max_inflight))
 
     def set_order(self, order: str) -> None:
-        """Task enqueue order: "row-major" (reference), "banded", or "auto"."""
-        code = {"auto": -1, "row-major": 0, "banded": 1}[order]
+        """Task enqueue order: "row-major" (reference), "banded", "shells", or "auto"."""
+        code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2}[order]
         N.call("tr_session_set_order", self._h, code)
 
     def fresh_uid(self, prefix: str = "m") -> str:

@@ -1,0 +1,63 @@
+"""Device-resident MLP training (GpuMLP: products through the tiled runtime,
+elementwise steps in the K3-K7 kernels) against the reference's golden f64
+trajectories and against the oracle at a larger width."""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import tilerun_oracle as O
+from paper_1511_04348_b200 import GpuMLP, Layer, homogeneous_machine
+
+pytestmark = pytest.mark.gpu
+G = Path(__file__).resolve().parent / "golden"
+
+
+def relerr(x, ref):
+    return float(np.linalg.norm(np.asarray(x, np.float64) - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+@pytest.mark.parametrize("act", ["sigmoid", "relu"])
+@pytest.mark.parametrize("tile", [16, 4096])
+def test_golden_trajectory(act, tile):
+    g = np.load(G / "ann.npz")
+    layers = [Layer(g[f"{act}_init_w{i}"], g[f"{act}_init_b{i}"], act, tag=f"layer{i}") for i in range(3)]
+    mlp = GpuMLP(layers, machine=homogeneous_machine(2, gpus=[0, 0]), tile_size=tile)
+    x = torch.as_tensor(g[f"{act}_x"], dtype=torch.float32).cuda()
+    t = torch.as_tensor(g[f"{act}_t"], dtype=torch.float32).cuda()
+    n, grads = mlp.loss_gradients(x, t)
+    loss0 = float(mlp._loss.item()) / n
+    assert abs(loss0 - g[f"{act}_loss0"][0]) <= 1e-5 * g[f"{act}_loss0"][0]
+    for i, (gw, gb) in enumerate(grads):
+        assert relerr(gw.cpu().numpy(), g[f"{act}_gw{i}"]) <= 1e-4
+        assert relerr(gb.cpu().numpy(), g[f"{act}_gb{i}"]) <= 1e-4
+    traj = np.array([mlp.train_step(x, t, 0.1) for _ in range(10)])
+    ref = g[f"{act}_losses"]
+    assert np.max(np.abs(traj - ref) / ref) <= 1e-5, (traj, ref)
+    for i, (w, b) in enumerate(mlp.to_host()):
+        assert relerr(w, g[f"{act}_final_w{i}"]) <= 1e-5
+    assert mlp.products == 11 * 3 * 3  # 11 passes x 3 layers x (1 forward + 2 backward products)
+    mlp.close()
+
+
+def test_wide_net_against_blas_oracle():
+    """784-2048-2048-2048-10, batch 2048 (cfg3 shape scaled by 1/4): three SGD
+    steps on the GPU vs the float64 oracle with the same init (SURVEY §7 init)."""
+    rng = np.random.default_rng(3)
+    sizes = [784, 2048, 2048, 2048, 10]
+    layers = [Layer.random(sizes[i], sizes[i + 1], rng, scale=1 / np.sqrt(sizes[i]), tag=f"layer{i}")
+              for i in range(4)]
+    x, t = O.random_regression(rng, 2048, 784, 10)
+    oracle_layers = [O.OracleLayer(L.weights.copy(), L.bias.copy(), L.activation) for L in layers]
+    mlp = GpuMLP(layers, tile_size=1024)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    for step in range(3):
+        lg = mlp.train_step(xd, td, 0.5)
+        lo = O.train_step(oracle_layers, x, t, 0.5, matmul=O.blas_matmul)
+        assert abs(lg - lo) <= 1e-5 * lo, (step, lg, lo)
+    for (w, b), L in zip(mlp.to_host(), oracle_layers):
+        assert relerr(w, L.weights) <= 1e-5 and relerr(b, L.bias) <= 1e-5
+    mlp.close()

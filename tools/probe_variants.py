@@ -15,34 +15,19 @@ C = torch.empty((n, n), device=dev)
 m = tr.homogeneous_machine(1, dtype=np.float32, gpus=[0])
 rows = torch.tensor([0, 4095, 4096, 20000, 32767], device=dev)
 ref = (A[rows].double() @ B.double())
-for pairs in (True, False, True):
-    set_gemm_pairs(pairs)
-    rt = tr.Runtime(m, T)
-    for _ in range(2):
-        rt.multiply(A, B, a_uid="A", b_uid="B", out=C)
-    spans = []
-    for _ in range(3):
-        _, s = rt.multiply(A, B, a_uid="A", b_uid="B", out=C)
-        spans.append(s.span_ms[0])
-    rt.set_inflight(1)
-    _, s1 = rt.multiply(A, B, a_uid="A", b_uid="B", out=C)
-    err = float((C[rows].double() - ref).norm() / ref.norm())
-    print(f"pairs={pairs}: warm product {np.mean(spans):.1f} ms -> {2*n**3/np.mean(spans)/1e9:.1f} TF/s; "
-          f"kernel alone {s1.kernel_ms[0]/s1.total_tasks:.3f} ms/launch -> {2*T*T*n/(s1.kernel_ms[0]/s1.total_tasks)/1e9:.1f} TF/s; err {err:.2e}", flush=True)
-    rt.close()
-set_gemm_pairs(True)
+set_gemm_pairs(False)
 a_host = tr.matrix.pinned_empty((n, n), np.float32); a_host[...] = A.cpu().numpy()
 b_host = tr.matrix.pinned_empty((n, n), np.float32); b_host[...] = B.cpu().numpy()
 del A, B, C
 torch.cuda.empty_cache()
-for order in ("row-major", "banded"):
-    for inflight in (2, 3, 4):
-        rt = tr.Runtime(m, T)
+for order in ("row-major", "banded", "shells"):
+    for fa, inflight in ((False, 2), (True, 2), (True, 3)):
+        rt = tr.Runtime(m, T, fetch_ahead=fa)
         rt.set_order(order); rt.set_inflight(inflight)
         ts = []
         for _ in range(3):
             t0 = time.perf_counter(); c, s = rt.multiply(a_host, b_host); ts.append(time.perf_counter() - t0); del c
-        print(f"order={order} inflight={inflight}: cold multiply {1e3*np.median(ts):.1f} ms "
+        print(f"order={order} fetch_ahead={fa} inflight={inflight}: cold multiply {1e3*np.median(ts):.1f} ms "
               f"(span {s.span_ms[0]:.1f}) -> {2*n**3/np.median(ts)/1e12:.1f} TF/s", flush=True)
         rt.close()
 ts = []
