@@ -62,6 +62,10 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
+    p.add_argument("--no-mlp", action="store_true")
+    p.add_argument("--mlp-steps", type=int, default=5)
+    p.add_argument("--mlp-sizes", default="784,8192,8192,8192,10")
+    p.add_argument("--mlp-batch", type=int, default=8192)
     return p.parse_args()
 
 
@@ -175,6 +179,84 @@ def cpu_port_sample(n: int, tile: int, target_s: float, threads: int = 0):
             f"{2.0 * m * m * k / 1e9:.1f} GFLOP), float32, k-ascending with no FMA (bit-identical to "
             f"tiles.py:197-212), {cores} threads on {cpu_model()}")
     return 2.0 * m * m * k / dt / 1e12, cores, desc, dt
+
+
+def mlp_flops(sizes, batch):
+    """3 products per layer per step (forward, dW, dX -- dX also for layer 0, as ann.py:171-172)."""
+    return sum(3 * 2.0 * batch * sizes[i] * sizes[i + 1] for i in range(len(sizes) - 1))
+
+
+def bench_mlp(args, tr, torch, local, barrier, max_over_ranks):
+    """cfg3: MLP training through the tiled runtime, device-resident (GpuMLP).
+
+    Per step (all inside the timed region): the batch x / target is copied H2D
+    from pinned host memory, forward + MSE + backward + SGD run (12 products via
+    Runtime.multiply, K3-K7 elementwise kernels), and the loss is read back D2H.
+    """
+    sizes = [int(v) for v in args.mlp_sizes.split(",")]
+    batch = args.mlp_batch
+    rng = np.random.default_rng(0)
+    # SURVEY.md §7: per-layer scale 1/sqrt(fan_in) (a single from_sizes scale saturates the sigmoids)
+    layers = [tr.Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
+                              tag=f"layer{i}") for i in range(len(sizes) - 1)]
+    x, t = tr.ann.random_regression(rng, batch, sizes[0], sizes[-1])
+    xh = tr.matrix.pinned_empty(x.shape, np.float32)
+    th = tr.matrix.pinned_empty(t.shape, np.float32)
+    xh[...] = x
+    th[...] = t
+    mlp = tr.GpuMLP(layers, tile_size=args.tile, device=local)
+    dev = torch.device("cuda", local)
+    xd = torch.empty(x.shape, dtype=torch.float32, device=dev)
+    td = torch.empty(t.shape, dtype=torch.float32, device=dev)
+    xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
+    losses = []
+    for _ in range(2):  # warm-up: slab sizing, kernel attributes
+        xd.copy_(xs, non_blocking=True)
+        td.copy_(ts, non_blocking=True)
+        losses.append(mlp.train_step(xd, td, 0.1))
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.mlp_steps):
+        xd.copy_(xs, non_blocking=True)
+        td.copy_(ts, non_blocking=True)
+        losses.append(mlp.train_step(xd, td, 0.1))
+    e1.record()
+    torch.cuda.synchronize()
+    dt = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.mlp_steps)
+    mlp.close()
+    flops = mlp_flops(sizes, batch)
+    return {"workload": f"cfg3 MLP {'-'.join(map(str, sizes))} batch {batch}, sigmoid, MSE, SGD lr 0.1 "
+                        "(device-resident GpuMLP; 12 products per step through Runtime.multiply)",
+            "samples_per_s": batch / dt, "ms_per_step": dt * 1e3, "tflops": flops / dt / 1e12,
+            "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
+            "loss_first": losses[0], "loss_last": losses[-1],
+            "h2d_bytes_per_step": int(x.size * 4 + t.size * 4), "d2h_bytes_per_step": 8}
+
+
+def mlp_cpu_baseline(sizes, batch, target_s=6.0):
+    """The oracle's f64 C port of the reference product on a bounded sample, extrapolated
+    to samples/s of the reference's train_step (products dominate)."""
+    from oracle import tilerun_oracle as O
+
+    O.build_c_oracle()
+    lib = O.c_oracle()
+    rng = np.random.default_rng(0)
+    m = 512
+    probe = rng.standard_normal((m, 256)), rng.standard_normal((256, m))
+    t0 = time.perf_counter()
+    lib.gemm(*probe)
+    rate = 2.0 * m * m * 256 / (time.perf_counter() - t0)
+    k = int(max(256, min(8192, target_s * rate / (2.0 * m * m))))
+    a, b = rng.standard_normal((m, k)), rng.standard_normal((k, m))
+    t0 = time.perf_counter()
+    lib.gemm(a, b)
+    rate = 2.0 * m * m * k / (time.perf_counter() - t0)
+    step_s = mlp_flops(sizes, batch) / rate
+    return {"value": batch / step_s, "unit": "samples/s", "cores": lib.max_threads(), "kind": "port",
+            "sample": f"f64 k-ascending product {m}x{k}x{m} ({rate / 1e9:.1f} GFLOP/s), extrapolated to the "
+                      f"{mlp_flops(sizes, batch) / 1e12:.2f} TFLOP of products per step"}
 
 
 # ----------------------------------------------------------------- reference arm
@@ -307,20 +389,28 @@ def main():
             got = C[torch.as_tensor(rows, device=dev)][:, torch.as_tensor(cols, device=dev)].double().cpu().numpy()
             parity = float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
 
+    rt.close()
+    del rt
+    torch.cuda.empty_cache()
+
+    # ---- MLP (cfg3): the metric's second half
+    mlp = None
+    if not args.no_mlp:
+        mlp = bench_mlp(args, tr, torch, local, barrier, max_over_ranks)
+        torch.cuda.empty_cache()
+
     # ---- e2e: reference-facing one-shot run() with pinned host numpy arrays
     e2e = None
     if not args.no_e2e:
-        rt.close()
-        del rt
-        torch.cuda.empty_cache()
         a_host = tr.matrix.pinned_empty((n, n), np.float32)
         b_host = tr.matrix.pinned_empty((n, n), np.float32)
         a_host[...] = A.cpu().numpy()
         b_host[...] = B.cpu().numpy()
         del A, B, C
         torch.cuda.empty_cache()
-        res = tr.run(machine, a_host, b_host, T, precision=args.precision)  # warm-up (allocators, pinned pool)
-        del res
+        for _ in range(2):  # warm-up: pinned output pool, HBM buffer pool, first large frees
+            res = tr.run(machine, a_host, b_host, T, precision=args.precision)
+            del res
         times = []
         h2d = d2h = 0
         for _ in range(max(1, args.e2e_steps)):
@@ -350,6 +440,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu:
         v, cores, desc, _ = cpu_port_sample(n, T, target_s=args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
+        if mlp is not None:
+            mlp["cpu_baseline"] = mlp_cpu_baseline([int(v) for v in args.mlp_sizes.split(",")], args.mlp_batch)
 
     if rank == 0:
         line = {
@@ -364,6 +456,7 @@ def main():
                        "l2": "inputs (8.6 GB) >> 126 MB L2; no flush needed",
                        "parallelism": f"task-sharded x{world}", "warm_cache": "all input tiles L1-resident"},
             "e2e": e2e,
+            "mlp": mlp,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "gpu_launches": launches,

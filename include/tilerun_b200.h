@@ -257,6 +257,12 @@ int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* 
 /* w -= lr * g                                                ann.py:243-247 */
 int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
 
+/* Drop every resident tile of matrix `uid` from the session's tile cache on all
+ * devices (the uid's content is dead, e.g. a retired weight version, ann.py:247).
+ * Not counted as an eviction.  The reference has no equivalent: its unbounded
+ * caches keep stale versions forever. */
+int tr_session_forget(tr_session* s, uint64_t uid, int64_t* dropped);
+
 /* Order every product of the session after the work already queued on `stream`
  * (cudaStream_t, e.g. the caller's framework stream); NULL clears it. */
 int tr_session_set_external_stream(tr_session* s, void* stream);

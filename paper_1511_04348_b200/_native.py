@@ -125,6 +125,7 @@ _PROTOS = {
     "tr_mlp_colsum": [vp, i64, i64, vp, vp],
     "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
     "tr_session_set_external_stream": [vp, vp],
+    "tr_session_forget": [vp, u64, P(i64)],
 }
 
 

@@ -409,6 +409,13 @@ int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* 
 int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
   return guarded([&] { TR_CUDA(tr::mlp_sgd(w, g, n, lr, static_cast<cudaStream_t>(stream))); });
 }
+int tr_session_forget(tr_session* s, uint64_t uid, int64_t* dropped) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> g(s->s->directory().mu);
+    const int64_t n = s->s->directory().forget_locked(uid);
+    if (dropped) *dropped = n;
+  });
+}
 int tr_session_set_external_stream(tr_session* s, void* stream) {
   return guarded([&] { s->s->set_external_stream(static_cast<cudaStream_t>(stream)); });
 }

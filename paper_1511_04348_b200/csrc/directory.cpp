@@ -295,6 +295,23 @@ void Directory::release_output_locked(int device, const TileKey& key, int64_t nb
   if (debug_) check_invariants_locked();
 }
 
+int64_t Directory::forget_locked(uint64_t uid) {
+  int64_t n = 0;
+  for (int d = 0; d < n_; ++d) {
+    Dev& dv = dev_[d];
+    std::vector<TileKey> dead;
+    for (const auto& e : dv.entries) {
+      if (e.first.matrix != uid) continue;
+      auto p = dv.pins.find(e.first);
+      if (p == dv.pins.end() || p->second == 0) dead.push_back(e.first);
+    }
+    for (const TileKey& k : dead) drop_locked(d, k);
+    n += static_cast<int64_t>(dead.size());
+  }
+  if (debug_) check_invariants_locked();
+  return n;
+}
+
 // coherence.py:300-313
 void Directory::check_invariants_locked() {
   std::vector<int64_t> per_dev(n_, 0);

@@ -88,6 +88,10 @@ class Directory {
   // keeps the reference's meaning.  *level/*source say where to copy from.
   bool prefetch_locked(int device, const TileKey& key, int32_t* slot, HitLevel* level, int32_t* source);
   void release_output_locked(int device, const TileKey& key, int64_t nbytes);
+  // Drop every unpinned resident tile of matrix `uid` on every device (the
+  // content is dead, e.g. a retired weight version).  Not an eviction; no
+  // counters change.  Returns the number of tiles dropped.
+  int64_t forget_locked(uint64_t uid);
   void check_invariants_locked();
   int32_t slot_of_locked(int device, const TileKey& key) const;
   // Owners of `key` (bitmask over device ids).

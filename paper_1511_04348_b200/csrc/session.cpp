@@ -114,22 +114,29 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       budget /= per_gpu[dc.gpu];
       const int64_t tile_bytes = static_cast<int64_t>(tile) * tile * 8;
       const int64_t slot_bytes = slot_elems_ * 2;
-      int64_t avail = budget - static_cast<int64_t>(dc.width) * 2 * tile_bytes;
+      int64_t avail = budget - (static_cast<int64_t>(dc.width + 2) * 2 + kStage) * tile_bytes;
       int64_t slots = avail / slot_bytes - 2 * dc.width;
       slots = std::min<int64_t>(slots, int64_t(1) << 22);
       if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
       if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
       dc.max_slots = static_cast<int32_t>(slots);
-      dc.streams.resize(dc.width + 1);  // + the fetch-ahead stream (index width)
+      dc.streams.resize(dc.width + 2);  // + fill (convert) stream [width] + copy stream [width+1]
       TR_CUDA(cudaEventCreate(&dc.span_start));
       TR_CUDA(cudaEventCreate(&dc.span_end));
-      for (auto& sc : dc.streams) {
-        TR_CUDA(cudaStreamCreateWithFlags(&sc.stream, cudaStreamNonBlocking));
+      int prio_low = 0, prio_high = 0;
+      TR_CUDA(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high));
+      for (size_t si = 0; si < dc.streams.size(); ++si) {
+        StreamCtx& sc = dc.streams[si];
+        // the fill stream runs at the highest priority: its split/convert kernels
+        // must not queue behind GEMM CTAs that occupy every SM
+        TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking,
+                                             static_cast<int>(si) == dc.width ? prio_high : prio_low));
         for (auto& ev : sc.ring) TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
       }
+      for (int k = 0; k < kStage; ++k) TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &dc.stage[k], &dc.stage_cap[k]));
     }
     // Peer access between every pair of distinct GPUs in use (NVLink / NVSwitch).
     for (int d = 0; d < n; ++d) {
@@ -177,6 +184,7 @@ Session::~Session() {
       cudaEventDestroy(t.end);
     }
     DevPool::get().release(dc.gpu, dc.slab, dc.slab_cap);
+    for (int k = 0; k < kStage; ++k) DevPool::get().release(dc.gpu, dc.stage[k], dc.stage_cap[k]);
     cudaEventDestroy(dc.span_start);
     cudaEventDestroy(dc.span_end);
   }
@@ -307,48 +315,76 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
     wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
     return phys;
   }
-  load_slot(d, s, phys, a.level, a.source, key, src, r, c, job);
+  // every fill runs on the device's high-priority fill stream; the task's stream waits for it
+  load_slot(d, dc.width, phys, a.level, a.source, key, src, r, c, job);
+  wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
   return phys;
 }
 
 // Physical side of an L2 hit (peer copy of the converted planes) or a miss
 // (host H2D + split/convert, or device-matrix split/convert) into slot `phys`
 // of device d, on stream s.  Caller holds the directory lock.
-void Session::load_slot(int d, int s, int32_t phys, HitLevel level, int32_t source, const TileKey& key,
-                        const Mat& src, int64_t r, int64_t c, Job& job) {
+void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level, int32_t source,
+                        const TileKey& key, const Mat& src, int64_t r, int64_t c, Job& job) {
   DeviceCtx& dc = devs_[d];
   SlotState& st = dc.slots[phys];
-  const int32_t gs = gs_of(d, s);
-  wait_slot_free(d, s, phys);
-  StreamCtx& sc = dc.streams[s];
+  const int F = dc.width;      // high-priority convert stream (writes slots)
+  const int X = dc.width + 1;  // copy stream (DMA only)
   if (level == HIT_L2) {
+    // peer copy of the already-converted planes, on the copy stream
+    const int32_t gx = gs_of(d, X);
+    wait_slot_free(d, X, phys);
     const int o = source;
     const int32_t src_phys = phys_of(o, dir_->slot_of_locked(o, key));
     SlotState& ss = devs_[o].slots[src_phys];
-    wait_event_if_foreign(d, s, ss.ready_gs, ss.ready_ev);
+    wait_event_if_foreign(d, X, ss.ready_gs, ss.ready_ev);
     const size_t bytes = static_cast<size_t>(slot_elems_ * 2);
+    cudaStream_t xs = dc.streams[X].stream;
     if (devs_[o].gpu == dc.gpu) {
-      TR_CUDA(cudaMemcpyAsync(slot_ptr(d, phys), slot_ptr(o, src_phys), bytes, cudaMemcpyDeviceToDevice, sc.stream));
+      TR_CUDA(cudaMemcpyAsync(slot_ptr(d, phys), slot_ptr(o, src_phys), bytes, cudaMemcpyDeviceToDevice, xs));
     } else {
-      TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, sc.stream));
+      TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, xs));
     }
-    cudaEvent_t ev = record(d, s);
+    cudaEvent_t ev = record(d, X);
     bool found = false;
     for (auto& u : ss.uses)
-      if (u.first == gs) {
+      if (u.first == gx) {
         u.second = ev;
         found = true;
       }
-    if (!found) ss.uses.emplace_back(gs, ev);
-    st.ready_gs = gs;
+    if (!found) ss.uses.emplace_back(gx, ev);
+    st.ready_gs = gx;
     st.ready_ev = ev;
     st.uses.clear();
     return;
   }
-  fill_slot(d, s, phys, src, r, c);
+  const int64_t T = tile_;
+  const int64_t tr_ = std::min(T, src.rows - r * T);
+  const int64_t tc = std::min(T, src.cols - c * T);
+  const int64_t es = src.esize();
+  const char* base = static_cast<const char*>(src.ptr) + (r * T * src.ld + c * T) * es;
+  cudaStream_t fs = dc.streams[F].stream;
+  wait_slot_free(d, F, phys);
+  if (src.location == TR_LOC_HOST) {
+    // H2D into the next staging buffer of the ring on the copy stream; the
+    // convert follows on the fill stream.  The DMA engine runs up to kStage
+    // tiles ahead of the converts (which may wait for SMs busy with GEMMs).
+    const int k = static_cast<int>(dc.stage_next++ % kStage);
+    cudaStream_t xs = dc.streams[X].stream;
+    if (dc.stage_free[k]) TR_CUDA(cudaStreamWaitEvent(xs, dc.stage_free[k], 0));
+    TR_CUDA(cudaMemcpy2DAsync(dc.stage[k], tc * es, base, src.ld * es, tc * es, tr_, cudaMemcpyHostToDevice, xs));
+    cudaEvent_t copied = record(d, X);
+    TR_CUDA(cudaStreamWaitEvent(fs, copied, 0));
+    TR_CUDA(launch_split_convert(dc.stage[k], src.dtype == TR_DTYPE_F64, tc, tr_, tc, slot_ptr(d, phys), ld_, T,
+                                 plane_elems_, planes_, fs));
+    dc.stage_free[k] = record(d, F);
+  } else {
+    TR_CUDA(launch_split_convert(base, src.dtype == TR_DTYPE_F64, src.ld, tr_, tc, slot_ptr(d, phys), ld_, T,
+                                 plane_elems_, planes_, fs));
+  }
   job.launches.fetch_add(1);
-  st.ready_gs = gs;
-  st.ready_ev = record(d, s);
+  st.ready_gs = gs_of(d, F);
+  st.ready_ev = record(d, F);
   st.uses.clear();
 }
 
@@ -359,7 +395,7 @@ void Session::load_slot(int d, int s, int32_t phys, HitLevel level, int32_t sour
 // never evicts and never counts, so the counters are exactly the reference's.
 void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen) {
   DeviceCtx& dc = devs_[d];
-  const int s = dc.width;  // fetch-ahead stream
+  const int s = dc.width;  // the fill stream
   for (uint64_t tid : dc.station->peek()) {
     if (seen[tid]) continue;
     seen[tid] = 1;

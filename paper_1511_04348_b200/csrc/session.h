@@ -90,6 +90,7 @@ class Session {
 
  private:
   static constexpr int kRing = 64;
+  static constexpr int kStage = 4;  // H2D staging ring depth per device
 
   struct SlotState {
     int32_t ready_gs = -1;
@@ -119,8 +120,13 @@ class Session {
     int32_t max_slots = 0;
     CUtensorMap tmap[4];
     std::vector<SlotState> slots;  // indexed by physical slot
+    // [0, width): task streams (station entries); [width]: fill (convert) stream,
+    // highest priority; [width+1]: copy stream (H2D into the staging ring, peer copies)
     std::vector<StreamCtx> streams;
-    std::unique_ptr<Station> station;
+    void* stage[kStage] = {};
+    size_t stage_cap[kStage] = {};
+    cudaEvent_t stage_free[kStage] = {};
+    uint64_t stage_next = 0;    std::unique_ptr<Station> station;
     tr_device_stats stats{};
     std::vector<TimedLaunch> timed, timed_pool;
     double last_kernel_ms = 0;

@@ -107,6 +107,7 @@ class GpuMLP:
             ys.append(y)
             acts.append(a)
             cur, cur_uid = a, self.rt.fresh_uid("x")
+        self._step_uids = list(uids)
         pred = acts[-1]
         d_out = self._buf("dout", pred.shape)
         N.call("tr_mlp_mse_grad", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(), _ptr(self._loss), s)
@@ -117,6 +118,7 @@ class GpuMLP:
             N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), _ptr(ys[li]), _ptr(acts[li]), d_y.numel(),
                    _ACT[L.activation], s)
             dy_uid = self.rt.fresh_uid("dy")
+            self._step_uids.append(dy_uid)
             d_w = self._buf(f"dw{li}", L.w.shape)
             self._mm(xs[li], d_y, d_w, ta=True, a_uid=uids[li], b_uid=dy_uid)
             d_x = self._buf(f"dx{li}", xs[li].shape)
@@ -137,7 +139,10 @@ class GpuMLP:
             N.call("tr_mlp_sgd", _ptr(L.w), _ptr(d_w), L.w.numel(), float(lr), s)
             if L.b is not None:
                 N.call("tr_mlp_sgd", _ptr(L.b), _ptr(d_b), L.b.numel(), float(lr), s)
+            self.rt.forget(L.weight_uid)  # this version is dead after the update
             L.version += 1
+        for uid in self._step_uids:  # this step's activations and gradients are dead too
+            self.rt.forget(uid)
         return float(self._loss.item()) / n
 
     def to_host(self):

@@ -433,6 +433,12 @@ class Runtime:
         code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2}[order]
         N.call("tr_session_set_order", self._h, code)
 
+    def forget(self, uid) -> int:
+        """Drop every cached tile of matrix ``uid`` (its content is dead); returns the count."""
+        n = N.i64()
+        N.call("tr_session_forget", self._h, self._uids.id(uid), C.byref(n))
+        return n.value
+
     def fresh_uid(self, prefix: str = "m") -> str:
         self._uid_n += 1
         return f"{prefix}#{self._uid_n}"
