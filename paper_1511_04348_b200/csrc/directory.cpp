@@ -196,39 +196,49 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
     r.nbytes = nbytes;
     return r;
   }
-  int32_t owner = -1;
-  const HitLevel lvl = lookup_locked(requester, key, &owner);
-  if (lvl == HIT_L1) {
+  // Classification (coherence.py:124-134) over COUNTED owners: a tile some device
+  // holds only as an unclaimed fetch-ahead is, for the counters, not resident yet
+  // -- exactly as in a run without fetch-ahead.
+  auto it = residency_.find(key);
+  const uint64_t owners = it == residency_.end() ? 0 : it->second;
+  uint64_t counted = 0;
+  for (int o = 0; o < n_; ++o)
+    if ((owners >> o & 1) && !dev_[o].entries.at(key).pending) counted |= 1ull << o;
+  const uint64_t others = counted & ~(1ull << requester);
+  if (owners >> requester & 1) {
     Entry& e = d.entries.at(key);
+    if (policy_ == TR_POLICY_LRU) d.order.splice(d.order.end(), d.order, e.pos);
     d.pins[key] += 1;
     r.slot = e.slot;
-    if (e.pending) {
-      // first request of a fetched-ahead tile: count what the fetch was
-      r.prefetched = true;
-      r.nbytes = nbytes;
-      if (e.pending - 1 == HIT_L2) {
-        stats_.l2_hits += 1;
-        ds.l2_hits += 1;
-        stats_.bytes_peer += nbytes;
-        ds.bytes_peer += nbytes;
-        r.level = HIT_L2;
-      } else {
-        stats_.host_fetches += 1;
-        ds.host_fetches += 1;
-        stats_.bytes_host += nbytes;
-        ds.bytes_host += nbytes;
-        r.level = HIT_MISS;
-      }
-      e.pending = 0;
+    if (!e.pending) {
+      stats_.l1_hits += 1;
+      ds.l1_hits += 1;
+      r.level = HIT_L1;
+      r.source = requester;
       return r;
     }
-    stats_.l1_hits += 1;
-    ds.l1_hits += 1;
-    r.level = HIT_L1;
-    r.source = requester;
+    // first request of a fetched-ahead tile: count it as the request would have
+    // been counted without the fetch-ahead (peer copy if a counted owner exists)
+    r.prefetched = true;
+    r.nbytes = nbytes;
+    e.pending = 0;
+    if (others) {
+      stats_.l2_hits += 1;
+      ds.l2_hits += 1;
+      stats_.bytes_peer += nbytes;
+      ds.bytes_peer += nbytes;
+      r.level = HIT_L2;
+      r.source = closest_owner(requester, others);
+    } else {
+      stats_.host_fetches += 1;
+      ds.host_fetches += 1;
+      stats_.bytes_host += nbytes;
+      ds.bytes_host += nbytes;
+      r.level = HIT_MISS;
+    }
     return r;
   }
-  if (lvl == HIT_L2) {
+  if (others) {
     // counters before admit, as coherence.py:233-237 does
     stats_.l2_hits += 1;
     ds.l2_hits += 1;
@@ -237,7 +247,8 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
     r.evicted = admit_locked(requester, key, true, &r.slot);
     d.pins[key] += 1;
     r.level = HIT_L2;
-    r.source = owner;
+    r.source = closest_owner(requester, others);
+    r.phys_source = r.source;
     r.nbytes = nbytes;
     return r;
   }
@@ -248,10 +259,14 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
   r.evicted = admit_locked(requester, key, true, &r.slot);
   d.pins[key] += 1;
   r.nbytes = nbytes;
+  // counted as a host fetch; physically, another device's in-flight fetch-ahead
+  // copy (if any) is closer than the host
+  const uint64_t pend = owners & ~(1ull << requester);
+  if (pend) r.phys_source = closest_owner(requester, pend);
   return r;
 }
 
-bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, HitLevel* level, int32_t* source) {
+bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source) {
   if (!enabled_ || host_worker_[device]) return false;
   Dev& d = dev_[device];
   if (d.entries.count(key)) return false;
@@ -259,10 +274,9 @@ bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, H
   if (slot_total_[device] > 0 && d.free_slots.empty()) return false;
   auto it = residency_.find(key);
   const uint64_t owners = it == residency_.end() ? 0 : it->second;
-  *level = owners ? HIT_L2 : HIT_MISS;
-  *source = owners ? closest_owner(device, owners) : TR_SOURCE_HOST;
+  *phys_source = owners ? closest_owner(device, owners) : TR_SOURCE_HOST;
   admit_locked(device, key, true, slot);  // cannot evict: checked above
-  d.entries.at(key).pending = static_cast<int8_t>(*level + 1);
+  d.entries.at(key).pending = 1;
   return true;
 }
 

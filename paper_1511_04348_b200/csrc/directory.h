@@ -47,6 +47,10 @@ struct Acquired {
   int32_t slot;    // physical slot on the requester (-1: none / bypass)
   std::vector<TileKey> evicted;
   bool prefetched = false;  // counted as `level` but already resident (filled ahead of the request)
+  // Physical source of the bytes when the requester is not resident: a device id
+  // (peer copy) or TR_SOURCE_HOST.  Differs from `source` only when the tile is
+  // counted as a host fetch but another device already holds a fetch-ahead copy.
+  int32_t phys_source = TR_SOURCE_HOST;
 };
 
 class Directory {
@@ -85,8 +89,9 @@ class Directory {
   // is already resident, the device is full, or coherence is off).  The first
   // acquire_input of the tile on `device` is then counted exactly as it would
   // have been without the prefetch (host fetch, or L2 hit), so every counter
-  // keeps the reference's meaning.  *level/*source say where to copy from.
-  bool prefetch_locked(int device, const TileKey& key, int32_t* slot, HitLevel* level, int32_t* source);
+  // keeps the reference's meaning: requests classify against COUNTED owners
+  // only.  *phys_source says where to copy from (a device id or host).
+  bool prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source);
   void release_output_locked(int device, const TileKey& key, int64_t nbytes);
   // Drop every unpinned resident tile of matrix `uid` on every device (the
   // content is dead, e.g. a retired weight version).  Not an eviction; no
@@ -105,7 +110,7 @@ class Directory {
   struct Entry {
     std::list<TileKey>::iterator pos;
     int32_t slot;
-    int8_t pending = 0;  // fetched ahead, not yet requested: HIT_MISS or HIT_L2 + 1
+    int8_t pending = 0;  // 1: fetched ahead, not yet requested on this device (uncounted)
   };
   struct Dev {
     std::list<TileKey> order;  // LRU order, most recent at the back

@@ -315,8 +315,8 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
     wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
     return phys;
   }
-  // every fill runs on the device's high-priority fill stream; the task's stream waits for it
-  load_slot(d, dc.width, phys, a.level, a.source, key, src, r, c, job);
+  // every fill runs on the device's fill/copy streams; the task's stream waits for it
+  load_slot(d, dc.width, phys, a.phys_source >= 0 ? HIT_L2 : HIT_MISS, a.phys_source, key, src, r, c, job);
   wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
   return phys;
 }
@@ -409,10 +409,9 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen) {
         const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
         const TileKey key{uid, r, c};
         std::lock_guard<std::mutex> g(dir_->mu);
-        int32_t slot = -1, source = -1;
-        HitLevel level;
-        if (!dir_->prefetch_locked(d, key, &slot, &level, &source)) continue;
-        load_slot(d, s, phys_of(d, slot), level, source, key, m, r, c, job);
+        int32_t slot = -1, source = TR_SOURCE_HOST;
+        if (!dir_->prefetch_locked(d, key, &slot, &source)) continue;
+        load_slot(d, s, phys_of(d, slot), source >= 0 ? HIT_L2 : HIT_MISS, source, key, m, r, c, job);
       }
     }
   }
