@@ -225,9 +225,11 @@ int tr_session_set_inflight(tr_session* s, int32_t max_inflight);
 /* Order in which tr_gemm enqueues task ids: 0 = row-major (the reference's,
  * scheduler.py:189-192), 1 = banded (pairs of task rows walked column by
  * column), 2 = shells (tasks with max(i,j) = s before shell s+1: first-touch
- * host traffic spread over the run), -1 = auto (default: shells unless some
- * device has a bounded capacity, where LRU eviction sequences -- and so the
- * counters -- depend on the order). */
+ * host traffic spread over the run), 3 = blocked (b x b task blocks whose
+ * 2b k-panels fit the smallest device tile budget: out-of-core reuse),
+ * -1 = auto (default): row-major if some device has a bounded capacity (LRU
+ * eviction sequences -- and so the counters -- then match the reference),
+ * blocked if A+B exceed the HBM tile budget, shells otherwise. */
 int tr_session_set_order(tr_session* s, int32_t order);
 /* Sessions return HBM slabs/staging buffers to a process-wide cache reused by
  * later sessions; this frees every cached block. */

@@ -693,10 +693,19 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   // over the run instead of loading every B panel during the first task row.
   const int64_t total = job.grid_rows * job.grid_cols;
   int order = order_;
+  const int64_t a_tiles_all = ceil_div(a.rows, T) * ceil_div(a.cols, T);
+  const int64_t b_tiles_all = ceil_div(b.rows, T) * ceil_div(b.cols, T);
+  int64_t room = INT64_MAX;  // smallest tile budget of any device
+  for (auto& dc : devs_) {
+    const int64_t cap = dc.capacity >= 0 ? dc.capacity : (dryrun_ ? INT64_MAX : dc.max_slots);
+    room = std::min(room, cap);
+  }
   if (order < 0) {
-    order = 2;
-    for (auto& dc : devs_)
-      if (dc.capacity >= 0) order = 0;
+    bool bounded = false;
+    for (auto& dc : devs_) bounded = bounded || dc.capacity >= 0;
+    if (bounded) order = 0;                                    // reference order: exact LRU parity
+    else if (a_tiles_all + b_tiles_all > room) order = 3;      // out-of-core: blocked
+    else order = 2;                                            // in-core: shells
   }
   std::vector<int64_t> ids;
   ids.reserve(static_cast<size_t>(total));
@@ -715,6 +724,15 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
       if (sh < job.grid_rows)
         for (int64_t j = 0; j <= std::min(sh, job.grid_cols - 1); ++j) ids.push_back(sh * job.grid_cols + j);
     }
+  } else if (order == 3) {
+    // blocked: b x b task blocks whose (b + b) k-panels fit the tile budget, so
+    // each A/B tile is fetched once per block instead of once per task row
+    const int64_t ks = std::max<int64_t>(1, job.k_steps);
+    const int64_t bsz = std::max<int64_t>(1, (room == INT64_MAX ? total : (room - 8)) / (2 * ks));
+    for (int64_t bi = 0; bi < job.grid_rows; bi += bsz)
+      for (int64_t bj = 0; bj < job.grid_cols; bj += bsz)
+        for (int64_t i = bi; i < std::min(bi + bsz, job.grid_rows); ++i)
+          for (int64_t j = bj; j < std::min(bj + bsz, job.grid_cols); ++j) ids.push_back(i * job.grid_cols + j);
   } else {
     for (int64_t t = 0; t < total; ++t) ids.push_back(t);
   }

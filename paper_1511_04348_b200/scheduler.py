@@ -429,8 +429,8 @@ class Runtime:
         N.call("tr_session_set_inflight", self._h, int(max_inflight))
 
     def set_order(self, order: str) -> None:
-        """Task enqueue order: "row-major" (reference), "banded", "shells", or "auto"."""
-        code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2}[order]
+        """Task enqueue order: "row-major" (reference), "banded", "shells", "blocked", or "auto"."""
+        code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2, "blocked": 3}[order]
         N.call("tr_session_set_order", self._h, code)
 
     def forget(self, uid) -> int:

@@ -250,3 +250,14 @@ def test_reports(tmp_path):
     write_report_csv(s, tmp_path / "r.csv")
     rows = (tmp_path / "r.csv").read_text().strip().splitlines()
     assert rows[0].startswith("device_id,kind,tasks_completed") and rows[-1].startswith("total")
+
+
+@pytest.mark.parametrize("order", ["row-major", "banded", "shells", "blocked"])
+def test_every_order_plans_the_same_task_set(order):
+    """Enqueue order is a scheduling choice only: the task set, exactly-once and
+    the first-touch identity hold for every order (unbounded capacity)."""
+    rt = Runtime(homogeneous_machine(3), 4, mode="dryrun")
+    rt.set_order(order)
+    _, s = rt.multiply(np.zeros((28, 20)), np.zeros((20, 36)), a_uid="A", b_uid="B")
+    assert s.total_tasks == 7 * 9 and sum(s.tasks_by_device.values()) == 63
+    assert s.cache.host_fetches == 7 * 5 + 5 * 9 and s.cache.input_requests == 2 * 63 * 5
