@@ -155,7 +155,8 @@ enum {
   TR_FLAG_DEBUG = 1u << 2,     /* Runtime(directory_debug=True): invariants per mutation */
   TR_FLAG_DRYRUN = 1u << 3,    /* schedule-only test mode: no CUDA, no arithmetic, C untouched */
   TR_FLAG_FIFO = 1u << 4,      /* FIFO eviction instead of LRU                          */
-  TR_FLAG_NO_PREFETCH = 1u << 5 /* disable fetch-ahead of reserved tasks' input tiles   */
+  TR_FLAG_NO_PREFETCH = 1u << 5, /* disable fetch-ahead of reserved tasks' input tiles  */
+  TR_FLAG_TRACE = 1u << 6       /* record a device timeline of every copy/kernel (tr_session_trace) */
 };
 
 typedef struct {
@@ -215,6 +216,18 @@ int tr_gemm_shard(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t tra
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
  * measured with CUDA events on the launching streams (sum over launches). */
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms /* n_devices */);
+/* Timeline of the last tr_gemm (sessions created with TR_FLAG_TRACE): one entry
+ * per H2D tile copy, split/convert, peer copy, GEMM launch and D2H writeback,
+ * with CUDA-event times in ms relative to the product's start on that device. */
+typedef enum { TR_TRACE_H2D = 0, TR_TRACE_CONVERT = 1, TR_TRACE_PEER = 2, TR_TRACE_GEMM = 3, TR_TRACE_D2H = 4 } tr_trace_kind;
+typedef struct {
+  int32_t device, kind, stream;
+  int64_t task;           /* task id (GEMM, D2H) or -1 */
+  uint64_t matrix;        /* tile uid (copies, converts) or 0 */
+  int64_t row, col;
+  double start_ms, end_ms;
+} tr_trace_event;
+int tr_session_trace(tr_session* s, tr_trace_event* out, int64_t cap, int64_t* n);
 /* Device-side span (ms) of the last tr_gemm on each device: CUDA events recorded
  * before the first and after the last operation of every worker stream. */
 int tr_session_span_ms(tr_session* s, double* per_device_ms /* n_devices */);

@@ -26,7 +26,8 @@ TR_HIT_L1, TR_HIT_L2, TR_HIT_MISS = 0, 1, 2
 TR_SOURCE_HOST = -1
 TR_KIND_ACCELERATOR, TR_KIND_HOST_WORKER = 0, 1
 TR_ACT_IDENTITY, TR_ACT_SIGMOID, TR_ACT_RELU = 0, 1, 2
-TR_FLAG_STEAL, TR_FLAG_COHERENCE, TR_FLAG_DEBUG, TR_FLAG_DRYRUN, TR_FLAG_FIFO, TR_FLAG_NO_PREFETCH = 1, 2, 4, 8, 16, 32
+TR_FLAG_STEAL, TR_FLAG_COHERENCE, TR_FLAG_DEBUG, TR_FLAG_DRYRUN, TR_FLAG_FIFO, TR_FLAG_NO_PREFETCH, TR_FLAG_TRACE = \
+    1, 2, 4, 8, 16, 32, 64
 
 i32, i64, u64, u8, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint8, C.c_double
 P = C.POINTER
@@ -65,6 +66,14 @@ class DeviceStatsC(C.Structure):
 
 class StealEventC(C.Structure):
     _fields_ = [("thief", i32), ("victim", i32), ("task_id", i64)]
+
+
+class TraceEventC(C.Structure):
+    _fields_ = [("device", i32), ("kind", i32), ("stream", i32), ("task", i64), ("matrix", u64), ("row", i64),
+                ("col", i64), ("start_ms", f64), ("end_ms", f64)]
+
+
+TRACE_KINDS = ("h2d", "convert", "peer", "gemm", "d2h")
 
 
 class GemmReportC(C.Structure):
@@ -114,6 +123,7 @@ _PROTOS = {
                       P(GemmReportC)],
     "tr_session_kernel_ms": [vp, P(f64)],
     "tr_session_span_ms": [vp, P(f64)],
+    "tr_session_trace": [vp, vp, i64, P(i64)],
     "tr_session_set_inflight": [vp, i32],
     "tr_session_set_order": [vp, i32],
     "tr_release_cached_memory": [],

@@ -315,6 +315,13 @@ int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t ta, const
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms) {
   return guarded([&] { s->s->kernel_ms(per_device_ms); });
 }
+int tr_session_trace(tr_session* s, tr_trace_event* out, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    const auto& t = s->s->trace();
+    for (int64_t i = 0; i < cap && i < static_cast<int64_t>(t.size()); ++i) out[i] = t[static_cast<size_t>(i)];
+    *n = static_cast<int64_t>(t.size());
+  });
+}
 int tr_session_span_ms(tr_session* s, double* per_device_ms) {
   return guarded([&] { s->s->span_ms(per_device_ms); });
 }

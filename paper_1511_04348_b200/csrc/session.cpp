@@ -58,6 +58,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   dryrun_ = flags & TR_FLAG_DRYRUN;
   steal_ = flags & TR_FLAG_STEAL;
   coherence_ = flags & TR_FLAG_COHERENCE;
+  tracing_ = (flags & TR_FLAG_TRACE) && !(flags & TR_FLAG_DRYRUN);
   element_bytes_ = m.element_bytes > 0 ? m.element_bytes : 8;
   planes_ = precision == TR_PREC_FP32ACC ? 2 : 1;
   ld_ = ceil_div(tile, 8) * 8;
@@ -253,6 +254,34 @@ cudaEvent_t Session::record(int d, int s) {
   return ev;
 }
 
+Session::TimedLaunch Session::timing_pair(int d) {
+  DeviceCtx& dc = devs_[d];
+  TimedLaunch tl;
+  if (!dc.timed_pool.empty()) {
+    tl = dc.timed_pool.back();
+    dc.timed_pool.pop_back();
+  } else {
+    TR_CUDA(cudaEventCreate(&tl.start));
+    TR_CUDA(cudaEventCreate(&tl.end));
+  }
+  return tl;
+}
+
+void Session::trace_begin(int d, int s, TimedLaunch* t) {
+  if (!tracing_) return;
+  *t = timing_pair(d);
+  TR_CUDA(cudaEventRecord(t->start, devs_[d].streams[s].stream));
+}
+
+void Session::trace_end(int d, int s, TimedLaunch t, int kind, int64_t task, uint64_t uid, int64_t r, int64_t c) {
+  if (!tracing_) return;
+  TR_CUDA(cudaEventRecord(t.end, devs_[d].streams[s].stream));
+  TraceRec rec;
+  rec.ev = tr_trace_event{d, kind, s, task, uid, r, c, 0.0, 0.0};
+  rec.t = t;
+  devs_[d].trace.push_back(rec);
+}
+
 void Session::wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev) {
   if (gs < 0 || gs == gs_of(d, s)) return;  // same stream: already ordered
   TR_CUDA(cudaStreamWaitEvent(devs_[d].streams[s].stream, ev, 0));
@@ -340,11 +369,14 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     wait_event_if_foreign(d, X, ss.ready_gs, ss.ready_ev);
     const size_t bytes = static_cast<size_t>(slot_elems_ * 2);
     cudaStream_t xs = dc.streams[X].stream;
+    TimedLaunch tt{};
+    trace_begin(d, X, &tt);
     if (devs_[o].gpu == dc.gpu) {
       TR_CUDA(cudaMemcpyAsync(slot_ptr(d, phys), slot_ptr(o, src_phys), bytes, cudaMemcpyDeviceToDevice, xs));
     } else {
       TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, xs));
     }
+    trace_end(d, X, tt, TR_TRACE_PEER, -1, key.matrix, key.row, key.col);
     cudaEvent_t ev = record(d, X);
     bool found = false;
     for (auto& u : ss.uses)
@@ -372,15 +404,23 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     const int k = static_cast<int>(dc.stage_next++ % kStage);
     cudaStream_t xs = dc.streams[X].stream;
     if (dc.stage_free[k]) TR_CUDA(cudaStreamWaitEvent(xs, dc.stage_free[k], 0));
+    TimedLaunch tc1{}, tc2{};
+    trace_begin(d, X, &tc1);
     TR_CUDA(cudaMemcpy2DAsync(dc.stage[k], tc * es, base, src.ld * es, tc * es, tr_, cudaMemcpyHostToDevice, xs));
+    trace_end(d, X, tc1, TR_TRACE_H2D, -1, key.matrix, key.row, key.col);
     cudaEvent_t copied = record(d, X);
     TR_CUDA(cudaStreamWaitEvent(fs, copied, 0));
+    trace_begin(d, F, &tc2);
     TR_CUDA(launch_split_convert(dc.stage[k], src.dtype == TR_DTYPE_F64, tc, tr_, tc, slot_ptr(d, phys), ld_, T,
                                  plane_elems_, planes_, fs));
+    trace_end(d, F, tc2, TR_TRACE_CONVERT, -1, key.matrix, key.row, key.col);
     dc.stage_free[k] = record(d, F);
   } else {
+    TimedLaunch tc2{};
+    trace_begin(d, F, &tc2);
     TR_CUDA(launch_split_convert(base, src.dtype == TR_DTYPE_F64, src.ld, tr_, tc, slot_ptr(d, phys), ld_, T,
                                  plane_elems_, planes_, fs));
+    trace_end(d, F, tc2, TR_TRACE_CONVERT, -1, key.matrix, key.row, key.col);
   }
   job.launches.fetch_add(1);
   st.ready_gs = gs_of(d, F);
@@ -481,18 +521,18 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     if (!dryrun_) {
       BoxKind ba, bb;
       gemm_boxes(job.ta, job.tb, args.m_valid, &ba, &bb);
-      TimedLaunch tl;
-      if (!dc.timed_pool.empty()) {
-        tl = dc.timed_pool.back();
-        dc.timed_pool.pop_back();
-      } else {
-        TR_CUDA(cudaEventCreate(&tl.start));
-        TR_CUDA(cudaEventCreate(&tl.end));
-      }
+      TimedLaunch tl = timing_pair(d);
       TR_CUDA(cudaEventRecord(tl.start, scp->stream));
       TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, job.ta, job.tb, scp->stream));
       TR_CUDA(cudaEventRecord(tl.end, scp->stream));
       dc.timed.push_back(tl);
+      if (tracing_) {
+        // the launch's own timing pair (dc.timed) provides the times; remember its index
+        TraceRec rec;
+        rec.ev = tr_trace_event{d, TR_TRACE_GEMM, s, tid, static_cast<uint64_t>(dc.timed.size() - 1), i, j, 0.0, 0.0};
+        rec.t = TimedLaunch{nullptr, nullptr};
+        dc.trace.push_back(rec);
+      }
       job.launches.fetch_add(1);
     }
     {
@@ -517,8 +557,11 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
   const int64_t wb_bytes = mt * nt * element_bytes_;
   if (!dryrun_ && job.c.location == TR_LOC_HOST) {
     char* dst = const_cast<char*>(static_cast<const char*>(job.c.ptr)) + (i * T * job.c.ld + j * T) * ces;
+    TimedLaunch tw{};
+    trace_begin(d, s, &tw);
     TR_CUDA(cudaMemcpy2DAsync(dst, job.c.ld * ces, scp->outbuf, nt * ces, nt * ces, mt, cudaMemcpyDeviceToHost,
                               scp->stream));
+    trace_end(d, s, tw, TR_TRACE_D2H, tid, job.c_uid, i, j);
   }
   {
     std::lock_guard<std::mutex> g(dir_->mu);
@@ -813,6 +856,30 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
     }
   }
   const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  // trace (before the timing events are recycled)
+  last_trace_.clear();
+  if (tracing_) {
+    for (auto& dc : devs_) {
+      for (auto& rec : dc.trace) {
+        float a = 0, b = 0;
+        if (rec.ev.kind == TR_TRACE_GEMM) {
+          const TimedLaunch& tl = dc.timed[static_cast<size_t>(rec.ev.matrix)];
+          rec.ev.matrix = 0;
+          cudaEventElapsedTime(&a, dc.span_start, tl.start);
+          cudaEventElapsedTime(&b, dc.span_start, tl.end);
+        } else {
+          cudaEventElapsedTime(&a, dc.span_start, rec.t.start);
+          cudaEventElapsedTime(&b, dc.span_start, rec.t.end);
+          dc.timed_pool.push_back(rec.t);
+        }
+        cudaGetLastError();
+        rec.ev.start_ms = a;
+        rec.ev.end_ms = b;
+        last_trace_.push_back(rec.ev);
+      }
+      dc.trace.clear();
+    }
+  }
   // kernel timings
   for (auto& dc : devs_) {
     double ms = 0;

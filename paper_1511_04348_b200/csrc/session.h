@@ -87,6 +87,7 @@ class Session {
   void set_inflight(int n);
   void set_order(int order) { order_ = order; }
   void set_external_stream(cudaStream_t s) { ext_stream_ = s; }
+  const std::vector<tr_trace_event>& trace() const { return last_trace_; }
 
  private:
   static constexpr int kRing = 64;
@@ -111,6 +112,10 @@ class Session {
   struct TimedLaunch {
     cudaEvent_t start, end;
   };
+  struct TraceRec {
+    tr_trace_event ev;
+    TimedLaunch t;
+  };
   struct DeviceCtx {
     int id = 0, gpu = 0, width = 4, max_inflight = 2;
     int64_t capacity = -1;
@@ -129,6 +134,7 @@ class Session {
     uint64_t stage_next = 0;    std::unique_ptr<Station> station;
     tr_device_stats stats{};
     std::vector<TimedLaunch> timed, timed_pool;
+    std::vector<TraceRec> trace;
     double last_kernel_ms = 0;
     int64_t last_launches = 0;
     double last_span_ms = 0;
@@ -151,6 +157,10 @@ class Session {
   cudaEvent_t record(int d, int s);
   int32_t gs_of(int d, int s) const { return d * 64 + s; }
   void reap(int d, Job& job, bool block_oldest);
+  // tracing (TR_FLAG_TRACE): bracket an async operation with timing events
+  TimedLaunch timing_pair(int d);
+  void trace_begin(int d, int s, TimedLaunch* t);
+  void trace_end(int d, int s, TimedLaunch t, int kind, int64_t task, uint64_t uid, int64_t r, int64_t c);
 
   // session-side
   void ensure_slab(int d, int64_t needed);
@@ -172,6 +182,8 @@ class Session {
   int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, 2 shells, -1 auto
   cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
   cudaEvent_t ext_ready_ = nullptr;
+  bool tracing_ = false;
+  std::vector<tr_trace_event> last_trace_;
   std::unique_ptr<Directory> dir_;
   std::vector<DeviceCtx> devs_;
   std::vector<Station*> station_ptrs_;

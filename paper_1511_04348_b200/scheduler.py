@@ -298,6 +298,7 @@ class RunStats:
     gpu_launches: int = 0
     kernel_ms: dict[int, float] = field(default_factory=dict)  # sum of tile-GEMM kernel durations
     span_ms: dict[int, float] = field(default_factory=dict)  # device-side span of the product
+    trace: list = field(default_factory=list)  # Runtime(trace=True): device timeline of the product
 
     @property
     def tasks_by_device(self) -> dict[int, int]:
@@ -376,7 +377,7 @@ class Runtime:
     def __init__(self, machine: Machine, tile_size: int, mode: str = "gpu", steal: bool = True,
                  coherence: bool = True, seed: int | None = None, directory_debug: bool = False,
                  precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru",
-                 fetch_ahead: bool = True):
+                 fetch_ahead: bool = True, trace: bool = False):
         if mode not in MODES:
             if mode == "sim":
                 raise ValueError("mode 'sim' is the reference's simulated engine; the B200 runtime executes on "
@@ -396,6 +397,8 @@ class Runtime:
         flags |= N.TR_FLAG_DRYRUN if mode == "dryrun" else 0
         flags |= N.TR_FLAG_FIFO if policy == "fifo" else 0
         flags |= 0 if fetch_ahead else N.TR_FLAG_NO_PREFETCH
+        flags |= N.TR_FLAG_TRACE if trace else 0
+        self.tracing = trace
         mc, keep = machine._as_c()
         h = C.c_void_p()
         N.call("tr_session_create", C.byref(mc), int(tile_size), precision_code(precision), flags,
@@ -496,6 +499,7 @@ class Runtime:
             N.call("tr_session_kernel_ms", self._h, kms)
             span = (N.f64 * n)()
             N.call("tr_session_span_ms", self._h, span)
+            trace = self._read_trace() if self.tracing else []
         done = [bool(completion[t]) for t in range(total)]
         want = [t % task_stride == task_offset for t in range(total)]
         if done != want:
@@ -515,8 +519,22 @@ class Runtime:
             precision=self.precision, gpu_launches=int(rep.gpu_launches),
             kernel_ms={d: float(kms[d]) for d in range(n)},
             span_ms={d: float(span[d]) for d in range(n)},
+            trace=trace,
         )
         return out, stats
+
+    def _read_trace(self) -> list[dict]:
+        n = N.i64()
+        N.call("tr_session_trace", self._h, None, 0, C.byref(n))
+        buf = (N.TraceEventC * max(1, n.value))()
+        N.call("tr_session_trace", self._h, buf, n.value, C.byref(n))
+        out = []
+        for k in range(n.value):
+            e = buf[k]
+            out.append({"device": e.device, "kind": N.TRACE_KINDS[e.kind], "stream": e.stream, "task": e.task,
+                        "tile": (self._uids.uid(e.matrix) if e.matrix else None, e.row, e.col),
+                        "start_ms": e.start_ms, "end_ms": e.end_ms})
+        return out
 
     @staticmethod
     def _prep(x):
