@@ -266,7 +266,7 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
   return r;
 }
 
-bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source) {
+bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source, bool host_only) {
   if (!enabled_ || host_worker_[device]) return false;
   Dev& d = dev_[device];
   if (d.entries.count(key)) return false;
@@ -274,6 +274,7 @@ bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, i
   if (slot_total_[device] > 0 && d.free_slots.empty()) return false;
   auto it = residency_.find(key);
   const uint64_t owners = it == residency_.end() ? 0 : it->second;
+  if (host_only && owners) return false;
   *phys_source = owners ? closest_owner(device, owners) : TR_SOURCE_HOST;
   admit_locked(device, key, true, slot);  // cannot evict: checked above
   d.entries.at(key).pending = 1;

@@ -91,7 +91,7 @@ class Directory {
   // have been without the prefetch (host fetch, or L2 hit), so every counter
   // keeps the reference's meaning: requests classify against COUNTED owners
   // only.  *phys_source says where to copy from (a device id or host).
-  bool prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source);
+  bool prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source, bool host_only = false);
   void release_output_locked(int device, const TileKey& key, int64_t nbytes);
   // Drop every unpinned resident tile of matrix `uid` on every device (the
   // content is dead, e.g. a retired weight version).  Not an eviction; no

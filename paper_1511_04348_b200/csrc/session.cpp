@@ -132,7 +132,6 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
         // must not queue behind GEMM CTAs that occupy every SM
         TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking,
                                              static_cast<int>(si) == dc.width ? prio_high : prio_low));
-        for (auto& ev : sc.ring) TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
@@ -170,7 +169,7 @@ Session::~Session() {
     cudaSetDevice(dc.gpu);
     cudaDeviceSynchronize();
     for (auto& sc : dc.streams) {
-      for (auto& ev : sc.ring) cudaEventDestroy(ev);
+      for (auto& ev : sc.evs) cudaEventDestroy(ev);
       cudaEventDestroy(sc.done);
       DevPool::get().release(dc.gpu, sc.staging, sc.staging_cap);
       DevPool::get().release(dc.gpu, sc.outbuf, sc.outbuf_cap);
@@ -247,11 +246,36 @@ void Session::ensure_slab(int d, int64_t needed) {
 }
 
 // ---------------------------------------------------------------- events / ordering
-cudaEvent_t Session::record(int d, int s) {
+Session::EvRef Session::record(int d, int s) {
   StreamCtx& sc = devs_[d].streams[s];
-  cudaEvent_t ev = sc.ring[sc.next++ % kRing];
-  TR_CUDA(cudaEventRecord(ev, sc.stream));
-  return ev;
+  int32_t idx = -1;
+  if (!sc.fifo.empty()) {
+    const cudaError_t q = cudaEventQuery(sc.evs[sc.fifo.front()]);
+    if (q == cudaSuccess) {
+      idx = sc.fifo.front();
+      sc.fifo.pop_front();
+    } else if (q != cudaErrorNotReady) {
+      TR_CUDA(q);
+    }
+  }
+  if (idx < 0) {
+    cudaEvent_t ev;
+    TR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    idx = static_cast<int32_t>(sc.evs.size());
+    sc.evs.push_back(ev);
+    sc.gen.push_back(0);
+  }
+  sc.gen[idx] += 1;
+  TR_CUDA(cudaEventRecord(sc.evs[idx], sc.stream));
+  sc.fifo.push_back(idx);
+  return EvRef{gs_of(d, s), idx, sc.gen[idx]};
+}
+
+void Session::wait_on(int d, int s, const EvRef& r) {
+  if (r.gs < 0 || r.gs == gs_of(d, s)) return;  // none, or same stream: already ordered
+  StreamCtx& src = devs_[r.gs / 64].streams[r.gs % 64];
+  if (src.gen[r.idx] != r.gen) return;  // the event was recycled: that point completed
+  TR_CUDA(cudaStreamWaitEvent(devs_[d].streams[s].stream, src.evs[r.idx], 0));
 }
 
 Session::TimedLaunch Session::timing_pair(int d) {
@@ -282,17 +306,21 @@ void Session::trace_end(int d, int s, TimedLaunch t, int kind, int64_t task, uin
   devs_[d].trace.push_back(rec);
 }
 
-void Session::wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev) {
-  if (gs < 0 || gs == gs_of(d, s)) return;  // same stream: already ordered
-  TR_CUDA(cudaStreamWaitEvent(devs_[d].streams[s].stream, ev, 0));
+void Session::note_use(SlotState& st, const EvRef& r) {
+  for (auto& u : st.uses)
+    if (u.gs == r.gs) {
+      u = r;
+      return;
+    }
+  st.uses.push_back(r);
 }
 
 // Before overwriting physical slot `phys` of device d from stream s: every other
 // stream that read it (kernels, peer copies) or is still filling it must be done.
 void Session::wait_slot_free(int d, int s, int32_t phys) {
   SlotState& st = devs_[d].slots[phys];
-  wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
-  for (auto& u : st.uses) wait_event_if_foreign(d, s, u.first, u.second);
+  wait_on(d, s, st.ready);
+  for (auto& u : st.uses) wait_on(d, s, u);
 }
 
 // Miss path: host (pinned) -> staging -> split/convert into the slot, or
@@ -339,14 +367,15 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
   DeviceCtx& dc = devs_[d];
   const int32_t phys = phys_of(d, a.slot);
   SlotState& st = dc.slots[phys];
+  if (a.prefetched && dc.pending_prefetch > 0) dc.pending_prefetch -= 1;  // claimed a fetched-ahead tile
   if (a.level == HIT_L1 || a.prefetched) {
     // resident (possibly still being filled ahead of time on another stream)
-    wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
+    wait_on(d, s, st.ready);
     return phys;
   }
   // every fill runs on the device's fill/copy streams; the task's stream waits for it
   load_slot(d, dc.width, phys, a.phys_source >= 0 ? HIT_L2 : HIT_MISS, a.phys_source, key, src, r, c, job);
-  wait_event_if_foreign(d, s, st.ready_gs, st.ready_ev);
+  wait_on(d, s, st.ready);
   return phys;
 }
 
@@ -361,12 +390,11 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
   const int X = dc.width + 1;  // copy stream (DMA only)
   if (level == HIT_L2) {
     // peer copy of the already-converted planes, on the copy stream
-    const int32_t gx = gs_of(d, X);
     wait_slot_free(d, X, phys);
     const int o = source;
     const int32_t src_phys = phys_of(o, dir_->slot_of_locked(o, key));
     SlotState& ss = devs_[o].slots[src_phys];
-    wait_event_if_foreign(d, X, ss.ready_gs, ss.ready_ev);
+    wait_on(d, X, ss.ready);
     const size_t bytes = static_cast<size_t>(slot_elems_ * 2);
     cudaStream_t xs = dc.streams[X].stream;
     TimedLaunch tt{};
@@ -377,16 +405,9 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
       TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, xs));
     }
     trace_end(d, X, tt, TR_TRACE_PEER, -1, key.matrix, key.row, key.col);
-    cudaEvent_t ev = record(d, X);
-    bool found = false;
-    for (auto& u : ss.uses)
-      if (u.first == gx) {
-        u.second = ev;
-        found = true;
-      }
-    if (!found) ss.uses.emplace_back(gx, ev);
-    st.ready_gs = gx;
-    st.ready_ev = ev;
+    const EvRef ev = record(d, X);
+    note_use(ss, ev);  // the source cannot be refilled under the copy
+    st.ready = ev;
     st.uses.clear();
     return;
   }
@@ -403,13 +424,12 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     // tiles ahead of the converts (which may wait for SMs busy with GEMMs).
     const int k = static_cast<int>(dc.stage_next++ % kStage);
     cudaStream_t xs = dc.streams[X].stream;
-    if (dc.stage_free[k]) TR_CUDA(cudaStreamWaitEvent(xs, dc.stage_free[k], 0));
+    wait_on(d, X, dc.stage_free[k]);
     TimedLaunch tc1{}, tc2{};
     trace_begin(d, X, &tc1);
     TR_CUDA(cudaMemcpy2DAsync(dc.stage[k], tc * es, base, src.ld * es, tc * es, tr_, cudaMemcpyHostToDevice, xs));
     trace_end(d, X, tc1, TR_TRACE_H2D, -1, key.matrix, key.row, key.col);
-    cudaEvent_t copied = record(d, X);
-    TR_CUDA(cudaStreamWaitEvent(fs, copied, 0));
+    wait_on(d, F, record(d, X));  // convert after the copy landed
     trace_begin(d, F, &tc2);
     TR_CUDA(launch_split_convert(dc.stage[k], src.dtype == TR_DTYPE_F64, tc, tr_, tc, slot_ptr(d, phys), ld_, T,
                                  plane_elems_, planes_, fs));
@@ -423,8 +443,7 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     trace_end(d, F, tc2, TR_TRACE_CONVERT, -1, key.matrix, key.row, key.col);
   }
   job.launches.fetch_add(1);
-  st.ready_gs = gs_of(d, F);
-  st.ready_ev = record(d, F);
+  st.ready = record(d, F);
   st.uses.clear();
 }
 
@@ -433,27 +452,56 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
 // are brought in on the device's fetch-ahead stream while earlier tasks compute,
 // overlapping H2D/NVLink traffic with the tensor pipe.  Directory::prefetch_locked
 // never evicts and never counts, so the counters are exactly the reference's.
-void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen) {
+// Prefetch every input tile of task `tid` that is not yet resident on device d.
+// host_only: only tiles resident nowhere (another device holding a tile serves it
+// over NVLink when actually needed).  Stops once `pending` reaches `budget`.
+bool Session::prefetch_task(int d, Job& job, int64_t tid, bool host_only, int64_t& pending, int64_t budget) {
+  const int s = devs_[d].width;  // the fill stream
+  const int64_t i = tid / job.grid_cols, j = tid % job.grid_cols;
+  for (int64_t k = 0; k < job.k_steps; ++k) {
+    for (int which = 0; which < 2; ++which) {
+      if (pending >= budget) return false;
+      const Mat& m = which == 0 ? job.a : job.b;
+      const uint64_t uid = which == 0 ? job.a_uid : job.b_uid;
+      const bool t = which == 0 ? job.ta : job.tb;
+      const int64_t r = which == 0 ? (t ? k : i) : (t ? j : k);
+      const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
+      const TileKey key{uid, r, c};
+      std::lock_guard<std::mutex> g(dir_->mu);
+      int32_t slot = -1, source = TR_SOURCE_HOST;
+      if (!dir_->prefetch_locked(d, key, &slot, &source, host_only)) continue;
+      load_slot(d, s, phys_of(d, slot), source >= 0 ? HIT_L2 : HIT_MISS, source, key, m, r, c, job);
+      ++pending;
+    }
+  }
+  return true;
+}
+
+// Fetch-ahead ("threaded fetch-ahead", absent from the
+// reference's code).  Two windows: (1) every input tile of the tasks this device
+// has RESERVED; (2) a bounded lookahead over the planned order just past the
+// queue head, for tiles resident nowhere -- this keeps the H2D engine busy
+// through the first-touch phase, when each new task needs several new panels.
+// Directory::prefetch_locked never evicts and never counts, so the counters are
+// exactly the reference's.  `pending` counts this device's fetched-ahead tiles
+// not yet claimed by one of its tasks.
+void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vector<uint8_t>& seen_global,
+                          int64_t& pending) {
   DeviceCtx& dc = devs_[d];
-  const int s = dc.width;  // the fill stream
+  constexpr int64_t kBudget = 32;   // unclaimed prefetched tiles per device
+  constexpr int64_t kLookahead = 16;
   for (uint64_t tid : dc.station->peek()) {
     if (seen[tid]) continue;
+    if (!prefetch_task(d, job, static_cast<int64_t>(tid), false, pending, kBudget)) return;
     seen[tid] = 1;
-    const int64_t i = static_cast<int64_t>(tid) / job.grid_cols, j = static_cast<int64_t>(tid) % job.grid_cols;
-    for (int64_t k = 0; k < job.k_steps; ++k) {
-      for (int which = 0; which < 2; ++which) {
-        const Mat& m = which == 0 ? job.a : job.b;
-        const uint64_t uid = which == 0 ? job.a_uid : job.b_uid;
-        const bool t = which == 0 ? job.ta : job.tb;
-        const int64_t r = which == 0 ? (t ? k : i) : (t ? j : k);
-        const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
-        const TileKey key{uid, r, c};
-        std::lock_guard<std::mutex> g(dir_->mu);
-        int32_t slot = -1, source = TR_SOURCE_HOST;
-        if (!dir_->prefetch_locked(d, key, &slot, &source)) continue;
-        load_slot(d, s, phys_of(d, slot), source >= 0 ? HIT_L2 : HIT_MISS, source, key, m, r, c, job);
-      }
-    }
+  }
+  const int64_t head = job.claimed.load();
+  const int64_t end = std::min<int64_t>(static_cast<int64_t>(job.order.size()), head + kLookahead);
+  for (int64_t pos = head; pos < end; ++pos) {
+    const int64_t tid = job.order[static_cast<size_t>(pos)];
+    if (seen_global[tid]) continue;
+    if (!prefetch_task(d, job, tid, true, pending, kBudget)) return;
+    seen_global[tid] = 1;
   }
 }
 
@@ -538,18 +586,8 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     {
       std::lock_guard<std::mutex> g(dir_->mu);
       if (!dryrun_ && coherence_) {
-        cudaEvent_t ev = record(d, s);
-        const int32_t gs = gs_of(d, s);
-        for (int32_t p : used_phys) {
-          SlotState& st = dc.slots[p];
-          bool found = false;
-          for (auto& u : st.uses)
-            if (u.first == gs) {
-              u.second = ev;
-              found = true;
-            }
-          if (!found) st.uses.emplace_back(gs, ev);
-        }
+        const EvRef ev = record(d, s);
+        for (int32_t p : used_phys) note_use(dc.slots[p], ev);
       }
       for (const TileKey& k : used) dir_->release_input_locked(d, k);
     }
@@ -605,6 +643,8 @@ void Session::run_job(int d, Job& job) {
   bool ahead = !dryrun_ && coherence_ && !(flags_ & TR_FLAG_NO_PREFETCH);
   for (auto& dv : devs_) ahead = ahead && dv.capacity < 0;  // bounded caches: keep eviction order exact
   std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.grid_rows * job.grid_cols) : 0, 0);
+  std::vector<uint8_t> seen_global(seen.size(), 0);
+  dc.pending_prefetch = 0;
   while (!job.abort.load()) {
     int active = 0;
     if (!dryrun_) {
@@ -615,8 +655,8 @@ void Session::run_job(int d, Job& job) {
       reap(d, job, true);
       continue;
     }
-    st.refill(job.queue, dc.width - active);
-    if (ahead) fetch_ahead(d, job, seen);
+    job.claimed.fetch_add(static_cast<int64_t>(st.refill(job.queue, dc.width - active).size()));
+    if (ahead) fetch_ahead(d, job, seen, seen_global, dc.pending_prefetch);
     uint64_t tid;
     int victim = -1;
     if (!st.pop_for_run(&tid)) {
@@ -783,6 +823,7 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   for (int64_t t : ids) {
     if (t % task_stride != task_offset) continue;
     job.queue.enqueue(static_cast<uint64_t>(t));
+    job.order.push_back(t);
     ++planned;
   }
   job.n_tasks = planned;
@@ -843,10 +884,7 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   if (!dryrun_) {
     for (auto& dc : devs_) {
       cudaSetDevice(dc.gpu);
-      for (int s = 1; s < static_cast<int>(dc.streams.size()); ++s) {
-        cudaEvent_t ev = record(dc.id, s);
-        cudaStreamWaitEvent(dc.streams[0].stream, ev, 0);
-      }
+      for (int s = 1; s < static_cast<int>(dc.streams.size()); ++s) wait_on(dc.id, 0, record(dc.id, s));
       cudaEventRecord(dc.span_end, dc.streams[0].stream);
       for (auto& sc : dc.streams) {
         cudaError_t e = cudaStreamSynchronize(sc.stream);

@@ -18,6 +18,7 @@
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
+#include <deque>
 #include <exception>
 #include <memory>
 #include <mutex>
@@ -63,6 +64,8 @@ struct Job {
   std::string err_msg;
   std::vector<tr_steal_event> steals;
   std::atomic<int64_t> launches{0};
+  std::vector<int64_t> order;          // planned task ids in enqueue order
+  std::atomic<int64_t> claimed{0};     // tasks pulled from the queue so far (all devices)
 
   explicit Job(int64_t total) : done(static_cast<size_t>(total)) {
     for (auto& d : done) d.store(0);
@@ -90,18 +93,25 @@ class Session {
   const std::vector<tr_trace_event>& trace() const { return last_trace_; }
 
  private:
-  static constexpr int kRing = 64;
   static constexpr int kStage = 4;  // H2D staging ring depth per device
 
+  // A point on a stream.  Events are recycled only after they completed, so a
+  // reference whose generation no longer matches its event names a point that
+  // is known to be complete (waiting on it is a no-op).
+  struct EvRef {
+    int32_t gs = -1;   // global stream id (device * 64 + stream); -1 = none
+    int32_t idx = -1;  // index in that stream's event pool
+    uint64_t gen = 0;  // generation of the recording
+  };
   struct SlotState {
-    int32_t ready_gs = -1;
-    cudaEvent_t ready_ev = nullptr;
-    std::vector<std::pair<int32_t, cudaEvent_t>> uses;  // (global stream, event of last use)
+    EvRef ready;              // fill (convert or peer copy) of the current content
+    std::vector<EvRef> uses;  // last read of the slot by each stream (kernels, peer copies)
   };
   struct StreamCtx {
     cudaStream_t stream = nullptr;
-    cudaEvent_t ring[kRing] = {};
-    uint32_t next = 0;
+    std::vector<cudaEvent_t> evs;   // event pool, recycled in recording order once complete
+    std::vector<uint64_t> gen;
+    std::deque<int32_t> fifo;
     cudaEvent_t done = nullptr;
     int64_t task = -1;      // in-flight task id, -1 idle
     uint64_t seq = 0;       // issue order
@@ -130,12 +140,13 @@ class Session {
     std::vector<StreamCtx> streams;
     void* stage[kStage] = {};
     size_t stage_cap[kStage] = {};
-    cudaEvent_t stage_free[kStage] = {};
+    EvRef stage_free[kStage];
     uint64_t stage_next = 0;    std::unique_ptr<Station> station;
     tr_device_stats stats{};
     std::vector<TimedLaunch> timed, timed_pool;
     std::vector<TraceRec> trace;
     double last_kernel_ms = 0;
+    int64_t pending_prefetch = 0;  // fetched-ahead tiles not yet claimed (this job)
     int64_t last_launches = 0;
     double last_span_ms = 0;
     cudaEvent_t span_start = nullptr, span_end = nullptr;
@@ -151,10 +162,13 @@ class Session {
   void fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c);
   void load_slot(int d, int s, int32_t phys, HitLevel level, int32_t source, const TileKey& key, const Mat& src,
                  int64_t r, int64_t c, Job& job);
-  void fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen);
+  void fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vector<uint8_t>& seen_global,
+                   int64_t& pending);
+  bool prefetch_task(int d, Job& job, int64_t tid, bool host_only, int64_t& pending, int64_t budget);
   void wait_slot_free(int d, int s, int32_t phys);
-  void wait_event_if_foreign(int d, int s, int32_t gs, cudaEvent_t ev);
-  cudaEvent_t record(int d, int s);
+  void wait_on(int d, int s, const EvRef& r);  // stream (d, s) waits for point r (unless same stream / complete)
+  EvRef record(int d, int s);
+  void note_use(SlotState& st, const EvRef& r);
   int32_t gs_of(int d, int s) const { return d * 64 + s; }
   void reap(int d, Job& job, bool block_oldest);
   // tracing (TR_FLAG_TRACE): bracket an async operation with timing events
