@@ -20,8 +20,8 @@ a_host = tr.matrix.pinned_empty((n, n), np.float32); a_host[...] = A.cpu().numpy
 b_host = tr.matrix.pinned_empty((n, n), np.float32); b_host[...] = B.cpu().numpy()
 del A, B, C
 torch.cuda.empty_cache()
-for order in ("row-major", "shells"):
-    for fa, inflight in ((False, 2), (True, 2), (True, 4)):
+for order in ("row-major", "banded", "shells"):
+    for fa, inflight in ((True, 2), (True, 3)):
         rt = tr.Runtime(m, T, fetch_ahead=fa)
         rt.set_order(order); rt.set_inflight(inflight)
         ts = []
