@@ -213,6 +213,30 @@ int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t transpose
 int tr_gemm_shard(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t transpose_a, const tr_matrix* b,
                   uint64_t b_uid, int32_t transpose_b, const tr_matrix* c, uint64_t c_uid, int64_t task_offset,
                   int64_t task_stride, tr_gemm_report* report);
+/* A batch of INDEPENDENT products scheduled as one round (their tasks interleave
+ * on the devices' streams; no product may read another's output).  Each may
+ * carry a fused epilogue post-op for float32 DEVICE outputs (MLP training):
+ *   TR_POST_BIAS_ACT  C = act(A.B + bias[col])        forward layer, ann.py:155-158
+ *   TR_POST_ACT_GRAD  C = (A.B) * act'(aux[row, col])  dX of layer l+1 times the
+ *                     activation derivative of layer l = dY of layer l, ann.py:171,222
+ * act' is taken from the activation OUTPUT (sigmoid: a(1-a), relu: a > 0). */
+typedef enum { TR_POST_NONE = 0, TR_POST_BIAS_ACT = 1, TR_POST_ACT_GRAD = 2 } tr_post_op;
+typedef struct {
+  tr_matrix a;
+  uint64_t a_uid;
+  int32_t transpose_a;
+  tr_matrix b;
+  uint64_t b_uid;
+  int32_t transpose_b;
+  tr_matrix c;
+  uint64_t c_uid;
+  int32_t post;        /* tr_post_op */
+  int32_t act;         /* tr_activation of the post-op */
+  const float* bias;   /* TR_POST_BIAS_ACT: c.cols floats (device), may be NULL */
+  const float* aux;    /* TR_POST_ACT_GRAD: c.rows x c.cols activation output (device) */
+  int64_t ldaux;
+} tr_product;
+int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_report* report);
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
  * measured with CUDA events on the launching streams (sum over launches). */
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms /* n_devices */);
@@ -261,7 +285,7 @@ int tr_dense_gemm(const tr_matrix* a, int32_t transpose_a, const tr_matrix* b, i
 typedef enum { TR_ACT_IDENTITY = 0, TR_ACT_SIGMOID = 1, TR_ACT_RELU = 2 } tr_activation; /* ann.py:27 */
 /* y += bias (per column; bias may be NULL); a = act(y)      ann.py:155-158 */
 int tr_mlp_bias_act(float* y, float* a, const float* bias, int64_t rows, int64_t cols, int32_t act, void* stream);
-/* dy = dout * act'(y, a)                                     ann.py:222, 40-48 */
+/* dy = dout * act'(a) from the activation output a (y unused, may be NULL)  ann.py:222, 40-48 */
 int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a, int64_t n, int32_t act,
                     void* stream);
 /* dout = 2 (pred - target) / n; *loss_sum (device double) = sum (pred - target)^2   ann.py:51-56 */

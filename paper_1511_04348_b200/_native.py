@@ -68,6 +68,15 @@ class StealEventC(C.Structure):
     _fields_ = [("thief", i32), ("victim", i32), ("task_id", i64)]
 
 
+class ProductC(C.Structure):
+    _fields_ = [("a", MatrixC), ("a_uid", u64), ("transpose_a", i32), ("b", MatrixC), ("b_uid", u64),
+                ("transpose_b", i32), ("c", MatrixC), ("c_uid", u64), ("post", i32), ("act", i32),
+                ("bias", C.c_void_p), ("aux", C.c_void_p), ("ldaux", i64)]
+
+
+TR_POST_NONE, TR_POST_BIAS_ACT, TR_POST_ACT_GRAD = 0, 1, 2
+
+
 class TraceEventC(C.Structure):
     _fields_ = [("device", i32), ("kind", i32), ("stream", i32), ("task", i64), ("matrix", u64), ("row", i64),
                 ("col", i64), ("start_ms", f64), ("end_ms", f64)]
@@ -121,6 +130,7 @@ _PROTOS = {
     "tr_gemm": [vp, P(MatrixC), u64, i32, P(MatrixC), u64, i32, P(MatrixC), u64, P(GemmReportC)],
     "tr_gemm_shard": [vp, P(MatrixC), u64, i32, P(MatrixC), u64, i32, P(MatrixC), u64, i64, i64,
                       P(GemmReportC)],
+    "tr_gemm_batch": [vp, i32, P(ProductC), P(GemmReportC)],
     "tr_session_kernel_ms": [vp, P(f64)],
     "tr_session_span_ms": [vp, P(f64)],
     "tr_session_trace": [vp, vp, i64, P(i64)],

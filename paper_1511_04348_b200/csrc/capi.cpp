@@ -308,6 +308,32 @@ int tr_gemm_shard(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t ta,
                report);
   });
 }
+int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_report* report) {
+  return guarded([&] {
+    if (n < 1 || !products) tr::fail(TR_ERR_VALUE, "empty product batch");
+    std::vector<tr::Product> v(static_cast<size_t>(n));
+    for (int32_t k = 0; k < n; ++k) {
+      const tr_product& q = products[k];
+      tr::Product& p = v[static_cast<size_t>(k)];
+      p.a = to_mat(&q.a);
+      p.b = to_mat(&q.b);
+      p.c = to_mat(&q.c);
+      p.ta = q.transpose_a != 0;
+      p.tb = q.transpose_b != 0;
+      p.a_uid = q.a_uid;
+      p.b_uid = q.b_uid;
+      p.c_uid = q.c_uid;
+      if (q.post < TR_POST_NONE || q.post > TR_POST_ACT_GRAD) tr::fail(TR_ERR_VALUE, "unknown post-op %d", q.post);
+      if (q.act < TR_ACT_IDENTITY || q.act > TR_ACT_RELU) tr::fail(TR_ERR_VALUE, "unknown activation %d", q.act);
+      p.post = q.post;
+      p.act = q.act;
+      p.bias = q.bias;
+      p.aux = q.aux;
+      p.ldaux = q.ldaux;
+    }
+    s->s->run_products(std::move(v), 0, 1, report);
+  });
+}
 int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t ta, const tr_matrix* b, uint64_t b_uid,
             int32_t tb, const tr_matrix* c, uint64_t c_uid, tr_gemm_report* report) {
   return tr_gemm_shard(s, a, a_uid, ta, b, b_uid, tb, c, c_uid, 0, 1, report);

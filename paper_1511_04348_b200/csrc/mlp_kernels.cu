@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include "common.h"
+#include "act.cuh"
 #include "mlp_kernels.h"
 
 namespace tr {
@@ -25,18 +26,6 @@ int grid_for(int64_t n) {
   if (b < 1) b = 1;
   if (b > 148 * 32) b = 148 * 32;
   return static_cast<int>(b);
-}
-
-__device__ __forceinline__ float act_fwd(int act, float y) {
-  if (act == ACT_SIGMOID) return 1.0f / (1.0f + __expf(-y));
-  if (act == ACT_RELU) return y > 0.f ? y : 0.f;
-  return y;
-}
-
-__device__ __forceinline__ float act_grad(int act, float y, float a) {
-  if (act == ACT_SIGMOID) return a * (1.0f - a);
-  if (act == ACT_RELU) return y > 0.f ? 1.f : 0.f;
-  return 1.f;
 }
 
 __global__ void bias_act_kernel(float* __restrict__ y, float* __restrict__ a, const float* __restrict__ bias,
@@ -55,7 +44,7 @@ __global__ void act_grad_kernel(float* __restrict__ dy, const float* __restrict_
                                 const float* __restrict__ a, int64_t n, int act) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    dy[i] = dout[i] * act_grad(act, y ? y[i] : 0.f, a ? a[i] : 0.f);
+    dy[i] = dout[i] * act_grad_from_out(act, a[i]);  // needs only the activation output (act.cuh)
 }
 
 // dout = 2 (pred - t) / n; loss partial sums of (pred - t)^2 in double, one atomic per block.

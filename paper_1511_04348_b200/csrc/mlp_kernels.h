@@ -5,9 +5,10 @@
 
 #include <cuda_runtime.h>
 
+#include "act.cuh"
+
 namespace tr {
 
-enum Activation : int32_t { ACT_IDENTITY = 0, ACT_SIGMOID = 1, ACT_RELU = 2 };
 
 cudaError_t mlp_bias_act(float* y, float* a, const float* bias, int64_t rows, int64_t cols, int act, cudaStream_t s);
 cudaError_t mlp_act_grad(float* dy, const float* dout, const float* y, const float* a, int64_t n, int act,

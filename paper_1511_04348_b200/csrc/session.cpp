@@ -455,15 +455,25 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
 // Prefetch every input tile of task `tid` that is not yet resident on device d.
 // host_only: only tiles resident nowhere (another device holding a tile serves it
 // over NVLink when actually needed).  Stops once `pending` reaches `budget`.
-bool Session::prefetch_task(int d, Job& job, int64_t tid, bool host_only, int64_t& pending, int64_t budget) {
+// Fetch-ahead ("threaded fetch-ahead", absent from the
+// reference's code): the input tiles of tasks already RESERVED by this device
+// are brought in on the device's fetch-ahead stream while earlier tasks compute,
+// overlapping H2D/NVLink traffic with the tensor pipe.  Directory::prefetch_locked
+// never evicts and never counts, so the counters are exactly the reference's.
+// Prefetch every input tile of task `tid` that is not yet resident on device d.
+// host_only: only tiles resident nowhere (another device holding a tile serves it
+// over NVLink when actually needed).  Stops once `pending` reaches `budget`.
+bool Session::prefetch_task(int d, Job& job, int64_t gtid, bool host_only, int64_t& pending, int64_t budget) {
   const int s = devs_[d].width;  // the fill stream
-  const int64_t i = tid / job.grid_cols, j = tid % job.grid_cols;
-  for (int64_t k = 0; k < job.k_steps; ++k) {
+  int64_t tid = 0;
+  const Product& p = job.prod_of(gtid, &tid);
+  const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+  for (int64_t k = 0; k < p.k_steps; ++k) {
     for (int which = 0; which < 2; ++which) {
       if (pending >= budget) return false;
-      const Mat& m = which == 0 ? job.a : job.b;
-      const uint64_t uid = which == 0 ? job.a_uid : job.b_uid;
-      const bool t = which == 0 ? job.ta : job.tb;
+      const Mat& m = which == 0 ? p.a : p.b;
+      const uint64_t uid = which == 0 ? p.a_uid : p.b_uid;
+      const bool t = which == 0 ? p.ta : p.tb;
       const int64_t r = which == 0 ? (t ? k : i) : (t ? j : k);
       const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
       const TileKey key{uid, r, c};
@@ -508,14 +518,16 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vect
 // ---------------------------------------------------------------- task issue
 // _execute_task (scheduler.py:371-410), asynchronous: the host sequence of
 // directory operations is identical; the arithmetic is enqueued on stream s.
-void Session::issue(int d, Job& job, int64_t tid, int s) {
+void Session::issue(int d, Job& job, int64_t gtid, int s) {
   DeviceCtx& dc = devs_[d];
+  int64_t tid = 0;
+  const Product& p = job.prod_of(gtid, &tid);
   const int64_t T = tile_;
-  const int64_t i = tid / job.grid_cols, j = tid % job.grid_cols;
-  const int64_t mt = std::min(T, job.M - i * T);
-  const int64_t nt = std::min(T, job.N - j * T);
-  const TileKey c_key{job.c_uid, i, j};
-  const int64_t ks = job.k_steps;
+  const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+  const int64_t mt = std::min(T, p.M - i * T);
+  const int64_t nt = std::min(T, p.N - j * T);
+  const TileKey c_key{p.c_uid, i, j};
+  const int64_t ks = p.k_steps;
   int64_t chunk = ks;
   if (!coherence_) chunk = 1;
   else if (dc.capacity >= 0 && dc.capacity < 2 * ks + 1) chunk = std::max<int64_t>(1, (dc.capacity - 1) / 2);
@@ -525,16 +537,16 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     dir_->admit_output_locked(d, c_key);  // pinned for the whole task (scheduler.py:390)
   }
   StreamCtx* scp = dryrun_ ? nullptr : &dc.streams[s];
-  const int64_t ces = job.c.esize();
+  const int64_t ces = p.c.esize();
   void* cptr = nullptr;
   int64_t ldc = 0;
   if (!dryrun_) {
-    if (job.c.location == TR_LOC_HOST) {
+    if (p.c.location == TR_LOC_HOST) {
       cptr = scp->outbuf;
       ldc = nt;
     } else {
-      cptr = const_cast<char*>(static_cast<const char*>(job.c.ptr)) + (i * T * job.c.ld + j * T) * ces;
-      ldc = job.c.ld;
+      cptr = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * ces;
+      ldc = p.c.ld;
     }
   }
   for (int64_t k0 = 0; k0 < ks; k0 += chunk) {
@@ -547,37 +559,44 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     args.planes = planes_;
     args.c = cptr;
     args.ldc = ldc;
-    args.c_f64 = job.c.dtype == TR_DTYPE_F64;
+    args.c_f64 = p.c.dtype == TR_DTYPE_F64;
     args.epilogue = k0 == 0 ? EPI_STORE : EPI_ACCUMULATE;
     args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+    if (p.post != POST_NONE && k0 + kc == ks) {  // fused post-op on the final chunk only
+      args.post = p.post;
+      args.act = p.act;
+      args.bias = p.bias ? p.bias + j * T : nullptr;
+      args.aux = p.aux ? p.aux + (i * T) * p.ldaux + j * T : nullptr;
+      args.ldaux = p.ldaux;
+    }
     std::vector<TileKey> used;
     std::vector<int32_t> used_phys;
     for (int64_t k = k0; k < k0 + kc; ++k) {
       // input acquire order per k-step: A then B (scheduler.py:394-396)
-      const int64_t ar = job.ta ? k : i, ac = job.ta ? i : k;
-      const int64_t br = job.tb ? j : k, bc = job.tb ? k : j;
-      const int32_t pa = acquire(d, s, job, job.a, job.a_uid, job.ta, ar, ac, 0);
-      const int32_t pb = acquire(d, s, job, job.b, job.b_uid, job.tb, br, bc, 1);
+      const int64_t ar = p.ta ? k : i, ac = p.ta ? i : k;
+      const int64_t br = p.tb ? j : k, bc = p.tb ? k : j;
+      const int32_t pa = acquire(d, s, job, p.a, p.a_uid, p.ta, ar, ac, 0);
+      const int32_t pb = acquire(d, s, job, p.b, p.b_uid, p.tb, br, bc, 1);
       args.a_z[k - k0] = pa * planes_;
       args.b_z[k - k0] = pb * planes_;
-      args.k_len[k - k0] = static_cast<int32_t>(std::min(T, job.K - k * T));
-      used.push_back(TileKey{job.a_uid, ar, ac});
-      used.push_back(TileKey{job.b_uid, br, bc});
+      args.k_len[k - k0] = static_cast<int32_t>(std::min(T, p.K - k * T));
+      used.push_back(TileKey{p.a_uid, ar, ac});
+      used.push_back(TileKey{p.b_uid, br, bc});
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
     if (!dryrun_) {
       BoxKind ba, bb;
-      gemm_boxes(job.ta, job.tb, args.m_valid, &ba, &bb);
+      gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
       TimedLaunch tl = timing_pair(d);
       TR_CUDA(cudaEventRecord(tl.start, scp->stream));
-      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, job.ta, job.tb, scp->stream));
+      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
       TR_CUDA(cudaEventRecord(tl.end, scp->stream));
       dc.timed.push_back(tl);
       if (tracing_) {
         // the launch's own timing pair (dc.timed) provides the times; remember its index
         TraceRec rec;
-        rec.ev = tr_trace_event{d, TR_TRACE_GEMM, s, tid, static_cast<uint64_t>(dc.timed.size() - 1), i, j, 0.0, 0.0};
+        rec.ev = tr_trace_event{d, TR_TRACE_GEMM, s, gtid, static_cast<uint64_t>(dc.timed.size() - 1), i, j, 0.0, 0.0};
         rec.t = TimedLaunch{nullptr, nullptr};
         dc.trace.push_back(rec);
       }
@@ -593,25 +612,25 @@ void Session::issue(int d, Job& job, int64_t tid, int s) {
     }
   }
   const int64_t wb_bytes = mt * nt * element_bytes_;
-  if (!dryrun_ && job.c.location == TR_LOC_HOST) {
-    char* dst = const_cast<char*>(static_cast<const char*>(job.c.ptr)) + (i * T * job.c.ld + j * T) * ces;
+  if (!dryrun_ && p.c.location == TR_LOC_HOST) {
+    char* dst = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * ces;
     TimedLaunch tw{};
     trace_begin(d, s, &tw);
-    TR_CUDA(cudaMemcpy2DAsync(dst, job.c.ld * ces, scp->outbuf, nt * ces, nt * ces, mt, cudaMemcpyDeviceToHost,
+    TR_CUDA(cudaMemcpy2DAsync(dst, p.c.ld * ces, scp->outbuf, nt * ces, nt * ces, mt, cudaMemcpyDeviceToHost,
                               scp->stream));
-    trace_end(d, s, tw, TR_TRACE_D2H, tid, job.c_uid, i, j);
+    trace_end(d, s, tw, TR_TRACE_D2H, gtid, p.c_uid, i, j);
   }
   {
     std::lock_guard<std::mutex> g(dir_->mu);
     dir_->release_output_locked(d, c_key, wb_bytes);  // coherence.py:263-280
   }
   if (dryrun_) {
-    job.mark(tid);
+    job.mark(gtid);
     dc.stats.tasks_completed += 1;
     return;
   }
   TR_CUDA(cudaEventRecord(scp->done, scp->stream));
-  scp->task = tid;
+  scp->task = gtid;
 }
 
 void Session::reap(int d, Job& job, bool block_oldest) {
@@ -642,7 +661,7 @@ void Session::run_job(int d, Job& job) {
   uint64_t seq = 0;
   bool ahead = !dryrun_ && coherence_ && !(flags_ & TR_FLAG_NO_PREFETCH);
   for (auto& dv : devs_) ahead = ahead && dv.capacity < 0;  // bounded caches: keep eviction order exact
-  std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.grid_rows * job.grid_cols) : 0, 0);
+  std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.total) : 0, 0);
   std::vector<uint8_t> seen_global(seen.size(), 0);
   dc.pending_prefetch = 0;
   while (!job.abort.load()) {
@@ -740,44 +759,94 @@ struct HostReg {
 
 void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t b_uid, bool tb, const Mat& c,
                    uint64_t c_uid, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep) {
-  const int64_t M = ta ? a.cols : a.rows, K = ta ? a.rows : a.cols;
-  const int64_t Kb = tb ? b.cols : b.rows, N = tb ? b.rows : b.cols;
-  if (a.rows < 1 || a.cols < 1 || b.rows < 1 || b.cols < 1) fail(TR_ERR_SHAPE, "matrix dimensions must be >= 1");
-  if (K != Kb)
-    fail(TR_ERR_SHAPE, "inner dimensions differ: (%lld, %lld) x (%lld, %lld)", (long long)M, (long long)K,
-         (long long)Kb, (long long)N);
-  if (c.rows != M || c.cols != N) fail(TR_ERR_SHAPE, "output is %lldx%lld, expected %lldx%lld", (long long)c.rows,
-                                       (long long)c.cols, (long long)M, (long long)N);
-  for (const Mat* m : {&a, &b, &c})
-    if (m->ld < m->cols || (!dryrun_ && !m->ptr)) fail(TR_ERR_SHAPE, "bad matrix descriptor (ld < cols or null)");
+  Product p;
+  p.a = a;
+  p.b = b;
+  p.c = c;
+  p.ta = ta;
+  p.tb = tb;
+  p.a_uid = a_uid;
+  p.b_uid = b_uid;
+  p.c_uid = c_uid;
+  std::vector<Product> v{p};
+  run_products(std::move(v), task_offset, task_stride, rep);
+}
+
+// Enqueue order of one product's task ids (see tr_session_set_order).
+static std::vector<int64_t> product_order(const Product& p, int order, int64_t room) {
+  const int64_t total = p.grid_rows * p.grid_cols;
+  std::vector<int64_t> ids;
+  ids.reserve(static_cast<size_t>(total));
+  if (order == 1) {
+    const int64_t G = 2;
+    for (int64_t b = 0; b < p.grid_rows; b += G)
+      for (int64_t j = 0; j < p.grid_cols; ++j)
+        for (int64_t i = b; i < std::min(b + G, p.grid_rows); ++i) ids.push_back(i * p.grid_cols + j);
+  } else if (order == 2) {
+    // shells: task (i, j) in shell max(i, j); each shell adds one A row and one
+    // B column of tiles, so compute starts after 2 k-panels instead of a full row
+    const int64_t g = std::max(p.grid_rows, p.grid_cols);
+    for (int64_t sh = 0; sh < g; ++sh) {
+      for (int64_t i = 0; i < std::min(sh, p.grid_rows); ++i)
+        if (sh < p.grid_cols) ids.push_back(i * p.grid_cols + sh);
+      if (sh < p.grid_rows)
+        for (int64_t j = 0; j <= std::min(sh, p.grid_cols - 1); ++j) ids.push_back(sh * p.grid_cols + j);
+    }
+  } else if (order == 3) {
+    // blocked: b x b task blocks whose (b + b) k-panels fit the tile budget, so
+    // each A/B tile is fetched once per block instead of once per task row
+    const int64_t ks = std::max<int64_t>(1, p.k_steps);
+    const int64_t bsz = std::max<int64_t>(1, (room == INT64_MAX ? total : (room - 8)) / (2 * ks));
+    for (int64_t bi = 0; bi < p.grid_rows; bi += bsz)
+      for (int64_t bj = 0; bj < p.grid_cols; bj += bsz)
+        for (int64_t i = bi; i < std::min(bi + bsz, p.grid_rows); ++i)
+          for (int64_t j = bj; j < std::min(bj + bsz, p.grid_cols); ++j) ids.push_back(i * p.grid_cols + j);
+  } else {
+    for (int64_t t = 0; t < total; ++t) ids.push_back(t);
+  }
+  return ids;
+}
+
+void Session::run_products(std::vector<Product> prods, int64_t task_offset, int64_t task_stride,
+                           tr_gemm_report* rep) {
+  if (prods.empty()) fail(TR_ERR_VALUE, "empty product batch");
   if (task_stride < 1 || task_offset < 0 || task_offset >= task_stride) fail(TR_ERR_VALUE, "bad task shard");
   const int64_t T = tile_;
-  Job job(ceil_div(M, T) * ceil_div(N, T));
-  job.a = a;
-  job.b = b;
-  job.c = c;
-  job.ta = ta;
-  job.tb = tb;
-  job.a_uid = a_uid;
-  job.b_uid = b_uid;
-  job.c_uid = c_uid;
-  job.M = M;
-  job.N = N;
-  job.K = K;
-  job.grid_rows = ceil_div(M, T);
-  job.grid_cols = ceil_div(N, T);
-  job.k_steps = ceil_div(K, T);
-  job.task_offset = task_offset;
-  job.task_stride = task_stride;
+  int64_t total = 0, in_tiles_all = 0;
+  for (Product& p : prods) {
+    const Mat &a = p.a, &b = p.b, &c = p.c;
+    p.M = p.ta ? a.cols : a.rows;
+    p.K = p.ta ? a.rows : a.cols;
+    const int64_t Kb = p.tb ? b.cols : b.rows;
+    p.N = p.tb ? b.rows : b.cols;
+    if (a.rows < 1 || a.cols < 1 || b.rows < 1 || b.cols < 1) fail(TR_ERR_SHAPE, "matrix dimensions must be >= 1");
+    if (p.K != Kb)
+      fail(TR_ERR_SHAPE, "inner dimensions differ: (%lld, %lld) x (%lld, %lld)", (long long)p.M, (long long)p.K,
+           (long long)Kb, (long long)p.N);
+    if (c.rows != p.M || c.cols != p.N)
+      fail(TR_ERR_SHAPE, "output is %lldx%lld, expected %lldx%lld", (long long)c.rows, (long long)c.cols,
+           (long long)p.M, (long long)p.N);
+    for (const Mat* m : {&a, &b, &c})
+      if (m->ld < m->cols || (!dryrun_ && !m->ptr)) fail(TR_ERR_SHAPE, "bad matrix descriptor (ld < cols or null)");
+    if (p.post != POST_NONE && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
+      fail(TR_ERR_VALUE, "fused epilogues need a float32 device output");
+    if (p.post == POST_ACT_GRAD && !p.aux) fail(TR_ERR_VALUE, "POST_ACT_GRAD needs the activation (aux) matrix");
+    p.grid_rows = ceil_div(p.M, T);
+    p.grid_cols = ceil_div(p.N, T);
+    p.k_steps = ceil_div(p.K, T);
+    p.base = total;
+    total += p.grid_rows * p.grid_cols;
+    in_tiles_all += ceil_div(a.rows, T) * ceil_div(a.cols, T) + ceil_div(b.rows, T) * ceil_div(b.cols, T);
+  }
+  Job job(total);
+  job.prods = std::move(prods);
   // plan(): every task enqueued up front (scheduler.py:189-192).  Row-major as in
   // the reference, or -- when no device has a bounded capacity, so the hit/miss
   // counters cannot depend on the order -- in "shells" (all tasks with
   // max(i, j) = s before shell s + 1), which spreads first-touch host traffic
   // over the run instead of loading every B panel during the first task row.
-  const int64_t total = job.grid_rows * job.grid_cols;
+  // Products of a batch are interleaved round-robin.
   int order = order_;
-  const int64_t a_tiles_all = ceil_div(a.rows, T) * ceil_div(a.cols, T);
-  const int64_t b_tiles_all = ceil_div(b.rows, T) * ceil_div(b.cols, T);
   int64_t room = INT64_MAX;  // smallest tile budget of any device
   for (auto& dc : devs_) {
     const int64_t cap = dc.capacity >= 0 ? dc.capacity : (dryrun_ ? INT64_MAX : dc.max_slots);
@@ -786,38 +855,22 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   if (order < 0) {
     bool bounded = false;
     for (auto& dc : devs_) bounded = bounded || dc.capacity >= 0;
-    if (bounded) order = 0;                                    // reference order: exact LRU parity
-    else if (a_tiles_all + b_tiles_all > room) order = 3;      // out-of-core: blocked
-    else order = 2;                                            // in-core: shells
+    if (bounded) order = 0;                          // reference order: exact LRU parity
+    else if (in_tiles_all > room) order = 3;         // out-of-core: blocked
+    else order = 2;                                  // in-core: shells
   }
+  std::vector<std::vector<int64_t>> per;
+  for (const Product& p : job.prods) per.push_back(product_order(p, order, room));
   std::vector<int64_t> ids;
   ids.reserve(static_cast<size_t>(total));
-  if (order == 1) {
-    const int64_t G = 2;
-    for (int64_t b = 0; b < job.grid_rows; b += G)
-      for (int64_t j = 0; j < job.grid_cols; ++j)
-        for (int64_t i = b; i < std::min(b + G, job.grid_rows); ++i) ids.push_back(i * job.grid_cols + j);
-  } else if (order == 2) {
-    // shells: task (i, j) in shell max(i, j); each shell adds one A row and one
-    // B column of tiles, so compute starts after 2 k-panels instead of a full row
-    const int64_t g = std::max(job.grid_rows, job.grid_cols);
-    for (int64_t sh = 0; sh < g; ++sh) {
-      for (int64_t i = 0; i < std::min(sh, job.grid_rows); ++i)
-        if (sh < job.grid_cols) ids.push_back(i * job.grid_cols + sh);
-      if (sh < job.grid_rows)
-        for (int64_t j = 0; j <= std::min(sh, job.grid_cols - 1); ++j) ids.push_back(sh * job.grid_cols + j);
-    }
-  } else if (order == 3) {
-    // blocked: b x b task blocks whose (b + b) k-panels fit the tile budget, so
-    // each A/B tile is fetched once per block instead of once per task row
-    const int64_t ks = std::max<int64_t>(1, job.k_steps);
-    const int64_t bsz = std::max<int64_t>(1, (room == INT64_MAX ? total : (room - 8)) / (2 * ks));
-    for (int64_t bi = 0; bi < job.grid_rows; bi += bsz)
-      for (int64_t bj = 0; bj < job.grid_cols; bj += bsz)
-        for (int64_t i = bi; i < std::min(bi + bsz, job.grid_rows); ++i)
-          for (int64_t j = bj; j < std::min(bj + bsz, job.grid_cols); ++j) ids.push_back(i * job.grid_cols + j);
-  } else {
-    for (int64_t t = 0; t < total; ++t) ids.push_back(t);
+  for (size_t r = 0;; ++r) {
+    bool any = false;
+    for (size_t q = 0; q < per.size(); ++q)
+      if (r < per[q].size()) {
+        ids.push_back(job.prods[q].base + per[q][r]);
+        any = true;
+      }
+    if (!any) break;
   }
   int64_t planned = 0;
   for (int64_t t : ids) {
@@ -843,12 +896,15 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
   } restore{!dryrun_, prev_dev};
   HostReg reg;
   if (!dryrun_) {
-    reg.ensure(a);
-    reg.ensure(b);
-    reg.ensure(c);
-    const int64_t a_tiles = ceil_div(a.rows, T) * ceil_div(a.cols, T);
-    const int64_t b_tiles = ceil_div(b.rows, T) * ceil_div(b.cols, T);
-    for (int d = 0; d < n_devices(); ++d) ensure_slab(d, dir_->used_tiles(d) + a_tiles + b_tiles);
+    for (const Product& p : job.prods) {
+      reg.ensure(p.a);
+      reg.ensure(p.b);
+      reg.ensure(p.c);
+    }
+    int64_t in_tiles = 0;
+    for (const Product& p : job.prods)
+      in_tiles += ceil_div(p.a.rows, T) * ceil_div(p.a.cols, T) + ceil_div(p.b.rows, T) * ceil_div(p.b.cols, T);
+    for (int d = 0; d < n_devices(); ++d) ensure_slab(d, dir_->used_tiles(d) + in_tiles);
   }
   const tr_cache_stats before = dir_->stats();
   const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();
@@ -939,9 +995,9 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
     fail(TR_ERR_RUNTIME, "run incomplete: %lld/%lld tasks", (long long)job.done_count.load(), (long long)job.n_tasks);
 
   if (rep) {
-    rep->grid_rows = job.grid_rows;
-    rep->grid_cols = job.grid_cols;
-    rep->k_steps = job.k_steps;
+    rep->grid_rows = job.prods[0].grid_rows;
+    rep->grid_cols = job.prods[0].grid_cols;
+    rep->k_steps = job.prods[0].k_steps;
     rep->total_tasks = job.n_tasks;
     rep->wall_seconds = wall;
     rep->cache = sub_stats(dir_->stats(), before);
@@ -955,7 +1011,7 @@ void Session::gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t
     if (rep->steals)
       for (int64_t k = 0; k < std::min<int64_t>(rep->steals_cap, rep->n_steals); ++k) rep->steals[k] = job.steals[k];
     if (rep->completion)
-      for (int64_t t = 0; t < std::min<int64_t>(rep->completion_cap, total); ++t)
+      for (int64_t t = 0; t < std::min<int64_t>(rep->completion_cap, job.total); ++t)
         rep->completion[t] = job.done[static_cast<size_t>(t)].load();
   }
 }

@@ -47,16 +47,27 @@ struct Mat {
 
 class Session;
 
-struct Job {
+// One product of a job (a batch of independent products may share a job).
+struct Product {
   Mat a, b, c;
   bool ta = false, tb = false;
   uint64_t a_uid = 0, b_uid = 0, c_uid = 0;
   int64_t M = 0, N = 0, K = 0;
   int64_t grid_rows = 0, grid_cols = 0, k_steps = 0;
-  int64_t task_offset = 0, task_stride = 1;
+  int64_t base = 0;  // first global task id of this product
+  // fused epilogue post-op (tile_gemm.h PostOp), device float32 outputs only
+  int32_t post = 0, act = 0;
+  const float* bias = nullptr;
+  const float* aux = nullptr;
+  int64_t ldaux = 0;
+};
+
+struct Job {
+  std::vector<Product> prods;
+  int64_t total = 0;    // global task ids [0, total)
   int64_t n_tasks = 0;  // planned tasks (shard)
   MSQueue queue;
-  std::vector<std::atomic<uint8_t>> done;  // exactly-once bitmap over ALL task ids
+  std::vector<std::atomic<uint8_t>> done;  // exactly-once bitmap over ALL global task ids
   std::atomic<int64_t> done_count{0};
   std::atomic<bool> abort{false};
   std::mutex mu;  // errors + steal log
@@ -64,11 +75,22 @@ struct Job {
   std::string err_msg;
   std::vector<tr_steal_event> steals;
   std::atomic<int64_t> launches{0};
-  std::vector<int64_t> order;          // planned task ids in enqueue order
+  std::vector<int64_t> order;          // planned global task ids in enqueue order
   std::atomic<int64_t> claimed{0};     // tasks pulled from the queue so far (all devices)
 
-  explicit Job(int64_t total) : done(static_cast<size_t>(total)) {
+  explicit Job(int64_t total_ids) : total(total_ids), done(static_cast<size_t>(total_ids)) {
     for (auto& d : done) d.store(0);
+  }
+  // product owning global task id g; *tid = its task id within the product
+  const Product& prod_of(int64_t g, int64_t* tid) const {
+    size_t lo = 0, hi = prods.size();
+    while (hi - lo > 1) {
+      const size_t mid = (lo + hi) / 2;
+      if (prods[mid].base <= g) lo = mid;
+      else hi = mid;
+    }
+    *tid = g - prods[lo].base;
+    return prods[lo];
   }
   void mark(int64_t tid);  // scheduler.py:78-83
   bool all_done() const { return done_count.load() == n_tasks; }
@@ -85,6 +107,8 @@ class Session {
   // Runs one product (scheduler.py:559-612); fills `rep`.
   void gemm(const Mat& a, uint64_t a_uid, bool ta, const Mat& b, uint64_t b_uid, bool tb, const Mat& c,
             uint64_t c_uid, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep);
+  // A batch of independent products scheduled as one job (their tasks interleave).
+  void run_products(std::vector<Product> prods, int64_t task_offset, int64_t task_stride, tr_gemm_report* rep);
   void kernel_ms(double* out) const;
   void span_ms(double* out) const;
   void set_inflight(int n);

@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cudaTypedefs.h>
 
+#include "act.cuh"
 #include "sm100_ptx.cuh"
 #include "tile_gemm.h"
 
@@ -256,6 +257,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
           if (j < ncols) dst[j] = acc_mode ? dst[j] + static_cast<double>(acc[j]) : static_cast<double>(acc[j]);
       } else {
         float* dst = static_cast<float*>(args.c) + off;
+        const int post = args.post;
+        const float* bias = args.bias ? args.bias + gcol0 : nullptr;
+        const float* aux = args.aux ? args.aux + static_cast<int64_t>(grow) * args.ldaux + gcol0 : nullptr;
+        auto finish = [&](float v, int j) -> float {
+          if (post == POST_BIAS_ACT) return act_fwd(args.act, v + (bias ? bias[j] : 0.f));
+          if (post == POST_ACT_GRAD) return v * act_grad_from_out(args.act, aux[j]);
+          return v;
+        };
         if (ncols == 128 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
           float4* d4 = reinterpret_cast<float4*>(dst);
 #pragma unroll
@@ -268,12 +277,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.z += o.z;
               v.w += o.w;
             }
+            if (post != POST_NONE) {
+              v.x = finish(v.x, 4 * j);
+              v.y = finish(v.y, 4 * j + 1);
+              v.z = finish(v.z, 4 * j + 2);
+              v.w = finish(v.w, 4 * j + 3);
+            }
             d4[j] = v;
           }
         } else {
 #pragma unroll
           for (int j = 0; j < 128; ++j)
-            if (j < ncols) dst[j] = acc_mode ? dst[j] + acc[j] : acc[j];
+            if (j < ncols) dst[j] = finish(acc_mode ? dst[j] + acc[j] : acc[j], j);
         }
       }
     }

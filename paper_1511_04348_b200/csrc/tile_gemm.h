@@ -25,6 +25,14 @@ enum Epilogue : int32_t {
   EPI_ACCUMULATE = 1,   // C += acc
 };
 
+// Fused post-op applied to the final value v (after STORE/ACCUMULATE), float32
+// outputs only (MLP training, ann.py:151-174):
+enum PostOp : int32_t {
+  POST_NONE = 0,
+  POST_BIAS_ACT = 1,  // C = act(v + bias[col])                 forward layer (K3 fused)
+  POST_ACT_GRAD = 2,  // C = v * act'(aux[row, col])            dX of layer l+1 -> dY of layer l (K4 fused)
+};
+
 struct GemmArgs {
   int32_t m_valid;               // output rows actually stored
   int32_t n_valid;               // output cols actually stored
@@ -38,6 +46,11 @@ struct GemmArgs {
   int32_t c_f64;                 // 0: float32 output, 1: float64 output
   int32_t epilogue;              // Epilogue
   int32_t seg_kb;                // k-blocks (of 64) per TMEM partial sum; see below
+  int32_t post;                  // PostOp
+  int32_t act;                   // Activation of the post-op
+  const float* bias;             // POST_BIAS_ACT: bias of this tile's first column
+  const float* aux;              // POST_ACT_GRAD: activation output at this tile's origin
+  int64_t ldaux;
 };
 
 // Accumulation-precision note (measured on B200, tools/probe_accum.py): the

@@ -83,52 +83,58 @@ class GpuMLP:
     def _stream(self):
         return self.torch.cuda.current_stream(self.dev).cuda_stream
 
-    def _mm(self, a, b, out, ta=False, tb=False, a_uid=None, b_uid=None):
+    def _batch(self, prods):
+        """Run independent products as one scheduling round (fused epilogues allowed)."""
         N.call("tr_session_set_external_stream", self.rt._h, self._stream())
-        self.rt.multiply(a, b, transpose_a=ta, transpose_b=tb, a_uid=a_uid, b_uid=b_uid, out=out)
-        self.products += 1
-        return out
+        self.rt.multiply_batch(prods)
+        self.products += len(prods)
 
     # -- one pass ------------------------------------------------------------
     def loss_gradients(self, x, target):
-        """Forward + backward without update; returns (loss, [(dW, db)]) on the device."""
-        torch = self.torch
+        """Forward + backward without update; returns (n, [(dW, db)]) with the loss
+        sum left in ``self._loss`` (device).
+
+        Fusion: the forward products write act(X W + b) directly (the epilogue
+        applies bias and activation; only the activation output is kept, which
+        is all act'() needs); the backward dX product of layer l multiplies by
+        act'(A_{l-1}) in its epilogue, producing dY_{l-1} directly; dW_l and
+        dX_l are independent and share one scheduling round.
+        """
         s = self._stream()
-        xs, ys, acts, uids = [], [], [], []
+        xs, uids = [], []
         cur, cur_uid = x, self.rt.fresh_uid("x")
         for li, L in enumerate(self.layers):
             xs.append(cur)
             uids.append(cur_uid)
-            y = self._buf(f"y{li}", (cur.shape[0], L.w.shape[1]))
-            self._mm(cur, L.w, y, a_uid=cur_uid, b_uid=L.weight_uid)
-            a = self._buf(f"a{li}", y.shape)
-            N.call("tr_mlp_bias_act", _ptr(y), _ptr(a), _ptr(L.b) if L.b is not None else None, y.shape[0],
-                   y.shape[1], _ACT[L.activation], s)
-            ys.append(y)
-            acts.append(a)
+            a = self._buf(f"a{li}", (cur.shape[0], L.w.shape[1]))
+            self._batch([dict(a=cur, b=L.w, out=a, a_uid=cur_uid, b_uid=L.weight_uid,
+                              post=("bias_act", L.b, L.activation))])
             cur, cur_uid = a, self.rt.fresh_uid("x")
         self._step_uids = list(uids)
-        pred = acts[-1]
+        pred = cur
         d_out = self._buf("dout", pred.shape)
         N.call("tr_mlp_mse_grad", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(), _ptr(self._loss), s)
+        last = len(self.layers) - 1
+        d_y = self._buf(f"dy{last}", pred.shape)
+        N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), None, _ptr(pred), d_y.numel(),
+               _ACT[self.layers[last].activation], s)
         grads = [None] * len(self.layers)
-        for li in range(len(self.layers) - 1, -1, -1):
+        for li in range(last, -1, -1):
             L = self.layers[li]
-            d_y = self._buf(f"dy{li}", ys[li].shape)
-            N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), _ptr(ys[li]), _ptr(acts[li]), d_y.numel(),
-                   _ACT[L.activation], s)
             dy_uid = self.rt.fresh_uid("dy")
             self._step_uids.append(dy_uid)
             d_w = self._buf(f"dw{li}", L.w.shape)
-            self._mm(xs[li], d_y, d_w, ta=True, a_uid=uids[li], b_uid=dy_uid)
-            d_x = self._buf(f"dx{li}", xs[li].shape)
-            self._mm(d_y, L.w, d_x, tb=True, a_uid=dy_uid, b_uid=L.weight_uid)
+            d_x = self._buf(f"dy{li - 1}" if li > 0 else "dx0", xs[li].shape)
+            dx = dict(a=d_y, b=L.w, out=d_x, transpose_b=True, a_uid=dy_uid, b_uid=L.weight_uid)
+            if li > 0:  # dX_l * act'(A_{l-1}) = dY_{l-1}  (xs[li] is A_{l-1})
+                dx["post"] = ("act_grad", xs[li], self.layers[li - 1].activation)
+            self._batch([dict(a=xs[li], b=d_y, out=d_w, transpose_a=True, a_uid=uids[li], b_uid=dy_uid), dx])
             d_b = None
             if L.b is not None:
                 d_b = self._buf(f"db{li}", L.b.shape)
                 N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
             grads[li] = (d_w, d_b)
-            d_out = d_x
+            d_y = d_x
         return pred.numel(), grads
 
     def train_step(self, x, target, lr: float) -> float:

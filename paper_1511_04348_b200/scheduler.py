@@ -478,33 +478,84 @@ class Runtime:
         dry = self.mode == "dryrun"
         if out is None:
             out = None if dry else _zeros_like_output(a_op, am, bn, pinned=True, zero=False)
+        ma = self._desc(a_op.tiled.base, dry)
+        mb = self._desc(b_op.tiled.base, dry)
+        mc = self._desc(out, dry, shape=(am, bn), dtype=a_op.tiled.base.dtype)
+        total = -(-am // self.tile_size) * -(-bn // self.tile_size)
+        ids = (self._uids.id(a_op.uid), self._uids.id(b_op.uid), self._uids.id(c_uid))
+
+        def call(rep):
+            N.call("tr_gemm_shard", self._h, C.byref(ma), ids[0], int(a_op.transposed), C.byref(mb), ids[1],
+                   int(b_op.transposed), C.byref(mc), ids[2], int(task_offset), int(task_stride), C.byref(rep))
+
+        stats = self._execute(call, total, lambda t: t % task_stride == task_offset)
+        return out, stats
+
+    def multiply_batch(self, products) -> RunStats:
+        """Independent products scheduled as ONE round (tr_gemm_batch): their tasks
+        interleave on the devices, so a small product overlaps a large one and the
+        per-call overhead is paid once.  Each product is a dict with keys ``a``,
+        ``b``, ``out`` (CUDA tensors), optional ``transpose_a``/``transpose_b``,
+        ``a_uid``/``b_uid``/``c_uid``, and an optional fused epilogue
+        ``post=("bias_act", bias, activation)`` or ``post=("act_grad", a_prev,
+        activation)`` (float32 device outputs).  Returns the combined RunStats."""
+        acts = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
+        arr = (N.ProductC * len(products))()
+        keep = []
+        total = 0
+        for k, pr in enumerate(products):
+            a, b, out = pr["a"], pr["b"], pr["out"]
+            ta, tb = bool(pr.get("transpose_a", False)), bool(pr.get("transpose_b", False))
+            q = arr[k]
+            q.a, q.b, q.c = describe(a), describe(b), describe(out)
+            q.transpose_a, q.transpose_b = int(ta), int(tb)
+            q.a_uid = self._uids.id(pr.get("a_uid") or self.fresh_uid())
+            q.b_uid = self._uids.id(pr.get("b_uid") or self.fresh_uid())
+            q.c_uid = self._uids.id(pr.get("c_uid") or self.fresh_uid("c"))
+            post = pr.get("post")
+            if post is not None:
+                kind, ref, act = post
+                q.act = acts[act]
+                if kind == "bias_act":
+                    q.post = N.TR_POST_BIAS_ACT
+                    q.bias = None if ref is None else ref.data_ptr()
+                elif kind == "act_grad":
+                    q.post = N.TR_POST_ACT_GRAD
+                    q.aux, q.ldaux = ref.data_ptr(), ref.stride(0)
+                else:
+                    raise ValueError(f"unknown post-op {kind!r}")
+                keep.append(ref)
+            m = a.shape[1] if ta else a.shape[0]
+            nn = b.shape[0] if tb else b.shape[1]
+            total += -(-m // self.tile_size) * -(-nn // self.tile_size)
+
+        def call(rep):
+            N.call("tr_gemm_batch", self._h, len(products), arr, C.byref(rep))
+
+        return self._execute(call, total, lambda t: True)
+
+    def _execute(self, call, total: int, planned) -> RunStats:
         n = self.machine.n_devices
         rep = N.GemmReportC()
         per_cache = (N.CacheStatsC * n)()
         per_dev = (N.DeviceStatsC * n)()
-        total = -(-am // self.tile_size) * -(-bn // self.tile_size)
         steals = (N.StealEventC * max(1, total))()
         completion = (N.u8 * max(1, total))()
         rep.cache_per_device, rep.devices = per_cache, per_dev
         rep.steals, rep.steals_cap = steals, total
         rep.completion, rep.completion_cap = completion, total
-        ma = self._desc(a_op.tiled.base, dry)
-        mb = self._desc(b_op.tiled.base, dry)
-        mc = self._desc(out, dry, shape=(am, bn), dtype=a_op.tiled.base.dtype)
         with self._lock:
-            N.call("tr_gemm_shard", self._h, C.byref(ma), self._uids.id(a_op.uid), int(a_op.transposed), C.byref(mb),
-                   self._uids.id(b_op.uid), int(b_op.transposed), C.byref(mc), self._uids.id(c_uid),
-                   int(task_offset), int(task_stride), C.byref(rep))
+            call(rep)
             kms = (N.f64 * n)()
             N.call("tr_session_kernel_ms", self._h, kms)
             span = (N.f64 * n)()
             N.call("tr_session_span_ms", self._h, span)
             trace = self._read_trace() if self.tracing else []
         done = [bool(completion[t]) for t in range(total)]
-        want = [t % task_stride == task_offset for t in range(total)]
+        want = [planned(t) for t in range(total)]
         if done != want:
             raise RuntimeError(f"run incomplete: {sum(done)}/{sum(want)} tasks")
-        stats = RunStats(
+        return RunStats(
             mode=self.mode, tile_size=self.tile_size, grid_rows=int(rep.grid_rows), grid_cols=int(rep.grid_cols),
             k_steps=int(rep.k_steps), total_tasks=int(rep.total_tasks), steal_enabled=self.steal,
             coherence_enabled=self.coherence, seed=self.seed,
@@ -521,7 +572,6 @@ class Runtime:
             span_ms={d: float(span[d]) for d in range(n)},
             trace=trace,
         )
-        return out, stats
 
     def _read_trace(self) -> list[dict]:
         n = N.i64()

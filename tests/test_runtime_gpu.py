@@ -192,3 +192,32 @@ def test_first_touch_identity_with_fetch_ahead_under_stealing():
         assert s.cache.bytes_host == 2 * g * g * t * t * 8
         assert s.cache.input_requests == 2 * g ** 3
         assert s.cache.bytes_peer == s.cache.l2_hits * t * t * 8
+
+
+@pytest.mark.parametrize("act", ["sigmoid", "relu", "identity"])
+def test_batch_with_fused_epilogues(act):
+    """tr_gemm_batch: independent products in one round, with the fused MLP
+    post-ops (bias + activation; times act'(a)) against a float64 torch reference."""
+    g = torch.Generator().manual_seed(5)
+    f = lambda *s: torch.randn(*s, generator=g, dtype=torch.float64)
+    x, w, bias, dy = f(300, 520), f(520, 270), f(270), f(300, 270)
+    a_prev = torch.rand(300, 520, generator=g, dtype=torch.float64)  # an activation output
+    if act == "relu":
+        a_prev = torch.relu(a_prev - 0.5)
+    dev = lambda t: t.float().cuda().contiguous()
+    out1 = torch.empty(300, 270, device="cuda")
+    out2 = torch.empty(300, 520, device="cuda")
+    rt = Runtime(homogeneous_machine(2, dtype=np.float32), 128)
+    s = rt.multiply_batch([
+        dict(a=dev(x), b=dev(w), out=out1, post=("bias_act", dev(bias), act)),
+        dict(a=dev(dy), b=dev(w), out=out2, transpose_b=True, post=("act_grad", dev(a_prev), act)),
+    ])
+    fwd = {"sigmoid": torch.sigmoid, "relu": torch.relu, "identity": lambda v: v}[act]
+    grad = {"sigmoid": lambda a: a * (1 - a), "relu": lambda a: (a > 0).double(),
+            "identity": lambda a: torch.ones_like(a)}[act]
+    ref1 = fwd(x @ w + bias)
+    ref2 = (dy @ w.T) * grad(a_prev.float().double())
+    assert rel(out1.double().cpu().numpy(), ref1.numpy()) <= 1e-5
+    assert rel(out2.double().cpu().numpy(), ref2.numpy()) <= 1e-5
+    assert s.total_tasks == 3 * 3 + 3 * 5
+    rt.close()
