@@ -1,0 +1,219 @@
+"""CLI behaviour (reference tests/test_cli.py): deterministic ``gen``, ``gemm``
+reports and exit codes, ``ann`` loss CSV / backend agreement, ``sweep`` CSV
+shape, speedup baseline and partial results.  CPU tests drive the ``dryrun``
+mode (scheduler + directory, exact counters); GPU tests run the products."""
+
+import csv
+import json
+
+import numpy as np
+import pytest
+
+from paper_1511_04348_b200 import cli
+from paper_1511_04348_b200.devices import homogeneous_machine, save_machine
+from paper_1511_04348_b200.errors import CapacityError
+from paper_1511_04348_b200.matio import load_matrix
+
+
+def run_cli(*argv):
+    return cli.main([str(a) for a in argv])
+
+
+def gen(tmp_path, name, rows, cols, seed=0, dist="int"):
+    path = tmp_path / name
+    assert run_cli("gen", "--rows", rows, "--cols", cols, "--seed", seed, "--dist", dist, "--out", path) == 0
+    return path
+
+
+def test_gen_is_deterministic(tmp_path):
+    p1 = gen(tmp_path, "a1.txt", 6, 5, seed=7)
+    p2 = gen(tmp_path, "a2.txt", 6, 5, seed=7)
+    p3 = gen(tmp_path, "a3.txt", 6, 5, seed=8)
+    assert p1.read_bytes() == p2.read_bytes() != p3.read_bytes()
+
+
+def test_gen_int_range_and_float(tmp_path):
+    m = load_matrix(gen(tmp_path, "a.txt", 20, 20, dist="int"))
+    assert np.array_equal(m, np.round(m)) and m.min() >= -4 and m.max() <= 4
+    f = load_matrix(gen(tmp_path, "f.bin", 20, 20, dist="float"))
+    assert f.min() >= -4 and f.max() < 4 and not np.array_equal(f, np.round(f))
+
+
+def test_gen_matches_numpy_stream(tmp_path):
+    m = load_matrix(gen(tmp_path, "a.bin", 3, 4, seed=11))
+    want = np.random.default_rng(11).integers(-4, 5, size=(3, 4)).astype(np.float64)
+    assert np.array_equal(m, want)
+
+
+def test_gen_single_value_binary(tmp_path):
+    p = tmp_path / "one.bin"
+    assert run_cli("gen", "--rows", 1, "--cols", 1, "--out", p) == 0
+    assert load_matrix(p).shape == (1, 1)
+
+
+def test_gen_rejects_bad_dims(tmp_path):
+    assert run_cli("gen", "--rows", 0, "--cols", 3, "--out", tmp_path / "x.txt") == cli.EXIT_CONFIG
+
+
+def test_gemm_dryrun_reports(tmp_path):
+    pa, pb = gen(tmp_path, "a.txt", 10, 7, seed=1), gen(tmp_path, "b.txt", 7, 9, seed=2)
+    report, csv_path, devcfg = tmp_path / "r.json", tmp_path / "r.csv", tmp_path / "devices.json"
+    save_machine(devcfg, homogeneous_machine(2))
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--tile-size", 3, "--devices", devcfg, "--mode", "dryrun",
+                   "--report", report, "--csv", csv_path) == 0
+    doc = json.loads(report.read_text())
+    assert doc["schema_version"] == 1 and doc["total_tasks"] == 4 * 3
+    assert doc["cache"]["host_fetches"] > 0
+    rows = list(csv.DictReader(csv_path.read_text().splitlines()))
+    assert len(rows) == 3 and rows[-1]["device_id"] == "total"
+
+
+def test_gemm_no_coherence_counts(tmp_path):
+    pa, pb = gen(tmp_path, "a.txt", 8, 8, seed=3), gen(tmp_path, "b.txt", 8, 8, seed=4)
+    r1, r2 = tmp_path / "r1.json", tmp_path / "r2.json"
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--tile-size", 2, "--mode", "dryrun", "--report", r1) == 0
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--tile-size", 2, "--mode", "dryrun", "--report", r2,
+                   "--no-coherence") == 0
+    g = 4
+    assert json.loads(r1.read_text())["cache"]["host_fetches"] == 2 * g * g
+    assert json.loads(r2.read_text())["cache"]["host_fetches"] == 2 * g ** 3
+
+
+def test_gemm_missing_input_is_io_error(tmp_path):
+    assert run_cli("gemm", "--a", tmp_path / "nope.txt", "--b", tmp_path / "nope2.txt") == cli.EXIT_IO
+
+
+def test_gemm_bad_device_config_is_config_error(tmp_path):
+    pa, pb = gen(tmp_path, "a.txt", 4, 4), gen(tmp_path, "b.txt", 4, 4)
+    bad = tmp_path / "devices.json"
+    bad.write_text('{"devices": [{"id": 0, "capacity_tiles": 1}]}')
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--devices", bad, "--mode", "dryrun") == cli.EXIT_CONFIG
+    bad.write_text('{"devices": [{"capacity_tiles": 8}]}')
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--devices", bad, "--mode", "dryrun") == cli.EXIT_CONFIG
+
+
+def test_gemm_shape_mismatch_is_config_error(tmp_path):
+    pa, pb = gen(tmp_path, "a.txt", 4, 5), gen(tmp_path, "b.txt", 4, 4)
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--mode", "dryrun") == cli.EXIT_CONFIG
+
+
+def test_capacity_error_maps_to_exit_three(tmp_path, monkeypatch):
+    pa, pb = gen(tmp_path, "a.txt", 4, 4), gen(tmp_path, "b.txt", 4, 4)
+
+    def boom(*a, **k):
+        raise CapacityError("working set does not fit")
+
+    monkeypatch.setattr(cli, "run", boom)
+    assert run_cli("gemm", "--a", pa, "--b", pb) == cli.EXIT_CAPACITY
+
+
+def test_ann_bad_layers_is_config_error():
+    assert run_cli("ann", "--layers", "5", "--steps", 1) == cli.EXIT_CONFIG
+    assert run_cli("ann", "--layers", "3,1", "--data", "xor", "--steps", 1) == cli.EXIT_CONFIG
+
+
+def test_sweep_dryrun_csv_shape(tmp_path):
+    out = tmp_path / "sweep.csv"
+    assert run_cli("sweep", "--sizes", "8,16", "--device-counts", "2", "--tile-size", 4, "--mode", "dryrun",
+                   "--out", out) == 0
+    rows = list(csv.DictReader(out.read_text().splitlines()))
+    assert len(rows) == 4  # the 1-device baseline is added
+    for r in rows:
+        if r["devices"] == "1":
+            assert float(r["speedup"]) == 1.0
+        assert int(r["host_fetches"]) > 0
+
+
+def test_sweep_no_coherence_counts(tmp_path):
+    out = tmp_path / "sweep.csv"
+    assert run_cli("sweep", "--sizes", "16", "--device-counts", "1,2", "--tile-size", 4, "--mode", "dryrun",
+                   "--no-coherence", "--out", out) == 0
+    for r in csv.DictReader(out.read_text().splitlines()):
+        assert int(r["host_fetches"]) == 2 * 4 ** 3
+
+
+def test_sweep_failure_keeps_partial_rows(tmp_path, monkeypatch):
+    real, calls = cli.run, []
+
+    def flaky(*a, **k):
+        calls.append(1)
+        if len(calls) > 2:
+            raise ValueError("injected failure")
+        return real(*a, **k)
+
+    monkeypatch.setattr(cli, "run", flaky)
+    out = tmp_path / "sweep.csv"
+    assert run_cli("sweep", "--sizes", "8,16", "--device-counts", "1,2", "--tile-size", 4, "--mode", "dryrun",
+                   "--out", out) == cli.EXIT_CONFIG
+    assert len(list(csv.DictReader(out.read_text().splitlines()))) == 2
+
+
+def test_module_entrypoint(tmp_path):
+    import subprocess
+    import sys
+
+    p = tmp_path / "m.txt"
+    r = subprocess.run([sys.executable, "-m", "paper_1511_04348_b200", "gen", "--rows", "2", "--cols", "2", "--out",
+                        str(p)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    assert load_matrix(p).shape == (2, 2)
+
+
+# ------------------------------------------------------------------ on the GPU
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["gpu", "threaded", "sim"])
+def test_gemm_end_to_end_exact(tmp_path, mode):
+    pa, pb = gen(tmp_path, "a.txt", 100, 70, seed=1), gen(tmp_path, "b.bin", 70, 90, seed=2)
+    out, devcfg, report = tmp_path / "c.bin", tmp_path / "devices.json", tmp_path / "r.json"
+    save_machine(devcfg, homogeneous_machine(2, capacity_tiles=64, gpus=[0, 0]))
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--out", out, "--tile-size", 32, "--devices", devcfg, "--mode",
+                   mode, "--report", report, "--steal", "off" if mode == "threaded" else "on") == 0
+    want = load_matrix(pa) @ load_matrix(pb)  # integer inputs: exact in every precision path
+    assert np.array_equal(load_matrix(out), want)
+    doc = json.loads(report.read_text())
+    assert doc["total_tasks"] == 4 * 3 and doc["gpu"]["launches"] > 0
+
+
+@pytest.mark.gpu
+def test_gemm_float_fp32acc_tolerance(tmp_path):
+    pa = gen(tmp_path, "a.bin", 300, 260, seed=5, dist="float")
+    pb = gen(tmp_path, "b.bin", 260, 200, seed=6, dist="float")
+    out = tmp_path / "c.bin"
+    assert run_cli("gemm", "--a", pa, "--b", pb, "--out", out, "--tile-size", 128) == 0
+    want = load_matrix(pa) @ load_matrix(pb)
+    got = load_matrix(out)
+    assert np.linalg.norm(got - want) / np.linalg.norm(want) <= 1e-5
+
+
+@pytest.mark.gpu
+def test_ann_dense_xor(tmp_path):
+    loss_csv, report = tmp_path / "loss.csv", tmp_path / "ann.json"
+    assert run_cli("ann", "--layers", "2,8,1", "--data", "xor", "--steps", 50, "--lr", 0.5, "--seed", 0,
+                   "--backend", "dense", "--loss-csv", loss_csv, "--report", report) == 0
+    losses = [float(r["loss"]) for r in csv.DictReader(loss_csv.read_text().splitlines())]
+    assert len(losses) == 50 and losses[-1] < losses[0]
+    assert json.loads(report.read_text())["final_loss"] == losses[-1]
+
+
+@pytest.mark.gpu
+def test_ann_backends_agree(tmp_path):
+    curves = {}
+    for backend in ("dense", "tiled", "fused"):
+        loss_csv = tmp_path / f"{backend}.csv"
+        assert run_cli("ann", "--layers", "3,5,2", "--data", "random", "--batch", 6, "--steps", 10, "--lr", 0.1,
+                       "--seed", 1, "--backend", backend, "--tile-size", 2 if backend == "tiled" else 16,
+                       "--loss-csv", loss_csv) == 0
+        curves[backend] = np.array([float(r["loss"]) for r in csv.DictReader(loss_csv.read_text().splitlines())])
+    # dense and tiled run the same products in fp32acc on float64 host data;
+    # fused keeps float32 weights in HBM, so it agrees to float32 rounding.
+    np.testing.assert_allclose(curves["tiled"], curves["dense"], rtol=1e-5)
+    np.testing.assert_allclose(curves["fused"], curves["dense"], rtol=1e-4)
+
+
+@pytest.mark.gpu
+def test_sweep_gpu(tmp_path):
+    out = tmp_path / "sweep.csv"
+    assert run_cli("sweep", "--sizes", "256", "--device-counts", "1,2", "--tile-size", 64, "--out", out) == 0
+    rows = list(csv.DictReader(out.read_text().splitlines()))
+    assert len(rows) == 2 and all(float(r["makespan"]) > 0 for r in rows)
