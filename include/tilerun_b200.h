@@ -288,10 +288,11 @@ int tr_mlp_bias_act(float* y, float* a, const float* bias, int64_t rows, int64_t
 /* dy = dout * act'(a) from the activation output a (y unused, may be NULL)  ann.py:222, 40-48 */
 int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a, int64_t n, int32_t act,
                     void* stream);
-/* dout = 2 (pred - target) / n; *loss_sum (device double) = sum (pred - target)^2   ann.py:51-56 */
+/* dout = 2 (pred - target) / n; *loss_sum (device double) = sum (pred - target)^2, summed in a
+ * fixed order (bitwise reproducible)                          ann.py:51-56 */
 int tr_mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
                     void* stream);
-/* out[c] = sum_r m[r, c]                                     ann.py:173 */
+/* out[c] = sum_r m[r, c], fixed summation order (reproducible)   ann.py:173 */
 int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream);
 /* w -= lr * g                                                ann.py:243-247 */
 int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
@@ -302,14 +303,30 @@ int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
  * caches keep stale versions forever. */
 int tr_session_forget(tr_session* s, uint64_t uid, int64_t* dropped);
 
-/* Order every product of the session after the work already queued on `stream`
- * (cudaStream_t, e.g. the caller's framework stream); NULL clears it. */
-int tr_session_set_external_stream(tr_session* s, void* stream);
+/* enabled != 0: order every product of the session after the work already queued
+ * on `stream` (a cudaStream_t, e.g. the caller's framework stream; NULL is the
+ * legacy default stream).  enabled == 0 clears it. */
+int tr_session_set_external_stream(tr_session* s, void* stream, int enabled);
+
+/* Stream-ordered products (1) or blocking products (0, default; the reference's
+ * semantics, scheduler.py:587-590).  When on, a product whose operands are ALL
+ * in device memory, run with an external stream set and tracing off, returns
+ * once every task is enqueued: the external stream waits for the product, and
+ * the next product starts after the external stream's queued work.  The report's
+ * counters and completion bitmap are final on return; per-launch kernel times
+ * and the device span are not measured (0).  Any other product blocks as usual. */
+int tr_session_set_async(tr_session* s, int on);
 
 /* Kernel variant switch (process-wide): 1 = CTA pairs (tcgen05 cta_group::2,
  * 256 x 256 per pair) for tiles taller than 128 rows, 0 = single CTAs
  * (128 x 256, default).  Also settable with TR_GEMM_PAIRS=1 in the environment. */
 int tr_set_gemm_pairs(int32_t on);
+
+/* Split-K policy (process-wide): at most `max_splits` (1..8) K-splits per tile
+ * GEMM launch whose output has fewer 128 x 256 blocks than the GPU has SMs
+ * (partials reduced in a fixed order: deterministic).  1 disables.  Default 8,
+ * or TR_SPLITK=<n> in the environment. */
+int tr_set_splitk(int32_t max_splits);
 
 #ifdef __cplusplus
 }

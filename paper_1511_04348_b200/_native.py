@@ -139,12 +139,14 @@ _PROTOS = {
     "tr_release_cached_memory": [],
     "tr_dense_gemm": [P(MatrixC), i32, P(MatrixC), i32, P(MatrixC), i32, i32, vp],
     "tr_set_gemm_pairs": [i32],
+    "tr_set_splitk": [i32],
     "tr_mlp_bias_act": [vp, vp, vp, i64, i64, i32, vp],
     "tr_mlp_act_grad": [vp, vp, vp, vp, i64, i32, vp],
     "tr_mlp_mse_grad": [vp, vp, vp, i64, vp, vp],
     "tr_mlp_colsum": [vp, i64, i64, vp, vp],
     "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
-    "tr_session_set_external_stream": [vp, vp],
+    "tr_session_set_external_stream": [vp, vp, i32],
+    "tr_session_set_async": [vp, i32],
     "tr_session_forget": [vp, u64, P(i64)],
 }
 

@@ -450,11 +450,22 @@ int tr_session_forget(tr_session* s, uint64_t uid, int64_t* dropped) {
     if (dropped) *dropped = n;
   });
 }
-int tr_session_set_external_stream(tr_session* s, void* stream) {
-  return guarded([&] { s->s->set_external_stream(static_cast<cudaStream_t>(stream)); });
+int tr_session_set_external_stream(tr_session* s, void* stream, int enabled) {
+  return guarded([&] { s->s->set_external_stream(static_cast<cudaStream_t>(stream), enabled != 0); });
+}
+
+int tr_session_set_async(tr_session* s, int on) {
+  return guarded([&] { s->s->set_async(on != 0); });
 }
 int tr_set_gemm_pairs(int32_t on) {
   return guarded([&] { tr::set_gemm_pairs(on != 0); });
+}
+
+int tr_set_splitk(int32_t max_splits) {
+  return guarded([&] {
+    if (max_splits < 1 || max_splits > 8) tr::fail(TR_ERR_VALUE, "split-K factor must be in 1..8");
+    tr::set_splitk_max(max_splits);
+  });
 }
 
 }  // extern "C"

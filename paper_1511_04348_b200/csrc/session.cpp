@@ -108,6 +108,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
     for (int d = 0; d < n; ++d) {
       DeviceCtx& dc = devs_[d];
       TR_CUDA(cudaSetDevice(dc.gpu));
+      TR_CUDA(cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dc.gpu));
       size_t free_b = 0, total_b = 0;
       TR_CUDA(cudaMemGetInfo(&free_b, &total_b));
       const double reusable = static_cast<double>(free_b) + static_cast<double>(DevPool::get().cached_bytes());
@@ -173,6 +174,7 @@ Session::~Session() {
       cudaEventDestroy(sc.done);
       DevPool::get().release(dc.gpu, sc.staging, sc.staging_cap);
       DevPool::get().release(dc.gpu, sc.outbuf, sc.outbuf_cap);
+      if (sc.ws) DevPool::get().release(dc.gpu, sc.ws, sc.ws_cap);
       cudaStreamDestroy(sc.stream);
     }
     for (auto& t : dc.timed) {
@@ -447,22 +449,10 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
   st.uses.clear();
 }
 
-// Fetch-ahead ("threaded fetch-ahead", absent from the
-// reference's code): the input tiles of tasks already RESERVED by this device
-// are brought in on the device's fetch-ahead stream while earlier tasks compute,
-// overlapping H2D/NVLink traffic with the tensor pipe.  Directory::prefetch_locked
-// never evicts and never counts, so the counters are exactly the reference's.
-// Prefetch every input tile of task `tid` that is not yet resident on device d.
-// host_only: only tiles resident nowhere (another device holding a tile serves it
-// over NVLink when actually needed).  Stops once `pending` reaches `budget`.
-// Fetch-ahead ("threaded fetch-ahead", absent from the
-// reference's code): the input tiles of tasks already RESERVED by this device
-// are brought in on the device's fetch-ahead stream while earlier tasks compute,
-// overlapping H2D/NVLink traffic with the tensor pipe.  Directory::prefetch_locked
-// never evicts and never counts, so the counters are exactly the reference's.
-// Prefetch every input tile of task `tid` that is not yet resident on device d.
-// host_only: only tiles resident nowhere (another device holding a tile serves it
-// over NVLink when actually needed).  Stops once `pending` reaches `budget`.
+// Prefetch every input tile of task `tid` that is not yet resident on device d
+// (see fetch_ahead).  host_only: only tiles resident nowhere (another device
+// holding a tile serves it over NVLink when actually needed).  Stops once
+// `pending` reaches `budget`.
 bool Session::prefetch_task(int d, Job& job, int64_t gtid, bool host_only, int64_t& pending, int64_t budget) {
   const int s = devs_[d].width;  // the fill stream
   int64_t tid = 0;
@@ -513,6 +503,48 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vect
     if (!prefetch_task(d, job, tid, true, pending, kBudget)) return;
     seen_global[tid] = 1;
   }
+}
+
+// ---------------------------------------------------------------- split-K
+// A launch whose output tile has fewer 128 x 256 blocks than the GPU has SMs
+// (skinny MLP layers: N = 10, K = 784 edges) is split along K so that about
+// two waves of CTAs run; partials go to the stream's workspace and a reduction
+// kernel sums them in a fixed order (deterministic) and applies the epilogue.
+void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
+  args.k_split = 1;
+  const int smax = splitk_max();
+  if (smax < 2) return;
+  int total_kb = 0;
+  for (int k = 0; k < args.n_ksteps; ++k) total_kb += (args.k_len[k] + 63) / 64;
+  const int64_t ctas = ((args.m_valid + 127) / 128) * static_cast<int64_t>((args.n_valid + 255) / 256);
+  const int64_t sms = devs_[d].sms;
+  if (ctas >= sms) return;
+  const int s = static_cast<int>(std::min<int64_t>({2 * sms / ctas, smax, total_kb / 8}));
+  if (s < 2) return;
+  const int64_t ws_ld = (args.n_valid + 255) / 256 * 256;
+  const int64_t zstride = static_cast<int64_t>(args.m_valid) * ws_ld;
+  const size_t need = static_cast<size_t>(s * zstride) * sizeof(float);
+  if (need > sc.ws_cap) {
+    DeviceCtx& dc = devs_[d];
+    if (sc.ws) {
+      TR_CUDA(cudaStreamSynchronize(sc.stream));  // the old workspace may still be read
+      DevPool::get().release(dc.gpu, sc.ws, sc.ws_cap);
+      sc.ws = nullptr;
+      sc.ws_cap = 0;
+    }
+    void* p = nullptr;
+    size_t cap = 0;
+    if (DevPool::get().alloc(dc.gpu, need, &p, &cap) != cudaSuccess) {
+      cudaGetLastError();
+      return;  // no room: run unsplit
+    }
+    sc.ws = static_cast<float*>(p);
+    sc.ws_cap = cap;
+  }
+  args.k_split = s;
+  args.ws = sc.ws;
+  args.ws_ld = ws_ld;
+  args.ws_zstride = zstride;
 }
 
 // ---------------------------------------------------------------- task issue
@@ -585,12 +617,23 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
-    if (!dryrun_) {
+    if (!dryrun_) plan_split_k(d, *scp, args);
+    if (!dryrun_ && job.async) {
+      BoxKind ba, bb;
+      gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
+      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+      if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
+      job.launches.fetch_add(args.k_split > 1 ? 2 : 1);
+    } else if (!dryrun_) {
       BoxKind ba, bb;
       gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
       TimedLaunch tl = timing_pair(d);
       TR_CUDA(cudaEventRecord(tl.start, scp->stream));
       TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+      if (args.k_split > 1) {
+        TR_CUDA(launch_splitk_reduce(args, scp->stream));
+        job.launches.fetch_add(1);
+      }
       TR_CUDA(cudaEventRecord(tl.end, scp->stream));
       dc.timed.push_back(tl);
       if (tracing_) {
@@ -624,7 +667,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     std::lock_guard<std::mutex> g(dir_->mu);
     dir_->release_output_locked(d, c_key, wb_bytes);  // coherence.py:263-280
   }
-  if (dryrun_) {
+  if (dryrun_ || job.async) {  // async: the task completes in stream order
     job.mark(gtid);
     dc.stats.tasks_completed += 1;
     return;
@@ -699,7 +742,9 @@ void Session::run_job(int d, Job& job) {
       devs_[victim].stats.steals_suffered += 1;
     }
     int s = 0;
-    if (!dryrun_) {
+    if (job.async) {
+      s = static_cast<int>(seq++ % static_cast<uint64_t>(dc.max_inflight));  // round-robin, nothing to reap
+    } else if (!dryrun_) {
       while (dc.streams[s].task >= 0) ++s;
       dc.streams[s].seq = ++seq;
     }
@@ -840,6 +885,14 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
   }
   Job job(total);
   job.prods = std::move(prods);
+  // Stream-ordered mode (tr_session_set_async): with a caller stream and every
+  // operand in device memory, the call returns once all tasks are enqueued; the
+  // caller's stream waits for the product, the next product's streams wait for
+  // the caller's stream, so successive products (and the caller's own kernels)
+  // stay ordered without a host round trip between them.
+  job.async = async_ && ext_on_ && !dryrun_ && !tracing_;
+  for (const Product& p : job.prods)
+    for (const Mat* m : {&p.a, &p.b, &p.c}) job.async = job.async && m->location == TR_LOC_DEVICE;
   // plan(): every task enqueued up front (scheduler.py:189-192).  Row-major as in
   // the reference, or -- when no device has a bounded capacity, so the hit/miss
   // counters cannot depend on the order -- in "shells" (all tasks with
@@ -909,7 +962,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
   const tr_cache_stats before = dir_->stats();
   const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();
   if (!dryrun_) {
-    if (ext_stream_) {
+    if (ext_on_) {
       // inputs produced on the caller's stream (e.g. torch) must be complete first
       if (!ext_ready_) TR_CUDA(cudaEventCreateWithFlags(&ext_ready_, cudaEventDisableTiming));
       TR_CUDA(cudaEventRecord(ext_ready_, ext_stream_));
@@ -918,7 +971,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     // span_end is recorded after every stream's last operation
     for (auto& dc : devs_) {
       TR_CUDA(cudaSetDevice(dc.gpu));
-      if (ext_stream_) TR_CUDA(cudaStreamWaitEvent(dc.streams[0].stream, ext_ready_, 0));
+      if (ext_on_) TR_CUDA(cudaStreamWaitEvent(dc.streams[0].stream, ext_ready_, 0));
       TR_CUDA(cudaEventRecord(dc.span_start, dc.streams[0].stream));
       for (size_t s = 1; s < dc.streams.size(); ++s)
         TR_CUDA(cudaStreamWaitEvent(dc.streams[s].stream, dc.span_start, 0));
@@ -937,7 +990,14 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     cv_done_.wait(lk, [&] { return workers_done_ == n_devices(); });
     job_ = nullptr;
   }
-  if (!dryrun_) {
+  if (job.async) {
+    for (auto& dc : devs_) {
+      TR_CUDA(cudaSetDevice(dc.gpu));
+      for (int s = 1; s < static_cast<int>(dc.streams.size()); ++s) wait_on(dc.id, 0, record(dc.id, s));
+      TR_CUDA(cudaEventRecord(dc.span_end, dc.streams[0].stream));
+      TR_CUDA(cudaStreamWaitEvent(ext_stream_, dc.span_end, 0));
+    }
+  } else if (!dryrun_) {
     for (auto& dc : devs_) {
       cudaSetDevice(dc.gpu);
       for (int s = 1; s < static_cast<int>(dc.streams.size()); ++s) wait_on(dc.id, 0, record(dc.id, s));
@@ -987,7 +1047,8 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     dc.timed.clear();
     dc.last_kernel_ms = ms;
     float span = 0;
-    if (!dryrun_ && cudaEventElapsedTime(&span, dc.span_start, dc.span_end) != cudaSuccess) cudaGetLastError();
+    if (!dryrun_ && !job.async && cudaEventElapsedTime(&span, dc.span_start, dc.span_end) != cudaSuccess)
+      cudaGetLastError();
     dc.last_span_ms = span;
   }
   if (job.err_status) throw Error(job.err_status, job.err_msg);

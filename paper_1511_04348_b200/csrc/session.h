@@ -77,6 +77,7 @@ struct Job {
   std::atomic<int64_t> launches{0};
   std::vector<int64_t> order;          // planned global task ids in enqueue order
   std::atomic<int64_t> claimed{0};     // tasks pulled from the queue so far (all devices)
+  bool async = false;                  // stream-ordered: tasks complete in stream order, no host wait
 
   explicit Job(int64_t total_ids) : total(total_ids), done(static_cast<size_t>(total_ids)) {
     for (auto& d : done) d.store(0);
@@ -113,7 +114,11 @@ class Session {
   void span_ms(double* out) const;
   void set_inflight(int n);
   void set_order(int order) { order_ = order; }
-  void set_external_stream(cudaStream_t s) { ext_stream_ = s; }
+  void set_external_stream(cudaStream_t s, bool on) {
+    ext_stream_ = on ? s : nullptr;
+    ext_on_ = on;
+  }
+  void set_async(bool on) { async_ = on; }
   const std::vector<tr_trace_event>& trace() const { return last_trace_; }
 
  private:
@@ -142,6 +147,8 @@ class Session {
     void* staging = nullptr;  // host-tile landing zone (T*T*8 bytes)
     void* outbuf = nullptr;   // C tile for host outputs (T*T*8 bytes)
     size_t staging_cap = 0, outbuf_cap = 0;
+    float* ws = nullptr;      // split-K partial sums (grown on demand)
+    size_t ws_cap = 0;
   };
   struct TimedLaunch {
     cudaEvent_t start, end;
@@ -152,6 +159,7 @@ class Session {
   };
   struct DeviceCtx {
     int id = 0, gpu = 0, width = 4, max_inflight = 2;
+    int sms = 148;  // multiprocessors of the GPU (split-K sizing)
     int64_t capacity = -1;
     uint16_t* slab = nullptr;
     size_t slab_cap = 0;
@@ -181,6 +189,7 @@ class Session {
   void worker_main(int d);
   void run_job(int d, Job& job);
   void issue(int d, Job& job, int64_t tid, int s);
+  void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
   int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
                   int scratch);
   void fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c);
@@ -219,6 +228,8 @@ class Session {
   int64_t hbm_budget_;
   int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, 2 shells, -1 auto
   cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
+  bool ext_on_ = false;                // ext_stream_ set (nullptr = the legacy default stream)
+  bool async_ = false;                 // device-resident products return once enqueued (see run_products)
   cudaEvent_t ext_ready_ = nullptr;
   bool tracing_ = false;
   std::vector<tr_trace_event> last_trace_;

@@ -77,11 +77,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int n0 = blockIdx.y * BN;                                   // output tile columns
   const int nb0 = n0 + static_cast<int>(rank) * BN_LOCAL;           // B columns this CTA stages
 
-  // total k-blocks and TMEM segments (identical on every role)
+  // k-blocks of this CTA (all of them, or its split-K share) and TMEM segments
   int total_kb = 0;
   for (int ks = 0; ks < args.n_ksteps; ++ks) total_kb += (args.k_len[ks] + BK - 1) / BK;
-  const int seg_kb = args.seg_kb > 0 ? args.seg_kb : total_kb;
-  const int n_seg = (total_kb + seg_kb - 1) / seg_kb;
+  const int n_split = static_cast<int>(gridDim.z);
+  const int kb_lo = static_cast<int>((static_cast<int64_t>(blockIdx.z) * total_kb) / n_split);
+  const int kb_hi = static_cast<int>((static_cast<int64_t>(blockIdx.z + 1) * total_kb) / n_split);
+  const int my_kb = kb_hi - kb_lo;
+  const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(my_kb, 1);
+  const int n_seg = (my_kb + seg_kb - 1) / seg_kb;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -115,11 +119,13 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       int stage = 0;
       uint32_t phase = 0;
+      int g = 0;  // global k-block index
       for (int ks = 0; ks < args.n_ksteps; ++ks) {
         const int nkb = (args.k_len[ks] + BK - 1) / BK;
         const int az = args.a_z[ks];
         const int bz = args.b_z[ks];
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          if (g < kb_lo || g >= kb_hi) continue;
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE_BYTES;
           uint8_t* sb = sa + PLANES * A_BYTES;
@@ -163,9 +169,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int kb_in_seg = 0, seg = 0;
       uint32_t tmem_d = tmem_base;
       uint32_t accumulate = 0;
+      int g = 0;  // global k-block index
       for (int ks = 0; ks < args.n_ksteps; ++ks) {
         const int nkb = (args.k_len[ks] + BK - 1) / BK;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          if (g < kb_lo || g >= kb_hi) continue;
           if (kb_in_seg == 0) {
             // new partial sum: wait until the epilogue(s) drained this TMEM buffer
             const int buf = seg & 1;
@@ -248,16 +256,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int gcol0 = n0 + half * 128;
     if (grow < args.m_valid && gcol0 < args.n_valid) {
       const int ncols = min(128, args.n_valid - gcol0);
+      const bool partial = n_split > 1;  // split-K: raw fp32 partial into the workspace
       const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
-      const bool acc_mode = args.epilogue == EPI_ACCUMULATE;
-      if (args.c_f64) {
+      const bool acc_mode = !partial && args.epilogue == EPI_ACCUMULATE;
+      if (args.c_f64 && !partial) {
         double* dst = static_cast<double*>(args.c) + off;
 #pragma unroll
         for (int j = 0; j < 128; ++j)
           if (j < ncols) dst[j] = acc_mode ? dst[j] + static_cast<double>(acc[j]) : static_cast<double>(acc[j]);
       } else {
-        float* dst = static_cast<float*>(args.c) + off;
-        const int post = args.post;
+        float* dst = partial ? args.ws + blockIdx.z * args.ws_zstride + static_cast<int64_t>(grow) * args.ws_ld + gcol0
+                             : static_cast<float*>(args.c) + off;
+        const int post = partial ? static_cast<int>(POST_NONE) : args.post;
         const float* bias = args.bias ? args.bias + gcol0 : nullptr;
         const float* aux = args.aux ? args.aux + static_cast<int64_t>(grow) * args.ldaux + gcol0 : nullptr;
         auto finish = [&](float v, int j) -> float {
@@ -314,7 +324,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
   if (attr_err != cudaSuccess) return attr_err;
   const int m_blocks = (args.m_valid + BM * CG - 1) / (BM * CG);
-  dim3 grid(m_blocks * CG, (args.n_valid + BN - 1) / BN);
+  dim3 grid(m_blocks * CG, (args.n_valid + BN - 1) / BN, args.k_split > 1 ? args.k_split : 1);
   if (CG == 1) {
     kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, args);
     return cudaGetLastError();
@@ -337,9 +347,9 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const
 // ---------------------------------------------------------------- K2 split/convert
 template <typename T>
 __global__ void split_convert_kernel(const T* __restrict__ src, int64_t ld_src, int64_t rows, int64_t cols,
-                                     uint16_t* __restrict__ dst, int64_t ld_dst, int64_t rows_cap,
+                                     uint16_t* __restrict__ dst, int64_t ld_dst, int64_t rows_cap, int64_t cols_cap,
                                      int64_t plane_stride, int planes) {
-  const int64_t chunks_per_row = ld_dst / 8;
+  const int64_t chunks_per_row = cols_cap / 8;
   const int64_t total = rows_cap * chunks_per_row;
   for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -358,6 +368,31 @@ __global__ void split_convert_kernel(const T* __restrict__ src, int64_t ld_src, 
     uint16_t* d = dst + r * ld_dst + c;
     *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(hi);
     if (planes == 2) *reinterpret_cast<uint4*>(d + plane_stride) = *reinterpret_cast<const uint4*>(lo);
+  }
+}
+
+// Split-K reduction: C (+)= sum_z ws[z] in z order, then the fused post-op.
+__global__ void splitk_reduce_kernel(const __grid_constant__ GemmArgs args) {
+  const int64_t n = args.n_valid;
+  const int64_t total = static_cast<int64_t>(args.m_valid) * n;
+  const bool acc_mode = args.epilogue == EPI_ACCUMULATE;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx / n, c = idx - r * n;
+    const float* w = args.ws + r * args.ws_ld + c;
+    float v = w[0];
+    for (int z = 1; z < args.k_split; ++z) v += w[z * args.ws_zstride];
+    const int64_t off = r * args.ldc + c;
+    if (args.c_f64) {
+      double* dst = static_cast<double*>(args.c) + off;
+      *dst = acc_mode ? *dst + static_cast<double>(v) : static_cast<double>(v);
+      continue;
+    }
+    float* dst = static_cast<float*>(args.c) + off;
+    if (acc_mode) v += *dst;
+    if (args.post == POST_BIAS_ACT) v = act_fwd(args.act, v + (args.bias ? args.bias[c] : 0.f));
+    else if (args.post == POST_ACT_GRAD) v = v * act_grad_from_out(args.act, args.aux[r * args.ldaux + c]);
+    *dst = v;
   }
 }
 
@@ -426,6 +461,29 @@ cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   }
 }
 
+cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {
+  if (args.k_split < 2 || !args.ws) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(args.m_valid) * args.n_valid;
+  const int threads = 256;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + threads - 1) / threads, 148 * 8));
+  splitk_reduce_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  return cudaGetLastError();
+}
+
+static std::atomic<int> g_splitk{-1};
+
+int splitk_max() {
+  int v = g_splitk.load();
+  if (v < 0) {
+    const char* e = getenv("TR_SPLITK");
+    v = e ? std::max(1, std::min(8, atoi(e))) : 8;
+    g_splitk.store(v);
+  }
+  return v;
+}
+
+void set_splitk_max(int n) { g_splitk.store(std::max(1, std::min(8, n))); }
+
 static std::atomic<int> g_pairs{-1};
 
 bool gemm_pairs_enabled() {
@@ -448,16 +506,22 @@ cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, i
                                  uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,
                                  int planes, cudaStream_t stream) {
   if (ld_dst % 8 != 0 || plane_stride % 8 != 0) return cudaErrorInvalidValue;
-  const int64_t total = rows_cap * (ld_dst / 8);
+  // The kernel's TMA boxes never read past the valid extent rounded up to 256
+  // (rows or columns), so only that part of the slot is written (zero padded);
+  // a ragged 4096 x 10 tile converts 4096 x 256 elements, not 4096 x 4096.
+  const int64_t rows_fill = std::min(rows_cap, (rows + 255) / 256 * 256);
+  const int64_t cols_fill = std::min(ld_dst, (cols + 255) / 256 * 256);
+  rows_cap = rows_fill;
+  const int64_t total = rows_cap * (cols_fill / 8);
   const int threads = 256;
   int64_t blocks = (total + threads - 1) / threads;
   blocks = std::max<int64_t>(1, std::min<int64_t>(blocks, 148 * 16));
   if (src_f64)
     split_convert_kernel<double><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        static_cast<const double*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, plane_stride, planes);
+        static_cast<const double*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, cols_fill, plane_stride, planes);
   else
     split_convert_kernel<float><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
-        static_cast<const float*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, plane_stride, planes);
+        static_cast<const float*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, cols_fill, plane_stride, planes);
   return cudaGetLastError();
 }
 

@@ -51,6 +51,14 @@ struct GemmArgs {
   const float* bias;             // POST_BIAS_ACT: bias of this tile's first column
   const float* aux;              // POST_ACT_GRAD: activation output at this tile's origin
   int64_t ldaux;
+  // Split-K (k_split > 1): CTA z of the grid's z dimension accumulates only the
+  // k-blocks [z*kb/k_split, (z+1)*kb/k_split) and stores its raw fp32 partial
+  // at ws + z*ws_zstride (row-major, ws_ld); launch_splitk_reduce then sums
+  // the partials in z order (deterministic) and applies epilogue + post-op.
+  int32_t k_split;
+  float* ws;
+  int64_t ws_ld;
+  int64_t ws_zstride;
 };
 
 // Accumulation-precision note (measured on B200, tools/probe_accum.py): the
@@ -82,6 +90,14 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box);
 cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
                              bool b_kmajor, cudaStream_t stream);
 void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b);
+// Sums the k_split partials of a split-K launch in z order into C, then applies
+// args.epilogue (STORE / ACCUMULATE) and args.post, exactly like the kernel's own
+// epilogue would have (same argument block).
+cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream);
+// Split-K policy switch (process-wide): max splits per launch, 1 disables.
+// Default 8; TR_SPLITK=<n> in the environment overrides.
+int splitk_max();
+void set_splitk_max(int n);
 // CTA-pair (cta_group::2, 256 x 256) variant for tiles taller than 128 rows.
 // Off by default; TR_GEMM_PAIRS=1 or set_gemm_pairs(true) selects it.
 bool gemm_pairs_enabled();

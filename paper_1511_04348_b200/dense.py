@@ -23,8 +23,13 @@ def precision_code(p) -> int:
 
 
 def set_gemm_pairs(on: bool) -> None:
-    """Select the CTA-pair (cta_group::2) kernel variant (default) or single CTAs."""
+    """Select the CTA-pair (cta_group::2) kernel variant (opt-in) or single CTAs (default)."""
     N.call("tr_set_gemm_pairs", int(bool(on)))
+
+
+def set_splitk(max_splits: int) -> None:
+    """At most ``max_splits`` (1..8) K-splits for tile GEMMs too small to fill the GPU; 1 disables."""
+    N.call("tr_set_splitk", int(max_splits))
 
 
 def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,

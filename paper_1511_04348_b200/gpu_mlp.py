@@ -54,7 +54,7 @@ class GpuMLP:
     """A float32 MLP living in HBM, trained through a tiled ``Runtime`` session."""
 
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
-                 device: int = 0, runtime: Runtime | None = None):
+                 device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True):
         import torch
 
         self.torch = torch
@@ -68,6 +68,7 @@ class GpuMLP:
             machine = machine or homogeneous_machine(1, dtype=np.float32, gpus=[device])
             runtime = Runtime(machine, tile_size, precision=precision)
         self.rt = runtime
+        self.stream_ordered = stream_ordered
         self._loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self._bufs: dict = {}
         self.products = 0
@@ -84,9 +85,17 @@ class GpuMLP:
         return self.torch.cuda.current_stream(self.dev).cuda_stream
 
     def _batch(self, prods):
-        """Run independent products as one scheduling round (fused epilogues allowed)."""
-        N.call("tr_session_set_external_stream", self.rt._h, self._stream())
-        self.rt.multiply_batch(prods)
+        """Run independent products as one scheduling round (fused epilogues allowed).
+
+        Stream-ordered (tr_session_set_async): every operand lives in HBM, so the
+        call returns once the tasks are enqueued and the torch stream waits for
+        them; the host prepares the next round while this one runs.
+        """
+        self.rt.set_stream(self._stream(), ordered=self.stream_ordered)
+        try:
+            self.rt.multiply_batch(prods)
+        finally:
+            self.rt.set_stream(self._stream(), ordered=False)
         self.products += len(prods)
 
     # -- one pass ------------------------------------------------------------

@@ -436,6 +436,16 @@ class Runtime:
         code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2, "blocked": 3}[order]
         N.call("tr_session_set_order", self._h, code)
 
+    def set_stream(self, stream=None, ordered: bool = False) -> None:
+        """Order products after the work queued on ``stream`` (a ``torch.cuda.Stream``
+        or raw cudaStream_t handle; None clears).  ``ordered=True`` makes products
+        whose operands are all CUDA tensors stream-ordered: the call returns once
+        the tasks are enqueued and ``stream`` waits for them (tr_session_set_async);
+        per-launch kernel times and the device span are then not measured."""
+        h = None if stream is None else int(getattr(stream, "cuda_stream", stream))  # 0: legacy default stream
+        N.call("tr_session_set_external_stream", self._h, h or None, int(h is not None))
+        N.call("tr_session_set_async", self._h, int(bool(ordered) and h is not None))
+
     def forget(self, uid) -> int:
         """Drop every cached tile of matrix ``uid`` (its content is dead); returns the count."""
         n = N.i64()

@@ -61,3 +61,25 @@ def test_wide_net_against_blas_oracle():
     for (w, b), L in zip(mlp.to_host(), oracle_layers):
         assert relerr(w, L.weights) <= 1e-5 and relerr(b, L.bias) <= 1e-5
     mlp.close()
+
+
+def test_stream_ordered_matches_blocking():
+    """GpuMLP's stream-ordered products (no host wait between scheduling rounds)
+    produce bit-identical trajectories and weights to blocking products."""
+    rng = np.random.default_rng(5)
+    sizes = [300, 700, 500, 7]
+    base = [Layer.random(sizes[i], sizes[i + 1], rng, scale=1 / np.sqrt(sizes[i]), tag=f"layer{i}")
+            for i in range(3)]
+    x, t = O.random_regression(rng, 333, 300, 7)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    runs = {}
+    for ordered in (False, True):
+        layers = [Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base]
+        mlp = GpuMLP(layers, machine=homogeneous_machine(2, gpus=[0, 0]), tile_size=128, stream_ordered=ordered)
+        losses = [mlp.train_step(xd, td, 0.2) for _ in range(4)]
+        runs[ordered] = (losses, mlp.to_host())
+        mlp.close()
+    assert runs[True][0] == runs[False][0]
+    for (w1, b1), (w0, b0) in zip(runs[True][1], runs[False][1]):
+        assert np.array_equal(w1, w0) and np.array_equal(b1, b0)

@@ -221,3 +221,94 @@ def test_batch_with_fused_epilogues(act):
     assert rel(out2.double().cpu().numpy(), ref2.numpy()) <= 1e-5
     assert s.total_tasks == 3 * 3 + 3 * 5
     rt.close()
+
+
+@pytest.mark.parametrize("side", [True, False])
+def test_stream_ordered_chain_with_torch_ops(side):
+    """Runtime.set_stream(ordered=True): products return once enqueued; a chain
+    product -> torch op -> product on the same stream (a side stream, or the
+    legacy default stream) sees every prior result, and matches the blocking run
+    bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn(700, 500, device="cuda", generator=g)
+    b = torch.randn(500, 500, device="cuda", generator=g)
+    outs = {}
+    for ordered in (False, True):
+        rt = Runtime(homogeneous_machine(2, dtype=np.float32, gpus=[0, 0]), 128)
+        stream = torch.cuda.Stream() if side else torch.cuda.default_stream()
+        stream.wait_stream(torch.cuda.current_stream())  # a, b were made on the default stream
+        rt.set_stream(stream, ordered=ordered)
+        with torch.cuda.stream(stream):
+            c = a.clone()
+            for step in range(5):
+                nxt = torch.empty_like(c)
+                s = rt.multiply(c, b, out=nxt, a_uid=f"c{step}", b_uid="B")[1]
+                assert s.total_tasks == 6 * 4 and s.cache.writebacks == 24
+                c = torch.tanh(nxt * 0.05)  # torch kernel on the same stream, reads the product
+        stream.synchronize()
+        outs[ordered] = c.cpu()
+        ref = a.double()
+        for _ in range(5):
+            ref = torch.tanh((ref @ b.double()) * 0.05)
+        assert rel(c.double().cpu().numpy(), ref.cpu().numpy()) <= 5 * 1e-5  # five chained products
+        rt.close()
+    assert torch.equal(outs[True], outs[False])
+
+
+@pytest.fixture
+def no_split():
+    from paper_1511_04348_b200.dense import set_splitk
+
+    yield lambda on: set_splitk(1 if on else 8)
+    set_splitk(8)
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+@pytest.mark.parametrize("m,k,n,tile,cap", [(300, 5000, 10, 512, None), (200, 3000, 700, 1024, None),
+                                             (130, 2600, 40, 256, 5)])
+def test_split_k_exact_on_integers(no_split, precision, m, k, n, tile, cap):
+    """Skinny outputs run split-K (partials reduced in a fixed order); integer
+    inputs make every summation order exact, so split and unsplit agree bitwise
+    (cap=5 also forces chunked launches that accumulate into C)."""
+    rng = np.random.default_rng(m + n)
+    a, b = int_matrix(rng, m, k), int_matrix(rng, k, n)
+    machine = homogeneous_machine(2, capacity_tiles=cap)
+    outs = []
+    for off in (False, True):
+        no_split(off)
+        c, s = run(machine, a, b, tile, precision=precision)
+        outs.append(c)
+    assert np.array_equal(outs[0], O.reference_gemm(a, b))
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_split_k_normal_data_and_fused_posts(no_split):
+    g = torch.Generator().manual_seed(11)
+    f = lambda *s: torch.randn(*s, generator=g, dtype=torch.float64)
+    x, w, bias = f(1000, 8192), f(8192, 10), f(10)
+    dy, w2 = f(1000, 10), f(784, 10)
+    a_prev = torch.rand(1000, 784, generator=g, dtype=torch.float64)
+    dev = lambda t: t.float().cuda().contiguous()
+    res = {}
+    for off in (False, True):
+        no_split(off)
+        rt = Runtime(homogeneous_machine(1, dtype=np.float32), 4096)
+        o1 = torch.empty(1000, 10, device="cuda")
+        o2 = torch.empty(1000, 784, device="cuda")
+        s = rt.multiply_batch([dict(a=dev(x), b=dev(w), out=o1, post=("bias_act", dev(bias), "sigmoid")),
+                               dict(a=dev(dy), b=dev(w2), out=o2, transpose_b=True,
+                                    post=("act_grad", dev(a_prev), "sigmoid"))])
+        assert s.total_tasks == 2
+        res[off] = (o1.double().cpu(), o2.double().cpu(), s.gpu_launches)
+        rt.close()
+    r32 = lambda t: t.float().double()  # the operands the GPU actually sees
+    ref1 = torch.sigmoid(r32(x) @ r32(w) + r32(bias))
+    ref2 = (r32(dy) @ r32(w2).T) * (r32(a_prev) * (1 - r32(a_prev)))
+    # pre-activations here are ~N(0, 8192): the product's 1e-5 relative error is
+    # relative to that scale, and the sigmoid (which maps it into (0, 1)) amplifies
+    # it in relative terms, hence 5e-5 for the fused output
+    for o1, o2, _ in res.values():
+        assert rel(o1.numpy(), ref1.numpy()) <= 5e-5
+        assert rel(o2.numpy(), ref2.numpy()) <= 1e-5
+    assert rel(res[False][0].numpy(), res[True][0].numpy()) <= 1e-5  # split vs unsplit: summation order only
+    assert res[False][2] > res[True][2]  # the split run launched reduction kernels
