@@ -58,7 +58,7 @@ def parse():
     p.add_argument("--n", type=int, default=32768, help="matrix size (cfg2: 32768)")
     p.add_argument("--tile", type=int, default=4096)
     p.add_argument("--precision", default="fp32acc", choices=["fp32acc", "bf16"])
-    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--e2e-steps", type=int, default=5)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
@@ -234,6 +234,17 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],
             "h2d_bytes_per_step": int(x.size * 4 + t.size * 4), "d2h_bytes_per_step": 8}
+
+
+def sim_prediction_ms(tr, n, T, world, precision):
+    """The reference's own scheduler (its sim engine, scheduler.py:432-464, replayed
+    bit-exactly by mode="sim") fed this B200's measured rates: what the reference's
+    schedule -- no fetch-ahead, fetch/writeback on one transfer clock -- would take
+    for the same cold product.  A model, not a measurement."""
+    z = np.lib.stride_tricks.as_strided(np.zeros(1, np.float32), (n, n), (0, 0))  # never read
+    with tr.Runtime(tr.b200_sim_machine(world, precision), T, mode="sim", compute=False) as rt:
+        _, s = rt.multiply(z, z)
+    return s.makespan * 1e3
 
 
 def mlp_cpu_baseline(sizes, batch, target_s=6.0):
@@ -435,7 +446,10 @@ def main():
             del res
         times = []
         h2d = d2h = 0
+        c_host = None
+        detail = []  # per step: [event ms, native wall ms, device span ms]
         for _ in range(max(1, args.e2e_steps)):
+            c_host = None  # release the previous result: its pinned block serves this step's output
             barrier()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -449,6 +463,7 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
+            detail.append([round(times[-1] * 1e3, 2), round(s.wall_elapsed * 1e3, 2), round(max(s.span_ms.values()), 2)])
             h2d = s.cache.bytes_host
             d2h = s.cache.bytes_writeback
         e2e_parity = None
@@ -465,7 +480,9 @@ def main():
         e2e = {"value": flops / t_e2e / 1e12, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": t_e2e * 1e3,
                "call": "paper_1511_04348_b200.run(machine, A_host_pinned, B_host_pinned, 4096)",
-               "parity_rel_fro_sampled": e2e_parity}
+               "steps_ms_event_wall_span": detail,
+               "parity_rel_fro_sampled": e2e_parity,
+               "sim_reference_schedule_ms": sim_prediction_ms(tr, n, T, world, args.precision)}
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None

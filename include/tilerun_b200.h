@@ -76,12 +76,12 @@ int tr_queue_is_empty(tr_queue* q, int32_t* empty);
 /* ------------------------------------- machine description (devices.py:30-216) */
 typedef struct {
   int32_t device_id;      /* DeviceSpec.device_id (devices.py:43)                       */
-  int32_t kind;           /* tr_device_kind; host workers are rejected by sessions       */
+  int32_t kind;           /* tr_device_kind; host workers only in TR_FLAG_SIM sessions    */
   int64_t capacity_tiles; /* DeviceSpec.capacity_tiles; -1 = unbounded (HBM-budget bound)  */
   int32_t slots;          /* reservation-station width (devices.py:49), = CUDA streams   */
   int32_t gpu;            /* physical CUDA ordinal; -1 = device_id % visible GPUs        */
-  double flops_per_unit;  /* kept for config round-trip; unused on hardware            */
-  double host_bandwidth;  /* idem                                                      */
+  double flops_per_unit;  /* simulated engine: flops per time unit (devices.py:255-261)   */
+  double host_bandwidth;  /* simulated engine: bytes per time unit to/from host (264-283) */
 } tr_device_spec;
 
 typedef struct {
@@ -89,6 +89,8 @@ typedef struct {
   const tr_device_spec* devices;
   const int64_t* hops;    /* n x n ProximityMatrix.hops (devices.py:78-118)             */
   int32_t element_bytes;  /* Machine.element_bytes (devices.py:145-154): byte accounting */
+  const double* peer_bandwidth; /* n x n ProximityMatrix.peer_bandwidth (simulated engine; may be NULL) */
+  double transfer_latency;      /* Machine.transfer_latency (simulated engine)                  */
 } tr_machine;
 
 /* ----------------------------------- cache directory (coherence.py:86-313) */
@@ -156,7 +158,10 @@ enum {
   TR_FLAG_DRYRUN = 1u << 3,    /* schedule-only test mode: no CUDA, no arithmetic, C untouched */
   TR_FLAG_FIFO = 1u << 4,      /* FIFO eviction instead of LRU                          */
   TR_FLAG_NO_PREFETCH = 1u << 5, /* disable fetch-ahead of reserved tasks' input tiles  */
-  TR_FLAG_TRACE = 1u << 6       /* record a device timeline of every copy/kernel (tr_session_trace) */
+  TR_FLAG_TRACE = 1u << 6,      /* record a device timeline of every copy/kernel (tr_session_trace) */
+  TR_FLAG_SIM = 1u << 7         /* simulated engine (scheduler.py:432-464): the reference's deterministic
+                                   event order and cost model, per-device clocks persisting across calls,
+                                   host workers allowed; no CUDA, no arithmetic (implies DRYRUN) */
 };
 
 typedef struct {
@@ -174,6 +179,7 @@ typedef struct {
 typedef struct {
   int32_t thief, victim;
   int64_t task_id;
+  double time;    /* simulated time of the steal (TR_FLAG_SIM sessions), else 0 */
 } tr_steal_event; /* scheduler.py:252-258 (queue_empty_observed is always true) */
 
 typedef struct {
@@ -190,6 +196,7 @@ typedef struct {
   int64_t steals_cap;
   uint8_t* completion;              /* total_tasks bytes: exactly-once bitmap snapshot */
   int64_t completion_cap;
+  double makespan;                  /* TR_FLAG_SIM: simulated time of this call (scheduler.py:602), else 0 */
 } tr_gemm_report;
 
 /* Runtime(machine, tile_size, mode, steal, coherence, seed, directory_debug)
@@ -255,6 +262,9 @@ int tr_session_trace(tr_session* s, tr_trace_event* out, int64_t cap, int64_t* n
 /* Device-side span (ms) of the last tr_gemm on each device: CUDA events recorded
  * before the first and after the last operation of every worker stream. */
 int tr_session_span_ms(tr_session* s, double* per_device_ms /* n_devices */);
+/* TR_FLAG_SIM sessions: max over devices of their compute / transfer clocks
+ * (Runtime.sim_now, scheduler.py:552-553); 0 for other sessions. */
+int tr_session_sim_now(tr_session* s, double* out);
 /* Tasks a device keeps executing concurrently (default min(2, slots)); the rest
  * of its reservation-station entries stay reserved (stealable).  1 serialises
  * a device's tasks, which the roofline measurement uses. */

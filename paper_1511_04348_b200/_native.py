@@ -28,6 +28,7 @@ TR_KIND_ACCELERATOR, TR_KIND_HOST_WORKER = 0, 1
 TR_ACT_IDENTITY, TR_ACT_SIGMOID, TR_ACT_RELU = 0, 1, 2
 TR_FLAG_STEAL, TR_FLAG_COHERENCE, TR_FLAG_DEBUG, TR_FLAG_DRYRUN, TR_FLAG_FIFO, TR_FLAG_NO_PREFETCH, TR_FLAG_TRACE = \
     1, 2, 4, 8, 16, 32, 64
+TR_FLAG_SIM = 128
 
 i32, i64, u64, u8, f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_uint8, C.c_double
 P = C.POINTER
@@ -39,7 +40,8 @@ class DeviceSpecC(C.Structure):
 
 
 class MachineC(C.Structure):
-    _fields_ = [("n_devices", i32), ("devices", P(DeviceSpecC)), ("hops", P(i64)), ("element_bytes", i32)]
+    _fields_ = [("n_devices", i32), ("devices", P(DeviceSpecC)), ("hops", P(i64)), ("element_bytes", i32),
+                ("peer_bandwidth", P(f64)), ("transfer_latency", f64)]
 
 
 class TileKeyC(C.Structure):
@@ -65,7 +67,7 @@ class DeviceStatsC(C.Structure):
 
 
 class StealEventC(C.Structure):
-    _fields_ = [("thief", i32), ("victim", i32), ("task_id", i64)]
+    _fields_ = [("thief", i32), ("victim", i32), ("task_id", i64), ("time", f64)]
 
 
 class ProductC(C.Structure):
@@ -90,7 +92,7 @@ class GemmReportC(C.Structure):
                 ("wall_seconds", f64), ("cache", CacheStatsC), ("n_steals", i64), ("gpu_launches", i64),
                 ("cache_per_device", P(CacheStatsC)), ("devices", P(DeviceStatsC)),
                 ("steals", P(StealEventC)), ("steals_cap", i64), ("completion", P(u8)),
-                ("completion_cap", i64)]
+                ("completion_cap", i64), ("makespan", f64)]
 
 
 vp = C.c_void_p
@@ -147,6 +149,7 @@ _PROTOS = {
     "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
     "tr_session_set_external_stream": [vp, vp, i32],
     "tr_session_set_async": [vp, i32],
+    "tr_session_sim_now": [vp, P(f64)],
     "tr_session_forget": [vp, u64, P(i64)],
 }
 

@@ -351,6 +351,9 @@ int tr_session_trace(tr_session* s, tr_trace_event* out, int64_t cap, int64_t* n
 int tr_session_span_ms(tr_session* s, double* per_device_ms) {
   return guarded([&] { s->s->span_ms(per_device_ms); });
 }
+int tr_session_sim_now(tr_session* s, double* out) {
+  return guarded([&] { *out = s->s->sim_now(); });
+}
 int tr_session_set_inflight(tr_session* s, int32_t max_inflight) {
   return guarded([&] {
     if (max_inflight < 1) tr::fail(TR_ERR_VALUE, "max_inflight must be >= 1");

@@ -1,5 +1,7 @@
 #include "devpool.h"
 
+#include <chrono>
+
 namespace tr {
 
 DevPool& DevPool::get() {
@@ -26,8 +28,32 @@ cudaError_t DevPool::alloc(int gpu, size_t bytes, void** out, size_t* cap) {
     trim();  // give cached blocks back and retry once
     e = cudaMalloc(out, bytes);
   }
-  if (e == cudaSuccess) *cap = bytes;
+  if (e == cudaSuccess) {
+    *cap = bytes;
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_info_.find(gpu);
+    if (it != free_info_.end()) it->second.bytes -= std::min(it->second.bytes, bytes);  // keep the cached view honest
+  }
   return e;
+}
+
+cudaError_t DevPool::free_bytes(int gpu, size_t* out, double max_age_s) {
+  const double now = std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  {
+    std::lock_guard<std::mutex> g(mu_);
+    auto it = free_info_.find(gpu);
+    if (it != free_info_.end() && now - it->second.when < max_age_s) {
+      *out = it->second.bytes;
+      return cudaSuccess;
+    }
+  }
+  size_t f = 0, t = 0;
+  cudaError_t e = cudaMemGetInfo(&f, &t);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(mu_);
+  free_info_[gpu] = FreeInfo{f, now};
+  *out = f;
+  return cudaSuccess;
 }
 
 void DevPool::release(int gpu, void* p, size_t cap) {
@@ -45,6 +71,7 @@ void DevPool::trim() {
     for (auto& b : kv.second) cudaFree(b.second);
     kv.second.clear();
   }
+  free_info_.clear();  // free memory changed: re-query next time
   if (prev >= 0) cudaSetDevice(prev);
 }
 

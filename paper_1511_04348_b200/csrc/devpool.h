@@ -26,10 +26,19 @@ class DevPool {
   void release(int gpu, void* p, size_t cap);
   void trim();  // cudaFree every cached block
   size_t cached_bytes();
+  // Free HBM on the current device `gpu` (cudaMemGetInfo), re-queried at most
+  // once per `max_age_s`: the query occasionally stalls for tens of ms, which a
+  // one-shot run() per product would otherwise pay on every call.
+  cudaError_t free_bytes(int gpu, size_t* out, double max_age_s = 10.0);
 
  private:
   std::mutex mu_;
   std::map<int, std::multimap<size_t, void*>> free_;  // gpu -> size -> ptr
+  struct FreeInfo {
+    size_t bytes = 0;
+    double when = -1e30;
+  };
+  std::map<int, FreeInfo> free_info_;
 };
 
 }  // namespace tr

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <functional>
+#include <queue>
 #include <string>
 
 #include "common.h"
@@ -55,7 +57,8 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   if (tile < 1) fail(TR_ERR_SHAPE, "tile_size must be >= 1, got %d", tile);
   if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC) fail(TR_ERR_VALUE, "unknown precision %d", precision);
   if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
-  dryrun_ = flags & TR_FLAG_DRYRUN;
+  sim_ = flags & TR_FLAG_SIM;
+  dryrun_ = (flags & TR_FLAG_DRYRUN) || sim_;
   steal_ = flags & TR_FLAG_STEAL;
   coherence_ = flags & TR_FLAG_COHERENCE;
   tracing_ = (flags & TR_FLAG_TRACE) && !(flags & TR_FLAG_DRYRUN);
@@ -71,13 +74,28 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   for (int d = 0; d < n; ++d) {
     const tr_device_spec& ds = m.devices[d];
     if (ds.device_id != d) fail(TR_ERR_CONFIG, "device ids must be 0..%d in order", n - 1);
-    if (ds.kind != TR_KIND_ACCELERATOR)
+    if (ds.kind != TR_KIND_ACCELERATOR && !sim_)
       fail(TR_ERR_CONFIG, "device %d is a host-worker: the B200 runtime has no CPU compute path", d);
+    hw[d] = ds.kind == TR_KIND_HOST_WORKER;
     if (ds.slots < 1 || ds.slots > 32) fail(TR_ERR_CONFIG, "device %d: slots must be in 1..32", d);
     caps[d] = ds.capacity_tiles;
     if (caps[d] >= 0 && caps[d] < 3) fail(TR_ERR_CONFIG, "capacity_tiles must be >= 3 (A+B+C working set)");
   }
   for (int64_t i = 0; i < static_cast<int64_t>(n) * n; ++i) hops[i] = m.hops ? m.hops[i] : (i % (n + 1) ? 1 : 0);
+  if (sim_) {
+    clocks_.assign(n, SimClock{});
+    host_worker_ = hw;
+    latency_ = m.transfer_latency;
+    for (int d = 0; d < n; ++d) {
+      const tr_device_spec& ds = m.devices[d];
+      if (!(ds.flops_per_unit > 0) || (!hw[d] && !(ds.host_bandwidth > 0)))
+        fail(TR_ERR_CONFIG, "device %d: flops_per_unit and host_bandwidth must be > 0", d);
+      flops_.push_back(ds.flops_per_unit);
+      host_bw_.push_back(ds.host_bandwidth);
+    }
+    peer_bw_.assign(static_cast<size_t>(n) * n, 0.0);
+    for (int64_t i = 0; i < static_cast<int64_t>(n) * n; ++i) peer_bw_[i] = m.peer_bandwidth ? m.peer_bandwidth[i] : 0.0;
+  }
   dir_ = std::make_unique<Directory>(n, caps, hw, hops, coherence_, (flags & TR_FLAG_FIFO) ? TR_POLICY_FIFO : TR_POLICY_LRU,
                                      (flags & TR_FLAG_DEBUG) != 0);
 
@@ -104,13 +122,19 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
     dc.station = std::make_unique<Station>(d, dc.width);
     station_ptrs_.push_back(dc.station.get());
   }
+  const bool tdebug = getenv("TR_TIMING") != nullptr;  // session set-up timing on stderr
+  auto tnow = [] { return std::chrono::steady_clock::now(); };
+  auto tms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+    return std::chrono::duration<double, std::milli>(b - a).count();
+  };
   if (!dryrun_) {
     for (int d = 0; d < n; ++d) {
       DeviceCtx& dc = devs_[d];
+      const auto q0 = tnow();
       TR_CUDA(cudaSetDevice(dc.gpu));
       TR_CUDA(cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dc.gpu));
-      size_t free_b = 0, total_b = 0;
-      TR_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      size_t free_b = 0;
+      TR_CUDA(DevPool::get().free_bytes(dc.gpu, &free_b));
       const double reusable = static_cast<double>(free_b) + static_cast<double>(DevPool::get().cached_bytes());
       int64_t budget = hbm_budget_ > 0 ? hbm_budget_ : static_cast<int64_t>(0.8 * reusable);
       budget /= per_gpu[dc.gpu];
@@ -122,6 +146,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
       if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
       dc.max_slots = static_cast<int32_t>(slots);
+      const auto q1 = tnow();
       dc.streams.resize(dc.width + 2);  // + fill (convert) stream [width] + copy stream [width+1]
       TR_CUDA(cudaEventCreate(&dc.span_start));
       TR_CUDA(cudaEventCreate(&dc.span_end));
@@ -138,6 +163,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
       }
       for (int k = 0; k < kStage; ++k) TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &dc.stage[k], &dc.stage_cap[k]));
+      if (tdebug) fprintf(stderr, "[tr] session dev %d: meminfo %.2f ms, streams+buffers %.2f ms\n", d, tms(q0, q1), tms(q1, tnow()));
     }
     // Peer access between every pair of distinct GPUs in use (NVLink / NVSwitch).
     for (int d = 0; d < n; ++d) {
@@ -154,7 +180,9 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       }
     }
   }
+  const auto q2 = tnow();
   for (int d = 0; d < n; ++d) devs_[d].worker = std::thread(&Session::worker_main, this, d);
+  if (tdebug) fprintf(stderr, "[tr] session threads %.2f ms\n", tms(q2, tnow()));
 }
 
 Session::~Session() {
@@ -737,7 +765,7 @@ void Session::run_job(int d, Job& job) {
     }
     if (victim >= 0) {
       std::lock_guard<std::mutex> g(job.mu);
-      job.steals.push_back(tr_steal_event{d, victim, static_cast<int64_t>(tid)});
+      job.steals.push_back(tr_steal_event{d, victim, static_cast<int64_t>(tid), 0.0});
       dc.stats.steals_performed += 1;
       devs_[victim].stats.steals_suffered += 1;
     }
@@ -777,6 +805,103 @@ void Session::worker_main(int d) {
       workers_done_ += 1;
     }
     cv_done_.notify_all();
+  }
+}
+
+// ---------------------------------------------------------------- simulated engine
+// The reference's sim engine (scheduler.py:432-464) with its cost model
+// (devices.py:255-283), replayed natively: devices are served in order of their
+// compute clock (ties to the lower id), each refills its station, pops (or,
+// after observing an empty queue, steals), and runs the whole task's directory
+// sequence at once; fetch k+1 overlaps compute k, the writeback waits for the
+// last accumulate.  Every double is formed in the reference's operation order,
+// so makespans match the reference bit for bit.
+double Session::sim_now() const {
+  double t = 0.0;
+  for (const SimClock& c : clocks_) t = std::max(t, std::max(c.compute, c.transfer));
+  return t;
+}
+
+double Session::xfer_cost(int src, int dst, int64_t nbytes) const {
+  if (src == dst) return 0.0;
+  if (src == TR_SOURCE_HOST || dst == TR_SOURCE_HOST) {
+    const int dev = src == TR_SOURCE_HOST ? dst : src;
+    if (host_worker_[dev]) return 0.0;
+    return static_cast<double>(nbytes) / host_bw_[dev] + latency_;
+  }
+  return static_cast<double>(nbytes) / peer_bw_[static_cast<size_t>(src) * n_devices() + dst] + latency_;
+}
+
+void Session::sim_task(int d, Job& job, int64_t gtid, double t) {
+  int64_t tid = 0;
+  const Product& p = job.prod_of(gtid, &tid);
+  const int64_t T = tile_;
+  const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+  const int64_t mt = std::min(T, p.M - i * T);
+  const int64_t nt = std::min(T, p.N - j * T);
+  const TileKey c_key{p.c_uid, i, j};
+  std::vector<std::pair<double, double>> steps;
+  steps.reserve(static_cast<size_t>(p.k_steps));
+  {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    dir_->admit_output_locked(d, c_key);  // scheduler.py:390
+    for (int64_t k = 0; k < p.k_steps; ++k) {
+      const int64_t ar = p.ta ? k : i, ac = p.ta ? i : k;
+      const int64_t br = p.tb ? j : k, bc = p.tb ? k : j;
+      const int64_t na = std::min(T, p.a.rows - ar * T) * std::min(T, p.a.cols - ac * T) * element_bytes_;
+      const int64_t nb = std::min(T, p.b.rows - br * T) * std::min(T, p.b.cols - bc * T) * element_bytes_;
+      const TileKey ka{p.a_uid, ar, ac}, kb{p.b_uid, br, bc};
+      const Acquired ra = dir_->acquire_input_locked(d, ka, na);
+      const Acquired rb = dir_->acquire_input_locked(d, kb, nb);
+      const double fetch = xfer_cost(ra.source, d, ra.nbytes) + xfer_cost(rb.source, d, rb.nbytes);
+      const int64_t kt = std::min(T, p.K - k * T);
+      const double compute = 2.0 * static_cast<double>(mt) * static_cast<double>(kt) * static_cast<double>(nt) / flops_[d];
+      dir_->release_input_locked(d, ka);
+      dir_->release_input_locked(d, kb);
+      steps.emplace_back(fetch, compute);
+    }
+    const int64_t wb_bytes = mt * nt * element_bytes_;
+    const double wb = xfer_cost(d, TR_SOURCE_HOST, wb_bytes);
+    dir_->release_output_locked(d, c_key, wb_bytes);
+    SimClock& eng = clocks_[d];
+    double tr = std::max(eng.transfer, t);  // transfers for this task cannot predate claiming it
+    double co = eng.compute;
+    for (const auto& st : steps) {
+      tr += st.first;
+      co = std::max(co, tr) + st.second;  // fetch k+1 overlaps compute k
+    }
+    tr = std::max(tr, co) + wb;  // the writeback waits for the last accumulate
+    eng.transfer = tr;
+    eng.compute = co;
+  }
+  job.mark(gtid);
+  devs_[d].stats.tasks_completed += 1;
+}
+
+void Session::run_sim(Job& job) {
+  using Ev = std::pair<double, int>;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> heap;
+  for (int d = 0; d < n_devices(); ++d) heap.emplace(clocks_[d].compute, d);
+  while (!heap.empty()) {
+    const Ev top = heap.top();
+    heap.pop();
+    const double t = top.first;
+    const int d = top.second;
+    Station& st = *devs_[d].station;
+    job.claimed.fetch_add(static_cast<int64_t>(st.refill(job.queue, st.width()).size()));
+    uint64_t tid = 0;
+    if (!st.pop_for_run(&tid)) {
+      int victim = -1;
+      bool got = false;
+      if (steal_ && job.queue.is_empty())
+        got = steal_task(d, station_ptrs_.data(), static_cast<int>(station_ptrs_.size()), &tid, &victim);
+      if (!got) continue;  // queue drained and nothing stealable: the device retires
+      job.steals.push_back(tr_steal_event{d, victim, static_cast<int64_t>(tid), t});
+      devs_[d].stats.steals_performed += 1;
+      devs_[victim].stats.steals_suffered += 1;
+    }
+    sim_task(d, job, static_cast<int64_t>(tid), t);
+    heap.emplace(clocks_[d].compute, d);
   }
 }
 
@@ -905,6 +1030,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     const int64_t cap = dc.capacity >= 0 ? dc.capacity : (dryrun_ ? INT64_MAX : dc.max_slots);
     room = std::min(room, cap);
   }
+  if (order < 0 && sim_) order = 0;  // the reference's row-major plan: exact sim parity
   if (order < 0) {
     bool bounded = false;
     for (auto& dc : devs_) bounded = bounded || dc.capacity >= 0;
@@ -978,18 +1104,24 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     }
   }
   const auto t0 = std::chrono::steady_clock::now();
-  {
-    std::lock_guard<std::mutex> lk(mu_);
-    job_ = &job;
-    workers_done_ = 0;
-    generation_ += 1;
+  const double sim_before = sim_now();
+  if (sim_) {
+    run_sim(job);  // one thread, the reference's event order (scheduler.py:432-464)
+  } else {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &job;
+      workers_done_ = 0;
+      generation_ += 1;
+    }
+    cv_.notify_all();
+    {
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_done_.wait(lk, [&] { return workers_done_ == n_devices(); });
+      job_ = nullptr;
+    }
   }
-  cv_.notify_all();
-  {
-    std::unique_lock<std::mutex> lk(mu_);
-    cv_done_.wait(lk, [&] { return workers_done_ == n_devices(); });
-    job_ = nullptr;
-  }
+  last_makespan_ = sim_ ? sim_now() - sim_before : 0.0;
   if (job.async) {
     for (auto& dc : devs_) {
       TR_CUDA(cudaSetDevice(dc.gpu));
@@ -1064,6 +1196,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     rep->cache = sub_stats(dir_->stats(), before);
     rep->n_steals = static_cast<int64_t>(job.steals.size());
     rep->gpu_launches = job.launches.load();
+    rep->makespan = last_makespan_;
     const auto after_dev = dir_->stats_per_device();
     for (int d = 0; d < n_devices(); ++d) {
       if (rep->cache_per_device) rep->cache_per_device[d] = sub_stats(after_dev[d], before_dev[d]);

@@ -119,6 +119,7 @@ class Session {
     ext_on_ = on;
   }
   void set_async(bool on) { async_ = on; }
+  double sim_now() const;
   const std::vector<tr_trace_event>& trace() const { return last_trace_; }
 
  private:
@@ -189,6 +190,10 @@ class Session {
   void worker_main(int d);
   void run_job(int d, Job& job);
   void issue(int d, Job& job, int64_t tid, int s);
+  // simulated engine (TR_FLAG_SIM)
+  void run_sim(Job& job);
+  void sim_task(int d, Job& job, int64_t gtid, double t);
+  double xfer_cost(int src, int dst, int64_t nbytes) const;
   void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
   int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
                   int scratch);
@@ -230,6 +235,17 @@ class Session {
   cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
   bool ext_on_ = false;                // ext_stream_ set (nullptr = the legacy default stream)
   bool async_ = false;                 // device-resident products return once enqueued (see run_products)
+  // simulated engine: reference cost model (devices.py:255-283) and per-device
+  // compute / transfer clocks that persist across calls (scheduler.py:416-429)
+  bool sim_ = false;
+  struct SimClock {
+    double compute = 0.0, transfer = 0.0;
+  };
+  std::vector<SimClock> clocks_;
+  std::vector<double> flops_, host_bw_, peer_bw_;
+  std::vector<bool> host_worker_;
+  double latency_ = 0.0;
+  double last_makespan_ = 0.0;
   cudaEvent_t ext_ready_ = nullptr;
   bool tracing_ = false;
   std::vector<tr_trace_event> last_trace_;

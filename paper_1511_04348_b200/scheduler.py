@@ -33,12 +33,13 @@ from . import _native as N
 from .coherence import CacheDirectory, CacheStats, UidTable
 from .dense import precision_code
 from .devices import Machine
+from .errors import NoDeviceError
 from .matrix import describe, is_device_tensor, pinned_empty, pinned_zeros
 from .msqueue import MichaelScottQueue
 from .tiles import TiledMatrix, TileKey, decode_task, partition
 
 SCHEMA_VERSION = 1
-MODES = ("gpu", "threaded", "dryrun")
+MODES = ("gpu", "threaded", "dryrun", "sim")
 
 
 class TaskState(Enum):
@@ -377,11 +378,8 @@ class Runtime:
     def __init__(self, machine: Machine, tile_size: int, mode: str = "gpu", steal: bool = True,
                  coherence: bool = True, seed: int | None = None, directory_debug: bool = False,
                  precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru",
-                 fetch_ahead: bool = True, trace: bool = False):
+                 fetch_ahead: bool = True, trace: bool = False, compute: bool = True):
         if mode not in MODES:
-            if mode == "sim":
-                raise ValueError("mode 'sim' is the reference's simulated engine; the B200 runtime executes on "
-                                 "hardware: use mode='gpu' (or 'threaded'), or 'dryrun' for schedule-only runs")
             raise ValueError(f"unknown mode {mode!r}")
         if tile_size < 1:
             raise ValueError(f"tile_size must be >= 1, got {tile_size}")
@@ -395,6 +393,8 @@ class Runtime:
         flags = (N.TR_FLAG_STEAL if steal else 0) | (N.TR_FLAG_COHERENCE if coherence else 0)
         flags |= N.TR_FLAG_DEBUG if directory_debug else 0
         flags |= N.TR_FLAG_DRYRUN if mode == "dryrun" else 0
+        flags |= N.TR_FLAG_SIM if mode == "sim" else 0
+        self.compute = compute
         flags |= N.TR_FLAG_FIFO if policy == "fifo" else 0
         flags |= 0 if fetch_ahead else N.TR_FLAG_NO_PREFETCH
         flags |= N.TR_FLAG_TRACE if trace else 0
@@ -457,8 +457,10 @@ class Runtime:
         return f"{prefix}#{self._uid_n}"
 
     def sim_now(self) -> float:
-        """No simulated clocks on hardware: always 0.0 (scheduler.py:552-553)."""
-        return 0.0
+        """Simulated time of the session (mode="sim"; scheduler.py:552-553), else 0.0."""
+        out = N.f64()
+        N.call("tr_session_sim_now", self._h, C.byref(out))
+        return out.value
 
     def operand(self, m, uid: str | None = None, transposed: bool = False) -> Operand:
         tiled = m if isinstance(m, TiledMatrix) else partition(m, self.tile_size)
@@ -485,7 +487,7 @@ class Runtime:
         if ak != bk:
             raise ValueError(f"inner dimensions differ: {a_op.element_shape} x {b_op.element_shape}")
         c_uid = c_uid or self.fresh_uid("c")
-        dry = self.mode == "dryrun"
+        dry = self.mode in ("dryrun", "sim")
         if out is None:
             out = None if dry else _zeros_like_output(a_op, am, bn, pinned=True, zero=False)
         ma = self._desc(a_op.tiled.base, dry)
@@ -499,7 +501,34 @@ class Runtime:
                    int(b_op.transposed), C.byref(mc), ids[2], int(task_offset), int(task_stride), C.byref(rep))
 
         stats = self._execute(call, total, lambda t: t % task_stride == task_offset)
+        if self.mode == "sim" and self.compute:
+            out = self._sim_product(a_op, b_op, out)
         return out, stats
+
+    def _sim_product(self, a_op: Operand, b_op: Operand, out):
+        """The numbers of a simulated run: the reference's sim engine computes the
+        product alongside its simulated clock; here the same sm_100a tile kernel
+        computes it in one dense launch (dense_gemm) -- there is no CPU path."""
+        if N.cuda_device_count() < 1:
+            raise NoDeviceError("mode='sim' computes the product on the GPU; Runtime(..., compute=False) "
+                                "simulates schedule, counters and time only")
+        import torch
+
+        from .dense import dense_gemm
+
+        on_device = is_device_tensor(a_op.tiled.base)
+        to_dev = lambda x: x if is_device_tensor(x) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
+        a, b = to_dev(a_op.tiled.base), to_dev(b_op.tiled.base)
+        if b.dtype != a.dtype:
+            b = b.to(a.dtype)
+        c = dense_gemm(a, b, transpose_a=a_op.transposed, transpose_b=b_op.transposed, precision=self.precision)
+        if out is not None:
+            if is_device_tensor(out):
+                out.copy_(c)
+            else:
+                out[...] = c.cpu().numpy()
+            return out
+        return c if on_device else c.cpu().numpy()
 
     def multiply_batch(self, products) -> RunStats:
         """Independent products scheduled as ONE round (tr_gemm_batch): their tasks
@@ -509,6 +538,8 @@ class Runtime:
         ``a_uid``/``b_uid``/``c_uid``, and an optional fused epilogue
         ``post=("bias_act", bias, activation)`` or ``post=("act_grad", a_prev,
         activation)`` (float32 device outputs).  Returns the combined RunStats."""
+        if self.mode == "sim":
+            raise ValueError("multiply_batch runs on the GPU; the simulated engine takes one product per call")
         acts = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
         arr = (N.ProductC * len(products))()
         keep = []
@@ -574,8 +605,9 @@ class Runtime:
                      for d in range(n)},
             cache=CacheStats.from_c(rep.cache),
             cache_per_device={d: CacheStats.from_c(per_cache[d]) for d in range(n)},
-            makespan=None, wall_elapsed=float(rep.wall_seconds),
-            steal_events=[StealEvent(int(steals[i].thief), int(steals[i].victim), int(steals[i].task_id), True)
+            makespan=float(rep.makespan) if self.mode == "sim" else None, wall_elapsed=float(rep.wall_seconds),
+            steal_events=[StealEvent(int(steals[i].thief), int(steals[i].victim), int(steals[i].task_id), True,
+                                     float(steals[i].time) if self.mode == "sim" else None)
                           for i in range(min(int(rep.n_steals), total))],
             precision=self.precision, gpu_launches=int(rep.gpu_launches),
             kernel_ms={d: float(kms[d]) for d in range(n)},
@@ -611,10 +643,10 @@ class Runtime:
 
 
 def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool = True, coherence: bool = True,
-        seed: int | None = None, directory_debug: bool = False, precision: str = "fp32acc"):
+        seed: int | None = None, directory_debug: bool = False, precision: str = "fp32acc", compute: bool = True):
     """One-shot product through a fresh session with uids "A","B","C" (scheduler.py:615-621)."""
     rt = Runtime(machine, tile_size, mode=mode, steal=steal, coherence=coherence, seed=seed,
-                 directory_debug=directory_debug, precision=precision)
+                 directory_debug=directory_debug, precision=precision, compute=compute)
     try:
         return rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C")
     finally:

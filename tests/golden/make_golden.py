@@ -15,6 +15,10 @@ Fixtures
   directory.json   random op sequences on CacheDirectory and its answers
   ann.npz          DenseBackend MLP: forward/backward/grad values and training
                    trajectories (xor 50 steps; per-layer-scaled 24-40-40-6 net)
+  sim_runs.json    the reference's SIMULATED engine (scheduler.py:432-464): makespans
+                   (float.hex, bitwise), sim clocks, steal events with times, per-device
+                   task counts and counters for heterogeneous / bounded / host-worker /
+                   bypass / no-steal / non-uniform-fabric machines and multi-call sessions
   cfg1.npz         cfg1 (N=2048, T=512, float32 machine): the reference's own
                    threaded run -- stats, sampled output blocks and per-tile checksums,
                    plus the float64 reference_gemm checksums of the same inputs
@@ -252,6 +256,98 @@ def tile_checksums(c, t):
                      for i in range(g)])
 
 
+def _sim_record(stats, rt=None):
+    rec = stats_dict(stats)
+    rec["makespan"] = float(stats.makespan).hex()
+    rec["steal_events"] = [[e.thief, e.victim, e.task_id, float(e.time).hex()] for e in stats.steal_events]
+    if rt is not None:
+        rec["sim_now"] = float(rt.sim_now()).hex()
+    return rec
+
+
+def _sim_machines():
+    D = ref.DeviceSpec
+    out = {}
+    out["homog1"] = ref.homogeneous_machine(1)
+    out["homog3"] = ref.homogeneous_machine(3)
+    out["hetero_1234"] = ref.Machine([D(i, flops_per_unit=1000.0 * (i + 1), host_bandwidth=8192.0) for i in range(4)],
+                                     ref.ProximityMatrix.uniform(4, bandwidth=32768.0))
+    out["bounded_cap6"] = ref.homogeneous_machine(3, capacity_tiles=6)
+    out["cap3_2dev"] = ref.homogeneous_machine(2, capacity_tiles=3)
+    out["host_worker_mix"] = ref.Machine(
+        [D(0, flops_per_unit=2000.0, host_bandwidth=4096.0), D(1, flops_per_unit=1500.0, host_bandwidth=8192.0, slots=2),
+         D(2, kind="host-worker", flops_per_unit=300.0, host_bandwidth=1.0, subtile_factor=2)],
+        ref.ProximityMatrix.uniform(3, bandwidth=16384.0))
+    hops = np.array([[0, 1, 2, 2], [1, 0, 2, 2], [2, 2, 0, 1], [2, 2, 1, 0]])
+    bw = np.array([[1.0, 50000.0, 9000.0, 9000.0], [50000.0, 1.0, 9000.0, 9000.0],
+                   [9000.0, 9000.0, 1.0, 50000.0], [9000.0, 9000.0, 50000.0, 1.0]])
+    out["fabric_latency"] = ref.Machine([D(i, flops_per_unit=1000.0 + 250.0 * i, host_bandwidth=6000.0 + 1000.0 * i,
+                                           slots=3 + (i % 2)) for i in range(4)],
+                                        ref.ProximityMatrix(hops, bw), transfer_latency=0.37)
+    out["float32_homog2"] = ref.homogeneous_machine(2, dtype=np.float32)
+    return out
+
+
+SIM_CASES = [
+    # name, machine, m, k, n, tile, coherence, steal
+    ("homog1_12_t4", "homog1", 12, 12, 12, 4, True, True),
+    ("homog3_24_t4", "homog3", 24, 24, 24, 4, True, True),
+    ("hetero_64_t8", "hetero_1234", 64, 64, 64, 8, True, True),
+    ("hetero_64_t8_nosteal", "hetero_1234", 64, 64, 64, 8, True, False),
+    ("bounded_24_t4", "bounded_cap6", 24, 24, 24, 4, True, True),
+    ("cap3_16_t4", "cap3_2dev", 16, 16, 16, 4, True, True),
+    ("hostmix_30x18x25_t7", "host_worker_mix", 30, 18, 25, 7, True, True),
+    ("fabric_40_t5", "fabric_latency", 40, 40, 40, 5, True, True),
+    ("fabric_40_t5_bypass", "fabric_latency", 40, 40, 40, 5, False, True),
+    ("ragged_37x53x29_t8", "homog3", 37, 53, 29, 8, True, True),
+    ("t1_9x7x5", "float32_homog2", 9, 7, 5, 1, True, True),
+]
+
+
+def gen_sim():
+    machines = _sim_machines()
+    out = {"machines": {k: m.to_dict() for k, m in machines.items()}, "runs": {}, "sessions": {}}
+    for name, mk, m, k, n, t, coh, steal in SIM_CASES:
+        rng = np.random.default_rng(len(name))
+        a, b = int_matrix(rng, m, k), int_matrix(rng, k, n)
+        _, stats = ref.run(machines[mk], a, b, tile_size=t, mode="sim", coherence=coh, steal=steal)
+        out["runs"][name] = {"machine": mk, "m": m, "k": k, "n": n, "tile": t, "coherence": coh, "steal": steal,
+                             "stats": _sim_record(stats)}
+    # sessions: clocks and residency persist across calls (an ANN-like sequence
+    # with a transposed reuse of X and a re-multiply that hits L1 everywhere)
+    for mk in ("homog3", "fabric_latency", "hetero_1234"):
+        rng = np.random.default_rng(7)
+        x, w, dy = int_matrix(rng, 20, 12), int_matrix(rng, 12, 16), int_matrix(rng, 20, 16)
+        rt = ref.Runtime(machines[mk], tile_size=4)
+        seq = []
+        _, s = rt.multiply(x, w, a_uid="X", b_uid="W", c_uid="Y")
+        seq.append(_sim_record(s, rt))
+        _, s = rt.multiply(x, dy, transpose_a=True, a_uid="X", b_uid="DY", c_uid="DW")
+        seq.append(_sim_record(s, rt))
+        _, s = rt.multiply(dy, w, transpose_b=True, a_uid="DY", b_uid="W", c_uid="DX")
+        seq.append(_sim_record(s, rt))
+        _, s = rt.multiply(x, w, a_uid="X", b_uid="W", c_uid="Y2")
+        seq.append(_sim_record(s, rt))
+        out["sessions"][mk] = seq
+    # the reference CLI's sweep table (cli.py:131-189, sim engine), byte for byte
+    import tempfile
+
+    from tilerun import cli as ref_cli
+
+    sweeps = {}
+    with tempfile.TemporaryDirectory() as td:
+        dev = Path(td) / "devices.json"
+        ref.save_machine(dev, machines["fabric_latency"])
+        out["sweep_devices"] = machines["fabric_latency"].to_dict()
+        for name, extra in (("plain", []), ("bypass", ["--no-coherence"]), ("template", ["--devices", str(dev)])):
+            path = Path(td) / f"{name}.csv"
+            ref_cli.main(["sweep", "--sizes", "8,16,20", "--device-counts", "2,3", "--tile-size", "4", "--seed", "3",
+                          "--out", str(path), *extra])
+            sweeps[name] = path.read_text()
+    out["sweeps"] = sweeps
+    (HERE / "sim_runs.json").write_text(json.dumps(out, indent=1))
+
+
 def gen_cfg1():
     n, t = 2048, 512
     a = np.random.default_rng(1).standard_normal((n, n)).astype(np.float32)
@@ -277,7 +373,7 @@ def gen_cfg1():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["tiles", "plans", "runs", "directory", "ann", "cfg1"]
+    which = sys.argv[1:] or ["tiles", "plans", "runs", "directory", "ann", "sim", "cfg1"]
     for w in which:
         t0 = time.perf_counter()
         globals()[f"gen_{w}"]()

@@ -229,7 +229,7 @@ def test_static_shards_cover_every_task_once():
 
 def test_mode_and_config_errors():
     with pytest.raises(ValueError):
-        Runtime(homogeneous_machine(1), 4, mode="sim")
+        Runtime(homogeneous_machine(1), 4, mode="simulated")
     with pytest.raises(ValueError):
         Runtime(homogeneous_machine(1), 0, mode="dryrun")
     with pytest.raises(ConfigError):
@@ -237,6 +237,9 @@ def test_mode_and_config_errors():
                 mode="dryrun")
     with pytest.raises(ValueError):
         Runtime(homogeneous_machine(1), 4, mode="dryrun").multiply(np.zeros((4, 4)), np.zeros((5, 4)))
+    # host workers exist only in the simulated engine (no CPU compute path on hardware)
+    Runtime(Machine([DeviceSpec(0), DeviceSpec(1, kind="host-worker")], ProximityMatrix.uniform(2)), 4,
+            mode="sim", compute=False).close()
 
 
 def test_reports(tmp_path):
