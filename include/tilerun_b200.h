@@ -338,6 +338,12 @@ int tr_set_gemm_pairs(int32_t on);
  * or TR_SPLITK=<n> in the environment. */
 int tr_set_splitk(int32_t max_splits);
 
+/* Grouped launches (process-wide, sessions created afterwards): up to
+ * `max_tasks` (1..8) ready tasks of one product from a device's reservation
+ * station run as ONE tile-GEMM launch (device outputs, unchunked tasks).  Each
+ * task keeps its own directory sequence; 1 disables.  Default 4, or TR_GROUP=<n>. */
+int tr_set_task_group(int32_t max_tasks);
+
 #ifdef __cplusplus
 }
 #endif

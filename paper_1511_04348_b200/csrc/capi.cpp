@@ -464,6 +464,13 @@ int tr_set_gemm_pairs(int32_t on) {
   return guarded([&] { tr::set_gemm_pairs(on != 0); });
 }
 
+int tr_set_task_group(int32_t max_tasks) {
+  return guarded([&] {
+    if (max_tasks < 1 || max_tasks > tr::kMaxGroup) tr::fail(TR_ERR_VALUE, "task group must be in 1..%d", tr::kMaxGroup);
+    tr::set_task_group_max(max_tasks);
+  });
+}
+
 int tr_set_splitk(int32_t max_splits) {
   return guarded([&] {
     if (max_splits < 1 || max_splits > 8) tr::fail(TR_ERR_VALUE, "split-K factor must be in 1..8");

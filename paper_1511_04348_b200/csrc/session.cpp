@@ -58,6 +58,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC) fail(TR_ERR_VALUE, "unknown precision %d", precision);
   if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
   sim_ = flags & TR_FLAG_SIM;
+  max_group_ = task_group_max();
   dryrun_ = (flags & TR_FLAG_DRYRUN) || sim_;
   steal_ = flags & TR_FLAG_STEAL;
   coherence_ = flags & TR_FLAG_COHERENCE;
@@ -538,16 +539,20 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vect
 // (skinny MLP layers: N = 10, K = 784 edges) is split along K so that about
 // two waves of CTAs run; partials go to the stream's workspace and a reduction
 // kernel sums them in a fixed order (deterministic) and applies the epilogue.
+// K-splits for a launch of `ctas` output blocks over `total_kb` k-blocks: about
+// two waves of CTAs, at most splitk_max(), each split >= 8 k-blocks; 1 = no split.
+int split_factor(int64_t ctas, int total_kb, int64_t sms) {
+  const int smax = splitk_max();
+  if (smax < 2 || ctas >= sms) return 1;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({2 * sms / ctas, smax, total_kb / 8})));
+}
+
 void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
   args.k_split = 1;
-  const int smax = splitk_max();
-  if (smax < 2) return;
   int total_kb = 0;
   for (int k = 0; k < args.n_ksteps; ++k) total_kb += (args.k_len[k] + 63) / 64;
   const int64_t ctas = ((args.m_valid + 127) / 128) * static_cast<int64_t>((args.n_valid + 255) / 256);
-  const int64_t sms = devs_[d].sms;
-  if (ctas >= sms) return;
-  const int s = static_cast<int>(std::min<int64_t>({2 * sms / ctas, smax, total_kb / 8}));
+  const int s = split_factor(ctas, total_kb, devs_[d].sms);
   if (s < 2) return;
   const int64_t ws_ld = (args.n_valid + 255) / 256 * 256;
   const int64_t zstride = static_cast<int64_t>(args.m_valid) * ws_ld;
@@ -573,6 +578,140 @@ void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
   args.ws = sc.ws;
   args.ws_ld = ws_ld;
   args.ws_zstride = zstride;
+}
+
+// ---------------------------------------------------------------- grouped issue
+static std::atomic<int> g_task_group{-1};
+
+int task_group_max() {
+  int v = g_task_group.load();
+  if (v < 0) {
+    const char* e = getenv("TR_GROUP");
+    v = e ? std::max(1, std::min(kMaxGroup, atoi(e))) : 4;
+    g_task_group.store(v);
+  }
+  return v;
+}
+
+void set_task_group_max(int n) { g_task_group.store(std::max(1, std::min(kMaxGroup, n))); }
+
+// A task qualifies for a grouped launch when it runs as ONE launch (coherence on,
+// capacity unbounded), writes a device output and would not be split along K.
+bool Session::groupable(int d, Job& job, int64_t gtid) {
+  if (dryrun_ || !coherence_ || devs_[d].capacity >= 0 || max_group_ < 2) return false;
+  int64_t tid = 0;
+  const Product& p = job.prod_of(gtid, &tid);
+  if (p.c.location != TR_LOC_DEVICE || p.k_steps > kMaxKSteps) return false;
+  const int64_t T = tile_;
+  const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+  const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
+  int total_kb = 0;
+  for (int64_t k = 0; k < p.k_steps; ++k) total_kb += static_cast<int>((std::min(T, p.K - k * T) + 63) / 64);
+  const int64_t ctas = ((mt + 127) / 128) * ((nt + 255) / 256);
+  return split_factor(ctas, total_kb, devs_[d].sms) < 2;  // launches that split along K run alone
+}
+
+// _execute_task for several tasks at once: each task's directory sequence is the
+// reference's (admit C, acquire A then B per k, release, release C); the
+// arithmetic of all of them is ONE launch on stream s.
+void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, int s) {
+  DeviceCtx& dc = devs_[d];
+  StreamCtx& sc = dc.streams[s];
+  const int64_t T = tile_;
+  GemmGroup grp;
+  grp.n_tasks = static_cast<int32_t>(gtids.size());
+  std::vector<TileKey> used;
+  std::vector<int32_t> used_phys;
+  const Product* p0 = nullptr;
+  for (size_t q = 0; q < gtids.size(); ++q) {
+    int64_t tid = 0;
+    const Product& p = job.prod_of(gtids[q], &tid);
+    p0 = &p;
+    const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+    const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
+    {
+      std::lock_guard<std::mutex> g(dir_->mu);
+      dir_->admit_output_locked(d, TileKey{p.c_uid, i, j});
+    }
+    GemmArgs& args = grp.task[q];
+    std::memset(&args, 0, sizeof(args));
+    args.m_valid = static_cast<int32_t>(mt);
+    args.n_valid = static_cast<int32_t>(nt);
+    args.n_ksteps = static_cast<int32_t>(p.k_steps);
+    args.planes = planes_;
+    args.c = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * p.c.esize();
+    args.ldc = p.c.ld;
+    args.c_f64 = p.c.dtype == TR_DTYPE_F64;
+    args.epilogue = EPI_STORE;
+    args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+    args.k_split = 1;
+    if (p.post != POST_NONE) {
+      args.post = p.post;
+      args.act = p.act;
+      args.bias = p.bias ? p.bias + j * T : nullptr;
+      args.aux = p.aux ? p.aux + (i * T) * p.ldaux + j * T : nullptr;
+      args.ldaux = p.ldaux;
+    }
+    for (int64_t k = 0; k < p.k_steps; ++k) {
+      const int64_t ar = p.ta ? k : i, ac = p.ta ? i : k;
+      const int64_t br = p.tb ? j : k, bc = p.tb ? k : j;
+      const int32_t pa = acquire(d, s, job, p.a, p.a_uid, p.ta, ar, ac, 0);
+      const int32_t pb = acquire(d, s, job, p.b, p.b_uid, p.tb, br, bc, 1);
+      args.a_z[k] = pa * planes_;
+      args.b_z[k] = pb * planes_;
+      args.k_len[k] = static_cast<int32_t>(std::min(T, p.K - k * T));
+      used.push_back(TileKey{p.a_uid, ar, ac});
+      used.push_back(TileKey{p.b_uid, br, bc});
+      used_phys.push_back(pa);
+      used_phys.push_back(pb);
+    }
+  }
+  BoxKind ba, bb;
+  gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
+  if (job.async) {
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, sc.stream));
+  } else {
+    TimedLaunch tl = timing_pair(d);
+    TR_CUDA(cudaEventRecord(tl.start, sc.stream));
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, sc.stream));
+    TR_CUDA(cudaEventRecord(tl.end, sc.stream));
+    dc.timed.push_back(tl);
+    if (tracing_) {
+      for (size_t q = 0; q < gtids.size(); ++q) {
+        int64_t tid = 0;
+        const Product& p = job.prod_of(gtids[q], &tid);
+        TraceRec rec;
+        rec.ev = tr_trace_event{d, TR_TRACE_GEMM, s, gtids[q], static_cast<uint64_t>(dc.timed.size() - 1),
+                                tid / p.grid_cols, tid % p.grid_cols, 0.0, 0.0};
+        rec.t = TimedLaunch{nullptr, nullptr};
+        dc.trace.push_back(rec);
+      }
+    }
+  }
+  job.launches.fetch_add(1);
+  {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    const EvRef ev = record(d, s);
+    for (int32_t ph : used_phys) note_use(dc.slots[ph], ev);
+    for (const TileKey& k : used) dir_->release_input_locked(d, k);
+    for (int64_t gt : gtids) {
+      int64_t tid = 0;
+      const Product& p = job.prod_of(gt, &tid);
+      const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+      const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
+      dir_->release_output_locked(d, TileKey{p.c_uid, i, j}, mt * nt * element_bytes_);  // coherence.py:263-280
+    }
+  }
+  if (job.async) {
+    for (int64_t gt : gtids) {
+      job.mark(gt);
+      dc.stats.tasks_completed += 1;
+    }
+    return;
+  }
+  TR_CUDA(cudaEventRecord(sc.done, sc.stream));
+  sc.task = gtids[0];
+  sc.group_rest.assign(gtids.begin() + 1, gtids.end());
 }
 
 // ---------------------------------------------------------------- task issue
@@ -721,6 +860,11 @@ void Session::reap(int d, Job& job, bool block_oldest) {
     TR_CUDA(e);
     job.mark(sc.task);
     dc.stats.tasks_completed += 1;
+    for (int64_t gt : sc.group_rest) {
+      job.mark(gt);
+      dc.stats.tasks_completed += 1;
+    }
+    sc.group_rest.clear();
     sc.task = -1;
   }
 }
@@ -775,6 +919,33 @@ void Session::run_job(int d, Job& job) {
     } else if (!dryrun_) {
       while (dc.streams[s].task >= 0) ++s;
       dc.streams[s].seq = ++seq;
+    }
+    if (victim < 0 && groupable(d, job, static_cast<int64_t>(tid))) {
+      // the station's other ready tasks of the same product join this launch
+      std::vector<int64_t> grp{static_cast<int64_t>(tid)};
+      int64_t t0 = 0;
+      const Product* p0 = &job.prod_of(grp[0], &t0);
+      const bool tall0 = std::min<int64_t>(tile_, p0->M - (t0 / p0->grid_cols) * tile_) > 128;
+      uint64_t more;
+      while (static_cast<int>(grp.size()) < std::min(max_group_, kMaxGroup) && st.peek_front(&more)) {
+        int64_t t1 = 0;
+        const Product* p1 = &job.prod_of(static_cast<int64_t>(more), &t1);
+        const bool tall1 = std::min<int64_t>(tile_, p1->M - (t1 / p1->grid_cols) * tile_) > 128;
+        if (p1 != p0 || tall1 != tall0 || !groupable(d, job, static_cast<int64_t>(more))) break;
+        if (!st.pop_for_run(&more)) break;
+        grp.push_back(static_cast<int64_t>(more));
+      }
+      if (grp.size() > 1) {
+        if (!job.async)  // one grouped launch in flight per device: pairs lose SM pairs to a concurrent kernel
+          while (true) {
+            int busy = 0;
+            for (int q = 0; q < dc.width; ++q) busy += dc.streams[q].task >= 0 && q != s;
+            if (!busy) break;
+            reap(d, job, true);
+          }
+        issue_group(d, job, grp, s);
+        continue;
+      }
     }
     issue(d, job, static_cast<int64_t>(tid), s);
   }
@@ -1042,7 +1213,13 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
   for (const Product& p : job.prods) per.push_back(product_order(p, order, room));
   std::vector<int64_t> ids;
   ids.reserve(static_cast<size_t>(total));
-  for (size_t r = 0;; ++r) {
+  if (max_group_ > 1 && !dryrun_) {
+    // grouped launches take consecutive tasks of ONE product: keep products contiguous
+    for (size_t q = 0; q < per.size(); ++q)
+      for (int64_t t : per[q]) ids.push_back(job.prods[q].base + t);
+  }
+  const bool interleave = ids.empty();  // products round-robin (per-task launches)
+  for (size_t r = 0; interleave; ++r) {
     bool any = false;
     for (size_t q = 0; q < per.size(); ++q)
       if (r < per[q].size()) {

@@ -98,6 +98,12 @@ struct Job {
   void set_error(int status, const std::string& msg);
 };
 
+// Tasks per grouped K1 launch for sessions created from now on (1 disables);
+// default 4, or TR_GROUP=<n> in the environment.
+int task_group_max();
+void set_task_group_max(int n);
+int split_factor(int64_t ctas, int total_kb, int64_t sms);
+
 class Session {
  public:
   Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t flags, int64_t hbm_budget);
@@ -144,6 +150,7 @@ class Session {
     std::deque<int32_t> fifo;
     cudaEvent_t done = nullptr;
     int64_t task = -1;      // in-flight task id, -1 idle
+    std::vector<int64_t> group_rest;  // further tasks of an in-flight grouped launch
     uint64_t seq = 0;       // issue order
     void* staging = nullptr;  // host-tile landing zone (T*T*8 bytes)
     void* outbuf = nullptr;   // C tile for host outputs (T*T*8 bytes)
@@ -195,6 +202,10 @@ class Session {
   void sim_task(int d, Job& job, int64_t gtid, double t);
   double xfer_cost(int src, int dst, int64_t nbytes) const;
   void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
+  // grouped launches: several ready tasks of one product in one K1 launch
+  bool groupable(int d, Job& job, int64_t gtid);
+  void issue_group(int d, Job& job, const std::vector<int64_t>& gtids, int s);
+  int max_group_ = -1;  // tasks per grouped launch (TR_GROUP env, default 4; 1 disables)
   int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
                   int scratch);
   void fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, int64_t c);

@@ -52,6 +52,13 @@ class Station {
     slots_.pop_back();
     return true;
   }
+  // The id the owner would pop next, without popping it.
+  bool peek_front(uint64_t* tid) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (slots_.empty()) return false;
+    *tid = slots_.front();
+    return true;
+  }
   int reserved_count() {
     std::lock_guard<std::mutex> g(mu_);
     return static_cast<int>(slots_.size());

@@ -54,7 +54,7 @@ struct Cfg {
 template <bool A_MN, bool B_K, int PLANES, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tile_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                     const __grid_constant__ GemmArgs args) {
+                     const __grid_constant__ GemmGroup grp) {
   using C = Cfg<PLANES, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int STAGE_BYTES = C::STAGE_BYTES;
@@ -73,8 +73,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;  // 0 = leader of the pair
   const bool leader = rank == 0;
-  const int m0 = (blockIdx.x / CG) * (BM * CG) + static_cast<int>(rank) * BM;
-  const int n0 = blockIdx.y * BN;                                   // output tile columns
+  // this CTA's task in the group and its block of that task's output
+  int t = 0;
+  while (t + 1 < grp.n_tasks && static_cast<int>(blockIdx.x) >= grp.cta_begin[t + 1]) ++t;
+  const GemmArgs& args = grp.task[t];
+  const int local = static_cast<int>(blockIdx.x) - grp.cta_begin[t];
+  const int m_cta = local % grp.m_blocks[t];
+  const int m0 = (m_cta / CG) * (BM * CG) + static_cast<int>(rank) * BM;
+  const int n0 = (local / grp.m_blocks[t]) * BN;                   // output tile columns
   const int nb0 = n0 + static_cast<int>(rank) * BN_LOCAL;           // B columns this CTA stages
 
   // k-blocks of this CTA (all of them, or its split-K share) and TMEM segments
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 template <bool A_MN, bool B_K, int PLANES, int CG>
-cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args,
+cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
                            cudaStream_t stream) {
   using C = Cfg<PLANES, CG>;
   auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG>;
@@ -323,10 +329,16 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
   if (attr_err != cudaSuccess) return attr_err;
-  const int m_blocks = (args.m_valid + BM * CG - 1) / (BM * CG);
-  dim3 grid(m_blocks * CG, (args.n_valid + BN - 1) / BN, args.k_split > 1 ? args.k_split : 1);
+  // flattened grid: task t owns CTAs [cta_begin[t], cta_begin[t+1]), M-blocks fastest
+  g.cta_begin[0] = 0;
+  for (int t = 0; t < g.n_tasks; ++t) {
+    const GemmArgs& a = g.task[t];
+    g.m_blocks[t] = ((a.m_valid + BM * CG - 1) / (BM * CG)) * CG;
+    g.cta_begin[t + 1] = g.cta_begin[t] + g.m_blocks[t] * ((a.n_valid + BN - 1) / BN);
+  }
+  dim3 grid(static_cast<unsigned>(g.cta_begin[g.n_tasks]), 1, k_split > 1 ? k_split : 1);
   if (CG == 1) {
-    kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, args);
+    kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, g);
     return cudaGetLastError();
   }
   cudaLaunchConfig_t cfg = {};
@@ -341,7 +353,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, const
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, args);
+  return cudaLaunchKernelEx(&cfg, kern, tmA, tmB, g);
 }
 
 // ---------------------------------------------------------------- K2 split/convert
@@ -428,37 +440,60 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box) {
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
 
-void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b) {
-  const bool pair = m_valid > BM && gemm_pairs_enabled();
+void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b, bool grouped) {
+  const bool pair = m_valid > BM && (grouped ? group_pairs_enabled() : gemm_pairs_enabled());
   *box_a = a_mn ? BOX_MN64 : BOX_K128;
   *box_b = b_kmajor ? (pair ? BOX_K128 : BOX_K256) : BOX_MN64;
 }
 
+static cudaError_t dispatch(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split, bool a_mn,
+                            bool b_kmajor, bool pair, int planes, cudaStream_t stream) {
+  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (planes == 2 ? 1 : 0) | (pair ? 8 : 0);
+  switch (variant) {
+    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, stream);
+    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, stream);
+    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, stream);
+    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, stream);
+    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, stream);
+    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, stream);
+    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, stream);
+    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, stream);
+    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, stream);
+    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, stream);
+    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, stream);
+    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, stream);
+    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, stream);
+    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, stream);
+    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, stream);
+    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, stream);
+  }
+}
+
+static bool args_ok(const GemmArgs& a) {
+  return a.m_valid > 0 && a.n_valid > 0 && a.n_ksteps > 0 && a.n_ksteps <= kMaxKSteps;
+}
+
 cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
                              bool b_kmajor, cudaStream_t stream) {
-  if (args.m_valid <= 0 || args.n_valid <= 0 || args.n_ksteps <= 0 || args.n_ksteps > kMaxKSteps)
-    return cudaErrorInvalidValue;
+  if (!args_ok(args)) return cudaErrorInvalidValue;
   // CTA pairs once a tile has more than one 128-row block; single CTAs otherwise.
   const bool pair = args.m_valid > BM && gemm_pairs_enabled();
-  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (args.planes == 2 ? 1 : 0) | (pair ? 8 : 0);
-  switch (variant) {
-    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, args, stream);
-    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, args, stream);
-    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, args, stream);
-    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, args, stream);
-    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, args, stream);
-    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, args, stream);
-    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, args, stream);
-    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, args, stream);
-    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, args, stream);
-    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, args, stream);
-    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, args, stream);
-    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, args, stream);
-    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, args, stream);
-    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, args, stream);
-    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, args, stream);
-    default: return launch_variant<true, true, 2, 2>(tmA, tmB, args, stream);
+  GemmGroup g;
+  g.n_tasks = 1;
+  g.task[0] = args;
+  return dispatch(tmA, tmB, g, args.k_split, a_mn, b_kmajor, pair, args.planes, stream);
+}
+
+cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
+                                   bool b_kmajor, cudaStream_t stream) {
+  if (g.n_tasks < 1 || g.n_tasks > kMaxGroup) return cudaErrorInvalidValue;
+  const bool pair = g.task[0].m_valid > BM && group_pairs_enabled();
+  for (int t = 0; t < g.n_tasks; ++t) {
+    const GemmArgs& a = g.task[t];
+    if (!args_ok(a) || a.k_split > 1 || a.planes != g.task[0].planes || (a.m_valid > BM && group_pairs_enabled()) != pair)
+      return cudaErrorInvalidValue;
   }
+  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, stream);
 }
 
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {
@@ -501,6 +536,22 @@ bool gemm_pairs_enabled() {
 }
 
 void set_gemm_pairs(bool on) { g_pairs.store(on ? 1 : 0); }
+
+static std::atomic<int> g_group_pairs{-1};
+
+bool group_pairs_enabled() {
+  int v = g_group_pairs.load();
+  if (v < 0) {
+    // Grouped launches run one at a time per device, where CTA pairs win
+    // (tools/probe_pairs.py: fp32acc +3%, bf16 +5% over single CTAs).
+    const char* e = getenv("TR_GROUP_PAIRS");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_group_pairs.store(v);
+  }
+  return v != 0;
+}
+
+void set_group_pairs(bool on) { g_group_pairs.store(on ? 1 : 0); }
 
 cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols,
                                  uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,

@@ -61,6 +61,20 @@ struct GemmArgs {
   int64_t ws_zstride;
 };
 
+// Several tasks in ONE launch (a station's worth of ready tasks): CTAs
+// [cta_begin[t], cta_begin[t+1]) of the flattened grid compute task t, M-blocks
+// fastest (m_blocks[t] CTAs along M, a multiple of the CTA-pair size).  One
+// launch instead of one per task removes the per-launch prologue/tail and the
+// wave-quantisation loss of a 512-CTA task grid (3.46 waves of 148 SMs), and
+// keeps CTA pairs from competing with a concurrent kernel for SM pairs.
+constexpr int kMaxGroup = 8;
+struct GemmGroup {
+  int32_t n_tasks;
+  int32_t cta_begin[kMaxGroup + 1];
+  int32_t m_blocks[kMaxGroup];
+  GemmArgs task[kMaxGroup];
+};
+
 // Accumulation-precision note (measured on B200, tools/probe_accum.py): the
 // tcgen05 fp32 accumulator rounds toward zero, so a long K accumulated in TMEM
 // drifts linearly in K (-1e-4 relative at K=32768).  The kernel therefore
@@ -89,7 +103,11 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box);
 // tmA/tmB must have been made with the boxes reported by gemm_boxes(a_mn, b_kmajor, m_valid).
 cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, const GemmArgs& args, bool a_mn,
                              bool b_kmajor, cudaStream_t stream);
-void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b);
+// All tasks of `g` must share the operand layouts (a_mn, b_kmajor), planes and
+// pair choice (m_valid > 128 for every task, or for none); no split-K.
+cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
+                                   bool b_kmajor, cudaStream_t stream);
+void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b, bool grouped = false);
 // Sums the k_split partials of a split-K launch in z order into C, then applies
 // args.epilogue (STORE / ACCUMULATE) and args.post, exactly like the kernel's own
 // epilogue would have (same argument block).
@@ -102,6 +120,10 @@ void set_splitk_max(int n);
 // Off by default; TR_GEMM_PAIRS=1 or set_gemm_pairs(true) selects it.
 bool gemm_pairs_enabled();
 void set_gemm_pairs(bool on);
+// Grouped launches (launch_tile_gemm_group) use CTA pairs by default
+// (TR_GROUP_PAIRS=0 or set_group_pairs(false) selects single CTAs).
+bool group_pairs_enabled();
+void set_group_pairs(bool on);
 
 // K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
 // into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything

@@ -27,6 +27,11 @@ def set_gemm_pairs(on: bool) -> None:
     N.call("tr_set_gemm_pairs", int(bool(on)))
 
 
+def set_task_group(max_tasks: int) -> None:
+    """Up to ``max_tasks`` (1..8) ready tasks per tile-GEMM launch for sessions created afterwards; 1 disables."""
+    N.call("tr_set_task_group", int(max_tasks))
+
+
 def set_splitk(max_splits: int) -> None:
     """At most ``max_splits`` (1..8) K-splits for tile GEMMs too small to fill the GPU; 1 disables."""
     N.call("tr_set_splitk", int(max_splits))

@@ -312,3 +312,60 @@ def test_split_k_normal_data_and_fused_posts(no_split):
         assert rel(o2.numpy(), ref2.numpy()) <= 1e-5
     assert rel(res[False][0].numpy(), res[True][0].numpy()) <= 1e-5  # split vs unsplit: summation order only
     assert res[False][2] > res[True][2]  # the split run launched reduction kernels
+
+
+@pytest.fixture
+def task_group():
+    from paper_1511_04348_b200.dense import set_task_group
+
+    yield set_task_group
+    set_task_group(4)
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True)])
+def test_grouped_launches_match_single(task_group, precision, ta, tb):
+    """Device-resident products run up to 4 station tasks per K1 launch; every
+    tile is computed by the same code, so grouped and per-task launches agree
+    bit for bit, with the reference's counters and one writeback per task."""
+    g = torch.Generator(device="cuda").manual_seed(21)
+    m, k, n = 1000, 700, 1100
+    a = torch.randn(k if ta else m, m if ta else k, device="cuda", generator=g)
+    b = torch.randn(n if tb else k, k if tb else n, device="cuda", generator=g)
+    outs = {}
+    for grp in (1, 4):
+        task_group(grp)
+        rt = Runtime(homogeneous_machine(2, dtype=np.float32, gpus=[0, 0]), 256, precision=precision)
+        c = torch.empty(m, n, device="cuda")
+        _, s = rt.multiply(a, b, transpose_a=ta, transpose_b=tb, a_uid="A", b_uid="B", out=c)
+        gm, gn, gk = -(-m // 256), -(-n // 256), -(-k // 256)
+        assert s.total_tasks == gm * gn and s.cache.writebacks == gm * gn
+        assert s.cache.l1_hits + s.cache.l2_hits + s.cache.host_fetches == 2 * gm * gn * gk
+        outs[grp] = (c.cpu(), s.gpu_launches)
+        rt.close()
+    assert torch.equal(outs[1][0], outs[4][0])
+    assert outs[4][1] < outs[1][1]  # fewer launches when grouped
+    ref = (a.double().T if ta else a.double()) @ (b.double().T if tb else b.double())
+    assert rel(outs[4][0].double().numpy(), ref.cpu().numpy()) <= TOL[precision]
+
+
+def test_grouped_launches_with_fused_posts_and_mlp(task_group):
+    """The MLP's fused epilogues in grouped launches: bitwise equal to per-task."""
+    rng = np.random.default_rng(4)
+    sizes = [300, 1100, 900, 7]
+    from paper_1511_04348_b200 import GpuMLP, Layer
+
+    base = [Layer.random(sizes[i], sizes[i + 1], rng, scale=1 / np.sqrt(sizes[i]), tag=f"layer{i}") for i in range(3)]
+    x, t = O.random_regression(rng, 600, 300, 7)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    res = {}
+    for grp in (1, 4):
+        task_group(grp)
+        layers = [Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base]
+        mlp = GpuMLP(layers, tile_size=256)
+        res[grp] = ([mlp.train_step(xd, td, 0.3) for _ in range(3)], mlp.to_host())
+        mlp.close()
+    assert res[1][0] == res[4][0]
+    for (w1, b1), (w4, b4) in zip(res[1][1], res[4][1]):
+        assert np.array_equal(w1, w4) and np.array_equal(b1, b4)
