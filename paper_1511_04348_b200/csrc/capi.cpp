@@ -420,8 +420,9 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
 
 int tr_session_set_order(tr_session* s, int32_t order) {
   return guarded([&] {
-    if (order < -1 || order > 3)
-      tr::fail(TR_ERR_VALUE, "order must be -1 (auto), 0 (row-major), 1 (banded), 2 (shells) or 3 (blocked)");
+    if (order < -1 || order > 4)
+      tr::fail(TR_ERR_VALUE,
+               "order must be -1 (auto), 0 (row-major), 1 (banded), 2 (shells), 3 (blocked) or 4 (k-panels)");
     s->s->set_order(order);
   });
 }

@@ -205,6 +205,9 @@ class Session {
   // grouped launches: several ready tasks of one product in one K1 launch
   bool groupable(int d, Job& job, int64_t gtid);
   void issue_group(int d, Job& job, const std::vector<int64_t>& gtids, int s);
+  // cold single-device products: k-panel schedule (see run_panels)
+  bool panels_apply(const Job& job) const;
+  bool run_panels(Job& job);  // false: no HBM for the C accumulators (nothing done)
   int max_group_ = -1;  // tasks per grouped launch (TR_GROUP env, default 4; 1 disables)
   int32_t acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, bool transposed, int64_t r, int64_t c,
                   int scratch);
@@ -242,7 +245,7 @@ class Session {
   bool dryrun_, steal_, coherence_;
   int32_t element_bytes_;
   int64_t hbm_budget_;
-  int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, 2 shells, -1 auto
+  int order_ = -1;  // task enqueue order: 0 row-major, 1 banded, 2 shells, 3 blocked, 4 k-panels, -1 auto
   cudaStream_t ext_stream_ = nullptr;  // products start after the work queued here
   bool ext_on_ = false;                // ext_stream_ set (nullptr = the legacy default stream)
   bool async_ = false;                 // device-resident products return once enqueued (see run_products)

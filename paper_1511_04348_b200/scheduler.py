@@ -432,8 +432,11 @@ class Runtime:
         N.call("tr_session_set_inflight", self._h, int(max_inflight))
 
     def set_order(self, order: str) -> None:
-        """Task enqueue order: "row-major" (reference), "banded", "shells", "blocked", or "auto"."""
-        code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2, "blocked": 3}[order]
+        """Task order: "row-major" (reference), "banded", "shells", "blocked", "k-panels"
+        (cold single-device products: the first half of the k-panels streamed
+        k-major), or "auto" (k-panels for cold in-core single-device
+        products, else shells / blocked / row-major)."""
+        code = {"auto": -1, "row-major": 0, "banded": 1, "shells": 2, "blocked": 3, "k-panels": 4}[order]
         N.call("tr_session_set_order", self._h, code)
 
     def set_stream(self, stream=None, ordered: bool = False) -> None:

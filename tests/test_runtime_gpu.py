@@ -369,3 +369,29 @@ def test_grouped_launches_with_fused_posts_and_mlp(task_group):
     assert res[1][0] == res[4][0]
     for (w1, b1), (w4, b4) in zip(res[1][1], res[4][1]):
         assert np.array_equal(w1, w4) and np.array_equal(b1, b4)
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+def test_kpanel_schedule_cold_product(precision):
+    """A cold single-device product (host A, B, C) runs the k-panel schedule:
+    the reference's counters exactly, integer inputs exact, float inputs within
+    tolerance, and the same numbers as the shells order up to rounding."""
+    rng = np.random.default_rng(31)
+    m, k, n, T = 1100, 1500, 900, 128  # 9 x 8 tasks, 12 k-steps
+    ai, bi = int_matrix(rng, m, k), int_matrix(rng, k, n)
+    af, bf = rng.standard_normal((m, k)), rng.standard_normal((k, n))
+    gm, gn, gk = -(-m // T), -(-n // T), -(-k // T)
+    res = {}
+    for order in ("auto", "shells"):
+        rt = Runtime(homogeneous_machine(1), T, precision=precision)
+        rt.set_order(order)
+        ci, s = rt.multiply(ai, bi, a_uid="Ai", b_uid="Bi")
+        assert np.array_equal(ci, O.reference_gemm(ai, bi))
+        assert s.cache.host_fetches == gm * gk + gk * gn and s.cache.writebacks == gm * gn
+        assert s.cache.l1_hits == 2 * gm * gn * gk - (gm * gk + gk * gn)
+        assert s.tasks_by_device == {0: gm * gn}
+        cf, _ = rt.multiply(af, bf, a_uid="Af", b_uid="Bf")
+        assert rel(cf, af @ bf) <= TOL[precision]
+        res[order] = cf
+        rt.close()
+    assert rel(res["auto"], res["shells"]) <= 1e-6 if precision == "fp32acc" else 1e-3
