@@ -139,19 +139,10 @@ std::vector<TileKey> Directory::admit_locked(int device, const TileKey& key, boo
   int32_t slot = -1;
   if (input && slot_total_[device] > 0) {
     if (d.free_slots.empty()) {
-      // Physical pool smaller than the logical capacity (HBM budget): evict LRU unpinned.
+      // Physical pool smaller than the logical capacity (HBM budget): evict a
+      // dead tile if the job's future is known, else the LRU unpinned one.
       TileKey victim{};
-      bool found = false;
-      for (const TileKey& k : d.order) {
-        auto e = d.entries.find(k);
-        if (e->second.slot < 0) continue;
-        auto p = d.pins.find(k);
-        if (p == d.pins.end() || p->second == 0) {
-          victim = k;
-          found = true;
-          break;
-        }
-      }
+      const bool found = physical_victim_locked(device, &victim, false);
       if (!found) fail(TR_ERR_CAPACITY, "device %d: HBM slab exhausted and all resident tiles pinned", device);
       drop_locked(device, victim);
       evicted.push_back(victim);
@@ -195,6 +186,10 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
     ds.bytes_host += nbytes;
     r.nbytes = nbytes;
     return r;
+  }
+  if (future_on_) {
+    auto f = future_.find(key);
+    if (f != future_.end()) f->second -= 1;
   }
   // Classification (coherence.py:124-134) over COUNTED owners: a tile some device
   // holds only as an unclaimed fetch-ahead is, for the counters, not resident yet
@@ -266,12 +261,53 @@ Acquired Directory::acquire_input_locked(int requester, const TileKey& key, int6
   return r;
 }
 
+bool Directory::physical_victim_locked(int device, TileKey* victim, bool dead_only) const {
+  const Dev& d = dev_[device];
+  const TileKey* lru = nullptr;
+  for (const TileKey& k : d.order) {
+    auto e = d.entries.find(k);
+    if (e->second.slot < 0) continue;
+    auto p = d.pins.find(k);
+    if (p != d.pins.end() && p->second > 0) continue;
+    if (!future_on_ || dead_locked(k)) {
+      *victim = k;
+      return true;
+    }
+    if (!lru && !e->second.pending) lru = &k;  // live: only if nothing is dead
+  }
+  if (dead_only || !lru) return false;
+  *victim = *lru;
+  return true;
+}
+
+bool Directory::dead_locked(const TileKey& key) const {
+  auto it = future_.find(key);
+  return it != future_.end() && it->second <= 0;
+}
+
+void Directory::set_future_locked(std::unordered_map<TileKey, int64_t, TileKeyHash> future) {
+  future_ = std::move(future);
+  future_on_ = true;
+}
+
+void Directory::clear_future_locked() {
+  future_.clear();
+  future_on_ = false;
+}
+
 bool Directory::prefetch_locked(int device, const TileKey& key, int32_t* slot, int32_t* phys_source, bool host_only) {
   if (!enabled_ || host_worker_[device]) return false;
   Dev& d = dev_[device];
   if (d.entries.count(key)) return false;
   if (capacity_[device] >= 0 && static_cast<int64_t>(d.order.size()) >= capacity_[device]) return false;
-  if (slot_total_[device] > 0 && d.free_slots.empty()) return false;
+  if (slot_total_[device] > 0 && d.free_slots.empty()) {
+    // out-of-core: a dead tile's slot may take the prefetch (never a live one)
+    TileKey victim{};
+    if (!future_on_ || !physical_victim_locked(device, &victim, true)) return false;
+    drop_locked(device, victim);
+    stats_.evictions += 1;
+    d.stats.evictions += 1;
+  }
   auto it = residency_.find(key);
   const uint64_t owners = it == residency_.end() ? 0 : it->second;
   if (host_only && owners) return false;

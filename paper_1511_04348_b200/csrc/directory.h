@@ -98,6 +98,13 @@ class Directory {
   // counters change.  Returns the number of tiles dropped.
   int64_t forget_locked(uint64_t uid);
   void check_invariants_locked();
+  // Out-of-core support (HBM slab smaller than the working set, logical capacity
+  // unbounded): the remaining requests of every input tile in the current job.
+  // While set, a physically full device evicts a DEAD tile (no remaining
+  // request) before any live one, and fetch-ahead may replace dead tiles.
+  // Logical (capacity_tiles) evictions keep the reference's LRU/FIFO order.
+  void set_future_locked(std::unordered_map<TileKey, int64_t, TileKeyHash> future);
+  void clear_future_locked();
   int32_t slot_of_locked(int device, const TileKey& key) const;
   // Owners of `key` (bitmask over device ids).
   uint64_t owners_locked(const TileKey& key) const;
@@ -121,6 +128,8 @@ class Directory {
   };
 
   int closest_owner(int requester, uint64_t owners) const;
+  bool dead_locked(const TileKey& key) const;  // no remaining request in the current job
+  bool physical_victim_locked(int device, TileKey* victim, bool dead_only) const;
   void unpin_locked(int device, const TileKey& key);
   void drop_locked(int device, const TileKey& key);  // remove residency (no counters)
 
@@ -134,6 +143,8 @@ class Directory {
   std::vector<Dev> dev_;
   std::vector<int64_t> slot_total_;
   std::unordered_map<TileKey, uint64_t, TileKeyHash> residency_;
+  std::unordered_map<TileKey, int64_t, TileKeyHash> future_;
+  bool future_on_ = false;
   tr_cache_stats stats_{};
 };
 

@@ -517,8 +517,10 @@ bool Session::prefetch_task(int d, Job& job, int64_t gtid, bool host_only, int64
 void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vector<uint8_t>& seen_global,
                           int64_t& pending) {
   DeviceCtx& dc = devs_[d];
-  constexpr int64_t kBudget = 32;   // unclaimed prefetched tiles per device
-  constexpr int64_t kLookahead = 16;
+  // unclaimed prefetched tiles per device / tasks looked ahead past the queue
+  // head; out-of-core jobs look further (the next task block's panels)
+  const int64_t kBudget = job.out_of_core ? 96 : 32;
+  const int64_t kLookahead = job.out_of_core ? 48 : 16;
   for (uint64_t tid : dc.station->peek()) {
     if (seen[tid]) continue;
     if (!prefetch_task(d, job, static_cast<int64_t>(tid), false, pending, kBudget)) return;
@@ -626,22 +628,21 @@ bool Session::run_panels(Job& job) {
   }
   // ---- 0. per-task C accumulators in HBM; without room, the caller runs the
   //         ordinary task path instead (nothing has been touched yet)
-  std::vector<void*> cbuf(nt_tasks, nullptr);
-  std::vector<size_t> ccap(nt_tasks, 0);
   struct CbufGuard {
     int gpu;
-    std::vector<void*>& b;
-    std::vector<size_t>& c;
+    void* p = nullptr;
+    size_t cap = 0;
     ~CbufGuard() {
-      for (size_t q = 0; q < b.size(); ++q)
-        if (b[q]) DevPool::get().release(gpu, b[q], c[q]);
+      if (p) DevPool::get().release(gpu, p, cap);
     }
-  } guard{dc.gpu, cbuf, ccap};
-  for (size_t q = 0; q < nt_tasks; ++q)
-    if (DevPool::get().alloc(dc.gpu, static_cast<size_t>(T * T * ces), &cbuf[q], &ccap[q]) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
-    }
+  } guard{dc.gpu};
+  const size_t ctile = static_cast<size_t>(T * T * ces);
+  if (DevPool::get().alloc(dc.gpu, ctile * nt_tasks, &guard.p, &guard.cap) != cudaSuccess) {  // one block
+    cudaGetLastError();
+    return false;
+  }
+  std::vector<void*> cbuf(nt_tasks);
+  for (size_t q = 0; q < nt_tasks; ++q) cbuf[q] = static_cast<char*>(guard.p) + q * ctile;
   // ---- 1. the unit list: (task, k0, k1, group) in issue order.  Default: the
   //         first P k-panels k-major in groups of G tasks, then one finishing
   //         unit per task (k = P..ks-1) in shells order.
@@ -1462,6 +1463,35 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     for (const Product& p : job.prods)
       in_tiles += ceil_div(p.a.rows, T) * ceil_div(p.a.cols, T) + ceil_div(p.b.rows, T) * ceil_div(p.b.cols, T);
     for (int d = 0; d < n_devices(); ++d) ensure_slab(d, dir_->used_tiles(d) + in_tiles);
+  }
+  // out-of-core (the inputs exceed the HBM slab, capacity unbounded): the
+  // directory learns every input tile's remaining requests so that physical
+  // evictions and fetch-ahead replace dead tiles first
+  bool unbounded = true;
+  for (auto& dc : devs_) unbounded = unbounded && dc.capacity < 0;
+  job.out_of_core = !dryrun_ && coherence_ && unbounded && in_tiles_all > room;
+  struct FutureGuard {
+    Directory* dir;
+    bool on;
+    ~FutureGuard() {
+      if (!on) return;
+      std::lock_guard<std::mutex> g(dir->mu);
+      dir->clear_future_locked();
+    }
+  } future_guard{dir_.get(), job.out_of_core};
+  if (job.out_of_core) {
+    std::unordered_map<TileKey, int64_t, TileKeyHash> future;
+    for (int64_t gt : job.order) {
+      int64_t tid = 0;
+      const Product& p = job.prod_of(gt, &tid);
+      const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+      for (int64_t k = 0; k < p.k_steps; ++k) {
+        future[TileKey{p.a_uid, p.ta ? k : i, p.ta ? i : k}] += 1;
+        future[TileKey{p.b_uid, p.tb ? j : k, p.tb ? k : j}] += 1;
+      }
+    }
+    std::lock_guard<std::mutex> g(dir_->mu);
+    dir_->set_future_locked(std::move(future));
   }
   const tr_cache_stats before = dir_->stats();
   const std::vector<tr_cache_stats> before_dev = dir_->stats_per_device();

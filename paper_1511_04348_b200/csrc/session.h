@@ -78,6 +78,7 @@ struct Job {
   std::vector<int64_t> order;          // planned global task ids in enqueue order
   std::atomic<int64_t> claimed{0};     // tasks pulled from the queue so far (all devices)
   bool async = false;                  // stream-ordered: tasks complete in stream order, no host wait
+  bool out_of_core = false;            // inputs exceed the HBM slab (future-aware eviction on)
 
   explicit Job(int64_t total_ids) : total(total_ids), done(static_cast<size_t>(total_ids)) {
     for (auto& d : done) d.store(0);
