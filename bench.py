@@ -63,6 +63,10 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU-baseline sample duration")
     p.add_argument("--no-mlp", action="store_true")
+    p.add_argument("--no-ooc", action="store_true", help="skip the out-of-core leg (cfg4 scaled)")
+    p.add_argument("--ooc-n", type=int, default=65536)
+    p.add_argument("--ooc-cache-gib", type=float, default=24.0)
+    p.add_argument("--ooc-steps", type=int, default=2)
     p.add_argument("--mlp-steps", type=int, default=5)
     p.add_argument("--mlp-sizes", default="784,8192,8192,8192,10")
     p.add_argument("--mlp-batch", type=int, default=8192)
@@ -234,6 +238,62 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],
             "h2d_bytes_per_step": int(x.size * 4 + t.size * 4), "d2h_bytes_per_step": 8}
+
+
+def bench_ooc(args, tr, torch, peaks_tf):
+    """cfg4 scaled to this box (196 GB of host RAM cannot hold N=131072's 206 GB):
+    N = 65536 fp32-accurate from pinned host with the tile cache capped so the
+    operands' converted planes (32 GiB) do not fit it -- the out-of-core path:
+    blocked task order, evictions, re-fetches, fetch-ahead into dead slots.
+    Each step is a cold one-shot session (host -> HBM -> host inside the timing)."""
+    n, T = args.ooc_n, args.tile
+    a = tr.matrix.pinned_empty((n, n), np.float32)
+    b = tr.matrix.pinned_empty((n, n), np.float32)
+    c = tr.matrix.pinned_empty((n, n), np.float32)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    rows = 4096
+    for m in (a, b):
+        for r in range(0, n, rows):
+            m[r:r + rows] = torch.randn((rows, n), device="cuda", generator=g).cpu().numpy()
+    machine = tr.homogeneous_machine(1, dtype=np.float32)
+    budget = int(args.ooc_cache_gib * 2**30)
+
+    def step():
+        with tr.Runtime(machine, T, precision=args.precision, hbm_budget_bytes=budget) as rt:
+            return rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C", out=c)[1]
+
+    step()  # warm-up: pools
+    times, stats = [], None
+    for _ in range(max(1, args.ooc_steps)):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        stats = step()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    t = float(np.mean(times))
+    flops = 2.0 * n ** 3
+    cs = stats.cache
+    h2d_bw = 55.6e9  # measured pinned H2D on this box (tools/probe_pcie2.py)
+    mode_peak = peaks_tf * 1e12 / (3 if args.precision == "fp32acc" else 1)
+    t_roof = max(flops / mode_peak, cs.bytes_host / h2d_bw, cs.bytes_writeback / 56e9)
+    from oracle import tilerun_oracle as O
+
+    ri = np.array([0, T - 1, T, n // 2 + 7, n - 1])
+    ci = np.array([1, T + 1, n // 3, n - 2, n - 1])
+    ref = O.c_oracle().gemm(a[ri].astype(np.float64), b[:, ci].astype(np.float64))
+    parity = float(np.linalg.norm(c[ri][:, ci].astype(np.float64) - ref) / np.linalg.norm(ref))
+    out = {"workload": f"cfg4 scaled: out-of-core GEMM N={n} fp32 from pinned host, tile cache capped at "
+                       f"{args.ooc_cache_gib:g} GiB (A and B planes {2 * n * n * 4 / 2**30:.0f} GiB)",
+           "value": flops / t / 1e12, "unit": UNIT, "ms_per_step": t * 1e3, "steps": len(times),
+           "host_fetches": cs.host_fetches, "bytes_host": cs.bytes_host, "evictions": cs.evictions,
+           "writebacks": cs.writebacks, "bytes_writeback": cs.bytes_writeback,
+           "roofline": {"time_ms": t_roof * 1e3, "frac": t_roof / t,
+                        "def": "max(2N^3 / (bf16 burst peak / 3), bytes_host / 55.6 GB/s, bytes_writeback / 56 GB/s)"},
+           "parity_rel_fro_sampled": parity}
+    del a, b, c
+    return out
 
 
 def sim_prediction_ms(tr, n, T, world, precision):
@@ -434,6 +494,12 @@ def main():
                                                     "loss_last")}
             torch.cuda.empty_cache()
 
+    # ---- out-of-core leg (cfg4 scaled), rank 0 at N=1 only
+    ooc = None
+    if not args.no_ooc and world == 1:
+        ooc = bench_ooc(args, tr, torch, peak)
+        torch.cuda.empty_cache()
+
     # ---- e2e: reference-facing one-shot run() with pinned host numpy arrays
     e2e = None
     if not args.no_e2e:
@@ -508,6 +574,7 @@ def main():
                        "parallelism": f"task-sharded x{world}", "warm_cache": "all input tiles L1-resident"},
             "e2e": e2e,
             "mlp": mlp,
+            "ooc": ooc,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
