@@ -1338,12 +1338,20 @@ static std::vector<int64_t> product_order(const Product& p, int order, int64_t r
   } else if (order == 3) {
     // blocked: b x b task blocks whose (b + b) k-panels fit the tile budget, so
     // each A/B tile is fetched once per block instead of once per task row
+    // (each block walked in shells from its corner, so compute starts after two
+    // k-panels of the block instead of its whole first task row)
     const int64_t ks = std::max<int64_t>(1, p.k_steps);
     const int64_t bsz = std::max<int64_t>(1, (room == INT64_MAX ? total : (room - 8)) / (2 * ks));
     for (int64_t bi = 0; bi < p.grid_rows; bi += bsz)
-      for (int64_t bj = 0; bj < p.grid_cols; bj += bsz)
-        for (int64_t i = bi; i < std::min(bi + bsz, p.grid_rows); ++i)
-          for (int64_t j = bj; j < std::min(bj + bsz, p.grid_cols); ++j) ids.push_back(i * p.grid_cols + j);
+      for (int64_t bj = 0; bj < p.grid_cols; bj += bsz) {
+        const int64_t br = std::min(bsz, p.grid_rows - bi), bc = std::min(bsz, p.grid_cols - bj);
+        for (int64_t sh = 0; sh < std::max(br, bc); ++sh) {
+          for (int64_t i = 0; i < std::min(sh, br); ++i)
+            if (sh < bc) ids.push_back((bi + i) * p.grid_cols + bj + sh);
+          if (sh < br)
+            for (int64_t j = 0; j <= std::min(sh, bc - 1); ++j) ids.push_back((bi + sh) * p.grid_cols + bj + j);
+        }
+      }
   } else {
     for (int64_t t = 0; t < total; ++t) ids.push_back(t);
   }
