@@ -260,7 +260,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
     const int grow = m0 + row;
     const int gcol0 = n0 + half * 128;
-    if (grow < args.m_valid && gcol0 < args.n_valid) {
+    const bool part = n_split > 1;  // split-K: raw fp32 partials into the workspace
+    float* obase = part ? args.ws + blockIdx.z * args.ws_zstride : static_cast<float*>(args.c);
+    const int64_t ldo = part ? args.ws_ld : args.ldc;
+    if ((part || !args.c_f64) && gcol0 + 128 <= args.n_valid && (ldo & 3) == 0 &&
+        (reinterpret_cast<uintptr_t>(obase) & 15) == 0) {
+      // Coalesced epilogue: this warp's 32 x 128 block goes through the (now idle)
+      // operand ring -- rows padded to 132 floats keep both the row-per-thread
+      // writes and the row-per-warp reads bank-conflict-free -- so every global
+      // access is 512 contiguous bytes instead of 32 scattered 16-byte pieces.
+      float* stage = reinterpret_cast<float*>(smem) + (warp - EPI_WARP0) * (32 * 132);
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        *reinterpret_cast<float4*>(stage + lane * 132 + 4 * j) =
+            make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+      __syncwarp();
+      const bool acc_mode = !part && args.epilogue == EPI_ACCUMULATE;
+      const int post = part ? static_cast<int>(POST_NONE) : args.post;
+      const int c = 4 * lane;
+      float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (post == POST_BIAS_ACT && args.bias)
+        for (int x = 0; x < 4; ++x) bias4[x] = args.bias[gcol0 + c + x];
+      const int row0 = m0 + q * 32;
+      for (int r = 0; r < 32 && row0 + r < args.m_valid; ++r) {
+        float4 v = *reinterpret_cast<const float4*>(stage + r * 132 + c);
+        float4* d4 = reinterpret_cast<float4*>(obase + static_cast<int64_t>(row0 + r) * ldo + gcol0 + c);
+        if (acc_mode) {
+          const float4 o = *d4;
+          v.x += o.x;
+          v.y += o.y;
+          v.z += o.z;
+          v.w += o.w;
+        }
+        if (post == POST_BIAS_ACT) {
+          v.x = act_fwd(args.act, v.x + bias4[0]);
+          v.y = act_fwd(args.act, v.y + bias4[1]);
+          v.z = act_fwd(args.act, v.z + bias4[2]);
+          v.w = act_fwd(args.act, v.w + bias4[3]);
+        } else if (post == POST_ACT_GRAD) {
+          const float* ax = args.aux + static_cast<int64_t>(row0 + r) * args.ldaux + gcol0 + c;
+          v.x *= act_grad_from_out(args.act, ax[0]);
+          v.y *= act_grad_from_out(args.act, ax[1]);
+          v.z *= act_grad_from_out(args.act, ax[2]);
+          v.w *= act_grad_from_out(args.act, ax[3]);
+        }
+        *d4 = v;
+      }
+    } else if (grow < args.m_valid && gcol0 < args.n_valid) {
       const int ncols = min(128, args.n_valid - gcol0);
       const bool partial = n_split > 1;  // split-K: raw fp32 partial into the workspace
       const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
