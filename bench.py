@@ -196,19 +196,29 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
     Per step (all inside the timed region): the batch x / target is copied H2D
     from pinned host memory, forward + MSE + backward + SGD run (12 products via
     Runtime.multiply, K3-K7 elementwise kernels), and the loss is read back D2H.
+    Under torchrun the global batch is split over the ranks (data parallel: each
+    layer's gradients are all-reduced over NCCL, overlapping the backward pass),
+    and samples/s counts the GLOBAL batch (strong scaling).
     """
+    import torch.distributed as dist
+
     sizes = [int(v) for v in args.mlp_sizes.split(",")]
     batch = args.mlp_batch
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
     rng = np.random.default_rng(0)
     # SURVEY.md §7: per-layer scale 1/sqrt(fan_in) (a single from_sizes scale saturates the sigmoids)
     layers = [tr.Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
                               tag=f"layer{i}") for i in range(len(sizes) - 1)]
     x, t = tr.ann.random_regression(rng, batch, sizes[0], sizes[-1])
+    shard = slice(rank * batch // world, (rank + 1) * batch // world)
+    x, t = x[shard], t[shard]
     xh = tr.matrix.pinned_empty(x.shape, np.float32)
     th = tr.matrix.pinned_empty(t.shape, np.float32)
     xh[...] = x
     th[...] = t
-    mlp = tr.GpuMLP(layers, tile_size=args.tile, device=local, precision=precision)
+    mlp = tr.GpuMLP(layers, tile_size=args.tile, device=local, precision=precision,
+                    process_group=dist.group.WORLD if world > 1 else None)
     dev = torch.device("cuda", local)
     xd = torch.empty(x.shape, dtype=torch.float32, device=dev)
     td = torch.empty(t.shape, dtype=torch.float32, device=dev)
@@ -233,7 +243,9 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
     flops = mlp_flops(sizes, batch)
     return {"workload": f"cfg3 MLP {'-'.join(map(str, sizes))} batch {batch}, sigmoid, MSE, SGD lr 0.1 "
                         "(device-resident GpuMLP; 12 products per step through the tiled runtime, "
-                        "fused bias/activation and activation-gradient epilogues)", "precision": precision,
+                        "fused bias/activation and activation-gradient epilogues"
+                        + (f"; data parallel over {world} GPUs, NCCL gradient all-reduce" if world > 1 else "") + ")",
+            "precision": precision,
             "samples_per_s": batch / dt, "ms_per_step": dt * 1e3, "tflops": flops / dt / 1e12,
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],

@@ -302,6 +302,11 @@ int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a
  * fixed order (bitwise reproducible)                          ann.py:51-56 */
 int tr_mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
                     void* stream);
+/* Data-parallel form: this rank holds n of the batch's n_global elements;
+ * dout = 2 (pred - target) / n_global, so summing dout-derived gradients over
+ * the ranks gives the full-batch gradient; *loss_sum = this shard's sum. */
+int tr_mlp_mse_grad_global(float* dout, const float* pred, const float* target, int64_t n, int64_t n_global,
+                           double* loss_sum, void* stream);
 /* out[c] = sum_r m[r, c], fixed summation order (reproducible)   ann.py:173 */
 int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream);
 /* w -= lr * g                                                ann.py:243-247 */

@@ -146,6 +146,7 @@ _PROTOS = {
     "tr_mlp_bias_act": [vp, vp, vp, i64, i64, i32, vp],
     "tr_mlp_act_grad": [vp, vp, vp, vp, i64, i32, vp],
     "tr_mlp_mse_grad": [vp, vp, vp, i64, vp, vp],
+    "tr_mlp_mse_grad_global": [vp, vp, vp, i64, i64, vp, vp],
     "tr_mlp_colsum": [vp, i64, i64, vp, vp],
     "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
     "tr_session_set_external_stream": [vp, vp, i32],

@@ -439,7 +439,14 @@ int tr_mlp_act_grad(float* dy, const float* dout, const float* y, const float* a
 int tr_mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
                     void* stream) {
   return guarded(
-      [&] { TR_CUDA(tr::mlp_mse_grad(dout, pred, target, n, loss_sum, static_cast<cudaStream_t>(stream))); });
+      [&] { TR_CUDA(tr::mlp_mse_grad(dout, pred, target, n, n, loss_sum, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_mse_grad_global(float* dout, const float* pred, const float* target, int64_t n, int64_t n_global,
+                           double* loss_sum, void* stream) {
+  return guarded([&] {
+    if (n_global < n) tr::fail(TR_ERR_VALUE, "n_global (%lld) < n (%lld)", (long long)n_global, (long long)n);
+    TR_CUDA(tr::mlp_mse_grad(dout, pred, target, n, n_global, loss_sum, static_cast<cudaStream_t>(stream)));
+  });
 }
 int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream) {
   return guarded([&] { TR_CUDA(tr::mlp_colsum(m, rows, cols, out, static_cast<cudaStream_t>(stream))); });

@@ -53,10 +53,11 @@ __global__ void act_grad_kernel(float* __restrict__ dy, const float* __restrict_
 
 // dout = 2 (pred - t) / n; loss partial sums of (pred - t)^2 in double, one atomic per block.
 __global__ void mse_grad_kernel(float* __restrict__ dout, const float* __restrict__ pred,
-                                const float* __restrict__ target, int64_t n, double* __restrict__ block_sums) {
+                                const float* __restrict__ target, int64_t n, int64_t n_mean,
+                                double* __restrict__ block_sums) {
   __shared__ double part[kThreads / 32];
   double acc = 0.0;
-  const float scale = 2.0f / static_cast<float>(n);
+  const float scale = 2.0f / static_cast<float>(n_mean);  // n_mean: elements of the (global) batch
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const float d = pred[i] - target[i];
@@ -163,13 +164,13 @@ static cudaError_t stream_scratch(cudaStream_t s, size_t bytes, void** out) {
   return cudaSuccess;
 }
 
-cudaError_t mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, double* loss_sum,
-                         cudaStream_t s) {
+cudaError_t mlp_mse_grad(float* dout, const float* pred, const float* target, int64_t n, int64_t n_mean,
+                         double* loss_sum, cudaStream_t s) {
   const int blocks = grid_for(n);
   double* parts = nullptr;
   cudaError_t e = stream_scratch(s, sizeof(double) * blocks, reinterpret_cast<void**>(&parts));
   if (e != cudaSuccess) return e;
-  mse_grad_kernel<<<blocks, kThreads, 0, s>>>(dout, pred, target, n, parts);
+  mse_grad_kernel<<<blocks, kThreads, 0, s>>>(dout, pred, target, n, n_mean, parts);
   sum_partials_kernel<<<1, kThreads, 0, s>>>(parts, blocks, loss_sum);
   return cudaGetLastError();
 }

@@ -18,6 +18,13 @@ per step, weight uids are versioned exactly like ``Layer.weight_uid``), so the
 backward products hit the tiles the forward products cached.  Activations and
 parameters are float32 on the device; the products run in the FP32-accurate
 mode; the loss is accumulated in float64.
+
+Data parallel over a ``torch.distributed`` process group (one process per GPU,
+NCCL): each rank trains on its shard of the global batch, the MSE gradient is
+scaled by the GLOBAL element count, and each layer's (dW, db) is all-reduced
+(sum) as soon as its backward round is enqueued -- on NCCL's stream, so the
+exchange overlaps the remaining backward products -- before the SGD update.
+The sum of the shards' gradients is the full-batch gradient of the reference.
 """
 
 from __future__ import annotations
@@ -54,7 +61,8 @@ class GpuMLP:
     """A float32 MLP living in HBM, trained through a tiled ``Runtime`` session."""
 
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
-                 device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True):
+                 device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
+                 process_group=None):
         import torch
 
         self.torch = torch
@@ -69,6 +77,14 @@ class GpuMLP:
             runtime = Runtime(machine, tile_size, precision=precision)
         self.rt = runtime
         self.stream_ordered = stream_ordered
+        self.pg = process_group
+        if process_group is not None:
+            import torch.distributed as dist
+
+            self.world = dist.get_world_size(process_group)
+        else:
+            self.world = 1
+        self._pending = []  # in-flight gradient all-reduces of the current step
         self._loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self._bufs: dict = {}
         self.products = 0
@@ -99,6 +115,17 @@ class GpuMLP:
         self.products += len(prods)
 
     # -- one pass ------------------------------------------------------------
+    def _allreduce(self, *tensors):
+        """Sum over the data-parallel group, asynchronously (NCCL's stream waits
+        for the current stream, so the products that made the tensors are done)."""
+        if self.pg is None or self.world == 1:
+            return
+        import torch.distributed as dist
+
+        for t in tensors:
+            if t is not None:
+                self._pending.append(dist.all_reduce(t, group=self.pg, async_op=True))
+
     def loss_gradients(self, x, target):
         """Forward + backward without update; returns (n, [(dW, db)]) with the loss
         sum left in ``self._loss`` (device).
@@ -122,7 +149,8 @@ class GpuMLP:
         self._step_uids = list(uids)
         pred = cur
         d_out = self._buf("dout", pred.shape)
-        N.call("tr_mlp_mse_grad", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(), _ptr(self._loss), s)
+        N.call("tr_mlp_mse_grad_global", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(),
+               pred.numel() * self.world, _ptr(self._loss), s)
         last = len(self.layers) - 1
         d_y = self._buf(f"dy{last}", pred.shape)
         N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), None, _ptr(pred), d_y.numel(),
@@ -142,6 +170,7 @@ class GpuMLP:
             if L.b is not None:
                 d_b = self._buf(f"db{li}", L.b.shape)
                 N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
+            self._allreduce(d_w, d_b)  # overlaps the next (lower) layer's backward round
             grads[li] = (d_w, d_b)
             d_y = d_x
         return pred.numel(), grads
@@ -149,6 +178,14 @@ class GpuMLP:
     def train_step(self, x, target, lr: float) -> float:
         """One SGD step (ann.py:239-248); returns the MSE loss (read back to the host)."""
         n, grads = self.loss_gradients(x, target)
+        for h in self._pending:  # the current stream waits for every gradient all-reduce
+            h.wait()
+        self._pending = []
+        self._allreduce(self._loss)
+        for h in self._pending:
+            h.wait()
+        self._pending = []
+        n *= self.world
         s = self._stream()
         for L, (d_w, d_b) in zip(self.layers, grads):
             N.call("tr_mlp_sgd", _ptr(L.w), _ptr(d_w), L.w.numel(), float(lr), s)

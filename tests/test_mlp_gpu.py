@@ -83,3 +83,50 @@ def test_stream_ordered_matches_blocking():
     assert runs[True][0] == runs[False][0]
     for (w1, b1), (w0, b0) in zip(runs[True][1], runs[False][1]):
         assert np.array_equal(w1, w0) and np.array_equal(b1, b0)
+
+
+def test_data_parallel_shards_sum_to_full_batch():
+    """The data-parallel gradient: two half-batch shards with the MSE scaled by
+    the global element count sum to the full-batch gradient (what the NCCL
+    all-reduce forms across ranks), and a 1-rank NCCL group trains exactly like
+    the plain model."""
+    rng = np.random.default_rng(8)
+    sizes = [200, 600, 300, 5]
+    base = [Layer.random(sizes[i], sizes[i + 1], rng, scale=1 / np.sqrt(sizes[i]), tag=f"layer{i}") for i in range(3)]
+    x, t = O.random_regression(rng, 512, 200, 5)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+
+    def grads(mlp, xs, ts, world):
+        mlp.world = world  # the global count the MSE gradient is scaled by
+        n, g = mlp.loss_gradients(xs, ts)
+        return [(w.double().cpu(), b.double().cpu()) for w, b in g], float(mlp._loss.item())
+
+    full = GpuMLP([Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base], tile_size=128)
+    g_full, loss_full = grads(full, xd, td, 1)
+    half = GpuMLP([Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base], tile_size=128)
+    g0, l0 = grads(half, xd[:256], td[:256], 2)
+    g1, l1 = grads(half, xd[256:], td[256:], 2)
+    for (wf, bf), (w0, b0), (w1, b1) in zip(g_full, g0, g1):
+        assert relerr((w0 + w1).numpy(), wf.numpy()) <= 1e-5 and relerr((b0 + b1).numpy(), bf.numpy()) <= 1e-5
+    assert abs((l0 + l1) - loss_full) <= 1e-6 * loss_full
+    full.close()
+    half.close()
+
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        runs = []
+        for pg in (None, dist.group.WORLD):
+            mlp = GpuMLP([Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base],
+                         tile_size=128, process_group=pg)
+            runs.append([mlp.train_step(xd, td, 0.2) for _ in range(3)])
+            mlp.close()
+        assert runs[0] == runs[1]
+    finally:
+        dist.destroy_process_group()
