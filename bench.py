@@ -521,8 +521,20 @@ def main():
         b_host[...] = B.cpu().numpy()
         del A, B, C
         torch.cuda.empty_cache()
+        # Under torchrun each rank computes one block of a pr x pc partition of the
+        # task grid: it reads its A row panel and B column panel in place (row /
+        # column slices of the pinned matrices) over its own host link.
+        a_v, b_v = a_host, b_host
+        if world > 1:
+            g = -(-n // T)
+            pr = max(d for d in range(1, int(world ** 0.5) + 1) if world % d == 0)
+            pc = world // pr
+            bi, bj = divmod(rank, pc)
+            r0, r1 = (bi * g // pr) * T, min(n, ((bi + 1) * g // pr) * T)
+            c0, c1 = (bj * g // pc) * T, min(n, ((bj + 1) * g // pc) * T)
+            a_v, b_v = a_host[r0:r1], b_host[:, c0:c1]
         for _ in range(2):  # warm-up: pinned output pool, HBM buffer pool, first large frees
-            res = tr.run(machine, a_host, b_host, T, precision=args.precision)
+            res = tr.run(machine, a_v, b_v, T, precision=args.precision)
             del res
         times = []
         h2d = d2h = 0
@@ -534,12 +546,7 @@ def main():
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            if world == 1:
-                c_host, s = tr.run(machine, a_host, b_host, T, precision=args.precision)
-            else:
-                with tr.Runtime(machine, T, precision=args.precision) as r2:
-                    c_host, s = r2.multiply(a_host, b_host, a_uid="A", b_uid="B", task_offset=rank,
-                                            task_stride=world)
+            c_host, s = tr.run(machine, a_v, b_v, T, precision=args.precision)
             e1.record()
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)

@@ -43,9 +43,23 @@ def describe(x) -> N.MatrixC:
     a = np.asarray(x)
     if a.ndim != 2:
         raise ValueError(f"expected a 2-D matrix, got shape {a.shape}")
-    if not a.flags.c_contiguous:
-        raise ValueError("host matrix must be C-contiguous")
-    return N.MatrixC(a.ctypes.data, a.shape[0], a.shape[1], max(a.shape[1], 1), dtype_code(a.dtype), N.TR_LOC_HOST)
+    if not row_major_view(a):
+        raise ValueError("host matrix must be row-major with unit column stride (a C-contiguous array or a "
+                         "row/column slice of one)")
+    ld = max(a.shape[1], 1) if a.shape[0] <= 1 else a.strides[0] // a.itemsize
+    return N.MatrixC(a.ctypes.data, a.shape[0], a.shape[1], ld, dtype_code(a.dtype), N.TR_LOC_HOST)
+
+
+def row_major_view(a: np.ndarray) -> bool:
+    """True for a C-contiguous array or a sub-block view of one (unit column
+    stride, row stride a positive multiple of the element size covering a row):
+    the runtime reads such views in place with pitched copies (ld = row stride)."""
+    if a.flags.c_contiguous:
+        return True
+    if a.shape[1] > 1 and a.strides[1] != a.itemsize:
+        return False
+    return a.shape[0] <= 1 or (a.strides[0] > 0 and a.strides[0] % a.itemsize == 0
+                               and a.strides[0] // a.itemsize >= a.shape[1])
 
 
 def pinned_empty(shape, dtype=np.float32) -> np.ndarray:

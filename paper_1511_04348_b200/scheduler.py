@@ -361,11 +361,14 @@ def write_report_csv(stats: RunStats, path) -> None:
 
 
 def _host_matrix(x):
-    """Host operand as a C-contiguous float32/float64 array (ints widen to f64)."""
+    """Host operand as a row-major float32/float64 array (ints widen to f64); a
+    row/column slice of a row-major array is read in place (no copy)."""
+    from .matrix import row_major_view
+
     a = np.asarray(x)
     if a.dtype not in (np.float32, np.float64):
         a = a.astype(np.float64)
-    return np.ascontiguousarray(a)
+    return a if a.ndim == 2 and row_major_view(a) else np.ascontiguousarray(a)
 
 
 class Runtime:

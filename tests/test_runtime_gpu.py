@@ -395,3 +395,19 @@ def test_kpanel_schedule_cold_product(precision):
         res[order] = cf
         rt.close()
     assert rel(res["auto"], res["shells"]) <= 1e-6 if precision == "fp32acc" else 1e-3
+
+
+def test_host_slices_read_in_place():
+    """Row slices of A, column slices of B and a sub-block of C are read and
+    written in place (pitched copies with the parent's row stride)."""
+    rng = np.random.default_rng(12)
+    a, b = int_matrix(rng, 700, 520), int_matrix(rng, 520, 900)
+    c = np.full((700, 900), -7.0)
+    a_v, b_v, c_v = a[100:600], b[:, 250:830], c[100:600, 250:830]
+    assert not b_v.flags.c_contiguous
+    rt = Runtime(homogeneous_machine(2, gpus=[0, 0]), 128)
+    out, s = rt.multiply(a_v, b_v, out=c_v)
+    assert out is c_v
+    assert np.array_equal(c[100:600, 250:830], O.reference_gemm(a_v, b_v))
+    assert (c[:100] == -7).all() and (c[:, :250] == -7).all() and (c[600:] == -7).all() and (c[:, 830:] == -7).all()
+    rt.close()

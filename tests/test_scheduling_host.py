@@ -264,3 +264,15 @@ def test_every_order_plans_the_same_task_set(order):
     _, s = rt.multiply(np.zeros((28, 20)), np.zeros((20, 36)), a_uid="A", b_uid="B")
     assert s.total_tasks == 7 * 9 and sum(s.tasks_by_device.values()) == 63
     assert s.cache.host_fetches == 7 * 5 + 5 * 9 and s.cache.input_requests == 2 * 63 * 5
+
+
+def test_describe_strided_host_views():
+    from paper_1511_04348_b200.matrix import describe
+
+    m = np.zeros((10, 12))
+    d = describe(m[2:7, 3:9])
+    assert (d.rows, d.cols, d.ld) == (5, 6, 12)
+    with pytest.raises(ValueError):
+        describe(m.T)  # column-major: not readable in place
+    with pytest.raises(ValueError):
+        describe(m[:, ::2])
