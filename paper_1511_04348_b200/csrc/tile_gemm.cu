@@ -47,10 +47,53 @@ struct Cfg {
   static constexpr int BN_LOCAL = BN / CG;                // B columns staged per CTA
   static constexpr int B_BYTES = BN_LOCAL * BK * 2;       // per plane
   static constexpr int STAGE_BYTES = PLANES * (A_BYTES + B_BYTES);
-  static constexpr int STAGES = std::min(6, (SMEM_BUDGET - 2048) / STAGE_BYTES);
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int STAGE_ROWS = 8;                    // epilogue staging: rows per warp per round
+  static constexpr int STAGE_LD = 132;                    // padded row (floats): conflict-free both ways
+  static constexpr int EPI_STAGE_BYTES = EPI_WARPS * STAGE_ROWS * STAGE_LD * 4;
+  static constexpr int STAGES = std::min(6, (SMEM_BUDGET - 2048 - EPI_STAGE_BYTES) / STAGE_BYTES);
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 };
 
+// Output unit u of a group launch -> (task, row/column origin).  A unit is one
+// 128 x 256 CTA tile (CG = 1) or one 256 x 256 pair tile (CG = 2).
+struct Unit {
+  int t, m0, n0;
+};
+template <int CG>
+__device__ __forceinline__ Unit unit_of(const GemmGroup& grp, int u, uint32_t rank) {
+  const int cta = u * CG;  // the unit's first CTA index in the flattened (non-persistent) grid
+  int t = 0;
+  while (t + 1 < grp.n_tasks && cta >= grp.cta_begin[t + 1]) ++t;
+  const int local = cta - grp.cta_begin[t];
+  const int m_cta = local % grp.m_blocks[t];
+  Unit r;
+  r.t = t;
+  r.m0 = (m_cta / CG) * (BM * CG) + static_cast<int>(rank) * BM;
+  r.n0 = (local / grp.m_blocks[t]) * BN;
+  return r;
+}
+
+// k-blocks of a task and this CTA's split-K share of them
+struct KRange {
+  int total, lo, hi;
+};
+__device__ __forceinline__ KRange krange(const GemmArgs& args) {
+  int total_kb = 0;
+  for (int ks = 0; ks < args.n_ksteps; ++ks) total_kb += (args.k_len[ks] + BK - 1) / BK;
+  const int n_split = static_cast<int>(gridDim.z);
+  KRange r;
+  r.total = total_kb;
+  r.lo = static_cast<int>((static_cast<int64_t>(blockIdx.z) * total_kb) / n_split);
+  r.hi = static_cast<int>((static_cast<int64_t>(blockIdx.z + 1) * total_kb) / n_split);
+  return r;
+}
+
+// The CTA (pair) walks output units u = cluster, cluster + n_clusters, ... of the
+// group -- one unit per CTA when the grid covers every unit, several when the
+// launch is persistent (grouped launches: one CTA per SM).  The producer and
+// the MMA issuer run straight across units; the epilogue warps drain unit i's
+// TMEM partial sums while the tensor core already computes unit i+1 into the
+// other TMEM buffer, so the store of one tile overlaps the next tile's k-loop.
 template <bool A_MN, bool B_K, int PLANES, int CG>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tile_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -68,30 +111,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue: partial sum ready in TMEM buffer b
   uint64_t* acc_empty = acc_full + 2;   // [2] epilogue -> MMA: TMEM buffer b drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;  // 0 = leader of the pair
   const bool leader = rank == 0;
-  // this CTA's task in the group and its block of that task's output
-  int t = 0;
-  while (t + 1 < grp.n_tasks && static_cast<int>(blockIdx.x) >= grp.cta_begin[t + 1]) ++t;
-  const GemmArgs& args = grp.task[t];
-  const int local = static_cast<int>(blockIdx.x) - grp.cta_begin[t];
-  const int m_cta = local % grp.m_blocks[t];
-  const int m0 = (m_cta / CG) * (BM * CG) + static_cast<int>(rank) * BM;
-  const int n0 = (local / grp.m_blocks[t]) * BN;                   // output tile columns
-  const int nb0 = n0 + static_cast<int>(rank) * BN_LOCAL;           // B columns this CTA stages
-
-  // k-blocks of this CTA (all of them, or its split-K share) and TMEM segments
-  int total_kb = 0;
-  for (int ks = 0; ks < args.n_ksteps; ++ks) total_kb += (args.k_len[ks] + BK - 1) / BK;
-  const int n_split = static_cast<int>(gridDim.z);
-  const int kb_lo = static_cast<int>((static_cast<int64_t>(blockIdx.z) * total_kb) / n_split);
-  const int kb_hi = static_cast<int>((static_cast<int64_t>(blockIdx.z + 1) * total_kb) / n_split);
-  const int my_kb = kb_hi - kb_lo;
-  const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(my_kb, 1);
-  const int n_seg = (my_kb + seg_kb - 1) / seg_kb;
+  const int n_units = grp.cta_begin[grp.n_tasks] / CG;
+  const int first_unit = static_cast<int>(blockIdx.x) / CG;
+  const int unit_stride = static_cast<int>(gridDim.x) / CG;
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -125,43 +153,50 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       int stage = 0;
       uint32_t phase = 0;
-      int g = 0;  // global k-block index
-      for (int ks = 0; ks < args.n_ksteps; ++ks) {
-        const int nkb = (args.k_len[ks] + BK - 1) / BK;
-        const int az = args.a_z[ks];
-        const int bz = args.b_z[ks];
-        for (int kb = 0; kb < nkb; ++kb, ++g) {
-          if (g < kb_lo || g >= kb_hi) continue;
-          ptx::mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
-          uint8_t* sb = sa + PLANES * A_BYTES;
-          const int k0 = kb * BK;
-          // completion bytes of both CTAs go to the leader's full barrier
-          const uint32_t bar = (CG == 2) ? ptx::mapa_shared(full0 + stage * 8, 0) : 0u;
-          if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE_BYTES);
-          auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1, int c2) {
-            if (CG == 2) ptx::tma_load_3d_cg2(dst, tm, bar, c0, c1, c2);
-            else ptx::tma_load_3d(dst, tm, &full[stage], c0, c1, c2);
-          };
+      for (int u = first_unit; u < n_units; u += unit_stride) {
+        const Unit un = unit_of<CG>(grp, u, rank);
+        const GemmArgs& args = grp.task[un.t];
+        const int nb0 = un.n0 + static_cast<int>(rank) * BN_LOCAL;  // B columns this CTA stages
+        const KRange kr = krange(args);
+        int g = 0;  // global k-block index
+        for (int ks = 0; ks < args.n_ksteps; ++ks) {
+          const int nkb = (args.k_len[ks] + BK - 1) / BK;
+          const int az = args.a_z[ks];
+          const int bz = args.b_z[ks];
+          for (int kb = 0; kb < nkb; ++kb, ++g) {
+            if (g < kr.lo || g >= kr.hi) continue;
+            ptx::mbar_wait(&empty[stage], phase ^ 1);
+            uint8_t* sa = smem + stage * STAGE_BYTES;
+            uint8_t* sb = sa + PLANES * A_BYTES;
+            const int k0 = kb * BK;
+            // completion bytes of both CTAs go to the leader's full barrier
+            const uint32_t bar = (CG == 2) ? ptx::mapa_shared(full0 + stage * 8, 0) : 0u;
+            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE_BYTES);
+            auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1, int c2) {
+              if (CG == 2) ptx::tma_load_3d_cg2(dst, tm, bar, c0, c1, c2);
+              else ptx::tma_load_3d(dst, tm, &full[stage], c0, c1, c2);
+            };
 #pragma unroll
-          for (int p = 0; p < PLANES; ++p) {
-            if (!A_MN) {
-              load(sa + p * A_BYTES, &tmA, k0, m0, az + p);
-            } else {
+            for (int p = 0; p < PLANES; ++p) {
+              if (!A_MN) {
+                load(sa + p * A_BYTES, &tmA, k0, un.m0, az + p);
+              } else {
 #pragma unroll
-              for (int g = 0; g < BM / 64; ++g) load(sa + p * A_BYTES + g * MN_GROUP_BYTES, &tmA, m0 + 64 * g, k0, az + p);
+                for (int gg = 0; gg < BM / 64; ++gg)
+                  load(sa + p * A_BYTES + gg * MN_GROUP_BYTES, &tmA, un.m0 + 64 * gg, k0, az + p);
+              }
+              if (B_K) {
+                load(sb + p * B_BYTES, &tmB, k0, nb0, bz + p);
+              } else {
+#pragma unroll
+                for (int gg = 0; gg < BN_LOCAL / 64; ++gg)
+                  load(sb + p * B_BYTES + gg * MN_GROUP_BYTES, &tmB, nb0 + 64 * gg, k0, bz + p);
+              }
             }
-            if (B_K) {
-              load(sb + p * B_BYTES, &tmB, k0, nb0, bz + p);
-            } else {
-#pragma unroll
-              for (int g = 0; g < BN_LOCAL / 64; ++g)
-                load(sb + p * B_BYTES + g * MN_GROUP_BYTES, &tmB, nb0 + 64 * g, k0, bz + p);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
             }
-          }
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
           }
         }
       }
@@ -172,61 +207,69 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, BN, A_MN, !B_K);
       int stage = 0;
       uint32_t phase = 0;
-      int kb_in_seg = 0, seg = 0;
-      uint32_t tmem_d = tmem_base;
-      uint32_t accumulate = 0;
-      int g = 0;  // global k-block index
-      for (int ks = 0; ks < args.n_ksteps; ++ks) {
-        const int nkb = (args.k_len[ks] + BK - 1) / BK;
-        for (int kb = 0; kb < nkb; ++kb, ++g) {
-          if (g < kb_lo || g >= kb_hi) continue;
-          if (kb_in_seg == 0) {
-            // new partial sum: wait until the epilogue(s) drained this TMEM buffer
-            const int buf = seg & 1;
-            ptx::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+      int seg = 0;  // TMEM partial sums issued so far (all units)
+      for (int u = first_unit; u < n_units; u += unit_stride) {
+        const Unit un = unit_of<CG>(grp, u, rank);
+        const GemmArgs& args = grp.task[un.t];
+        const KRange kr = krange(args);
+        const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(kr.hi - kr.lo, 1);
+        int kb_in_seg = 0;
+        uint32_t tmem_d = tmem_base;
+        uint32_t accumulate = 0;
+        int g = 0;
+        for (int ks = 0; ks < args.n_ksteps; ++ks) {
+          const int nkb = (args.k_len[ks] + BK - 1) / BK;
+          for (int kb = 0; kb < nkb; ++kb, ++g) {
+            if (g < kr.lo || g >= kr.hi) continue;
+            if (kb_in_seg == 0) {
+              // new partial sum: wait until the epilogue(s) drained this TMEM buffer
+              const int buf = seg & 1;
+              ptx::mbar_wait(&acc_empty[buf], ((seg >> 1) & 1) ^ 1);
+              ptx::tc_fence_after();
+              tmem_d = tmem_base + static_cast<uint32_t>(buf * BN);
+              accumulate = 0;
+            }
+            ptx::mbar_wait(&full[stage], phase);
             ptx::tc_fence_after();
-            tmem_d = tmem_base + static_cast<uint32_t>(buf * BN);
-            accumulate = 0;
-          }
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
-          const uint32_t b_base = a_base + PLANES * A_BYTES;
-          // PLANES == 2: small cross terms first, then hi*hi.
+            const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
+            const uint32_t b_base = a_base + PLANES * A_BYTES;
+            // PLANES == 2: small cross terms first, then hi*hi.
 #pragma unroll
-          for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
-            const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
-            const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
+            for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
+              const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
+              const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
 #pragma unroll
-            for (int k16 = 0; k16 < BK / 16; ++k16) {
-              const uint64_t adesc =
-                  A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024)
-                       : ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 32, 16, 1024);
-              const uint64_t bdesc =
-                  B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 32, 16, 1024)
-                      : ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024);
-              if (CG == 2) ptx::mma_bf16_cg2(tmem_d, adesc, bdesc, idesc, accumulate);
-              else ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
-              accumulate = 1;
+              for (int k16 = 0; k16 < BK / 16; ++k16) {
+                const uint64_t adesc =
+                    A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024)
+                         : ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 32, 16, 1024);
+                const uint64_t bdesc =
+                    B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 32, 16, 1024)
+                        : ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024);
+                if (CG == 2) ptx::mma_bf16_cg2(tmem_d, adesc, bdesc, idesc, accumulate);
+                else ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
+                accumulate = 1;
+              }
+            }
+            if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+            else ptx::mma_commit(&empty[stage]);
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            if (++kb_in_seg == seg_kb) {
+              if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+              else ptx::mma_commit(&acc_full[seg & 1]);
+              kb_in_seg = 0;
+              ++seg;
             }
           }
-          if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
-          else ptx::mma_commit(&empty[stage]);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-          if (++kb_in_seg == seg_kb) {
-            if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
-            else ptx::mma_commit(&acc_full[seg & 1]);
-            kb_in_seg = 0;
-            ++seg;
-          }
         }
-      }
-      if (kb_in_seg != 0) {
-        if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
-        else ptx::mma_commit(&acc_full[seg & 1]);
+        if (kb_in_seg != 0) {  // the unit's last, partial segment
+          if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+          else ptx::mma_commit(&acc_full[seg & 1]);
+          ++seg;
+        }
       }
     }
   } else if (warp >= EPI_WARP0) {
@@ -236,121 +279,112 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int row = q * 32 + lane;
     const uint32_t tlane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 128);
     const uint32_t empty_leader = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0) : 0u;
-    float acc[128];
+    float* stage = epi_stage + (warp - EPI_WARP0) * (C::STAGE_ROWS * C::STAGE_LD);
+    int seg = 0;
+    for (int u = first_unit; u < n_units; u += unit_stride) {
+      const Unit un = unit_of<CG>(grp, u, rank);
+      const GemmArgs& args = grp.task[un.t];
+      const KRange kr = krange(args);
+      const int my_kb = kr.hi - kr.lo;
+      const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(my_kb, 1);
+      const int n_seg = (my_kb + seg_kb - 1) / seg_kb;
+      float acc[128];
 #pragma unroll
-    for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-    for (int seg = 0; seg < n_seg; ++seg) {
-      const int buf = seg & 1;
-      ptx::mbar_wait(&acc_full[buf], (seg >> 1) & 1);
-      ptx::tc_fence_after();
+      for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+      for (int s = 0; s < n_seg; ++s, ++seg) {
+        const int buf = seg & 1;
+        ptx::mbar_wait(&acc_full[buf], (seg >> 1) & 1);
+        ptx::tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        uint32_t r[16];
-        ptx::tmem_ld_32x32b_x16(tlane + static_cast<uint32_t>(buf * BN + c * 16), r);
-        ptx::tmem_ld_wait();
+        for (int c = 0; c < 8; ++c) {
+          uint32_t r[16];
+          ptx::tmem_ld_32x32b_x16(tlane + static_cast<uint32_t>(buf * BN + c * 16), r);
+          ptx::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(r[j]);
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (CG == 2) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
-        else ptx::mbar_arrive(&acc_empty[buf]);
-      }
-    }
-    const int grow = m0 + row;
-    const int gcol0 = n0 + half * 128;
-    const bool part = n_split > 1;  // split-K: raw fp32 partials into the workspace
-    float* obase = part ? args.ws + blockIdx.z * args.ws_zstride : static_cast<float*>(args.c);
-    const int64_t ldo = part ? args.ws_ld : args.ldc;
-    if ((part || !args.c_f64) && gcol0 + 128 <= args.n_valid && (ldo & 3) == 0 &&
-        (reinterpret_cast<uintptr_t>(obase) & 15) == 0) {
-      // Coalesced epilogue: this warp's 32 x 128 block goes through the (now idle)
-      // operand ring -- rows padded to 132 floats keep both the row-per-thread
-      // writes and the row-per-warp reads bank-conflict-free -- so every global
-      // access is 512 contiguous bytes instead of 32 scattered 16-byte pieces.
-      float* stage = reinterpret_cast<float*>(smem) + (warp - EPI_WARP0) * (32 * 132);
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        *reinterpret_cast<float4*>(stage + lane * 132 + 4 * j) =
-            make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
-      __syncwarp();
-      const bool acc_mode = !part && args.epilogue == EPI_ACCUMULATE;
-      const int post = part ? static_cast<int>(POST_NONE) : args.post;
-      const int c = 4 * lane;
-      float bias4[4] = {0.f, 0.f, 0.f, 0.f};
-      if (post == POST_BIAS_ACT && args.bias)
-        for (int x = 0; x < 4; ++x) bias4[x] = args.bias[gcol0 + c + x];
-      const int row0 = m0 + q * 32;
-      for (int r = 0; r < 32 && row0 + r < args.m_valid; ++r) {
-        float4 v = *reinterpret_cast<const float4*>(stage + r * 132 + c);
-        float4* d4 = reinterpret_cast<float4*>(obase + static_cast<int64_t>(row0 + r) * ldo + gcol0 + c);
-        if (acc_mode) {
-          const float4 o = *d4;
-          v.x += o.x;
-          v.y += o.y;
-          v.z += o.z;
-          v.w += o.w;
+          for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(r[j]);
         }
-        if (post == POST_BIAS_ACT) {
-          v.x = act_fwd(args.act, v.x + bias4[0]);
-          v.y = act_fwd(args.act, v.y + bias4[1]);
-          v.z = act_fwd(args.act, v.z + bias4[2]);
-          v.w = act_fwd(args.act, v.w + bias4[3]);
-        } else if (post == POST_ACT_GRAD) {
-          const float* ax = args.aux + static_cast<int64_t>(row0 + r) * args.ldaux + gcol0 + c;
-          v.x *= act_grad_from_out(args.act, ax[0]);
-          v.y *= act_grad_from_out(args.act, ax[1]);
-          v.z *= act_grad_from_out(args.act, ax[2]);
-          v.w *= act_grad_from_out(args.act, ax[3]);
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (CG == 2) ptx::mbar_arrive_cluster(empty_leader + buf * 8);
+          else ptx::mbar_arrive(&acc_empty[buf]);
         }
-        *d4 = v;
       }
-    } else if (grow < args.m_valid && gcol0 < args.n_valid) {
-      const int ncols = min(128, args.n_valid - gcol0);
-      const bool partial = n_split > 1;  // split-K: raw fp32 partial into the workspace
-      const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
-      const bool acc_mode = !partial && args.epilogue == EPI_ACCUMULATE;
-      if (args.c_f64 && !partial) {
-        double* dst = static_cast<double*>(args.c) + off;
+      const int grow = un.m0 + row;
+      const int gcol0 = un.n0 + half * 128;
+      const bool part = gridDim.z > 1;  // split-K: raw fp32 partials into the workspace
+      float* obase = part ? args.ws + blockIdx.z * args.ws_zstride : static_cast<float*>(args.c);
+      const int64_t ldo = part ? args.ws_ld : args.ldc;
+      if ((part || !args.c_f64) && gcol0 + 128 <= args.n_valid && (ldo & 3) == 0 &&
+          (reinterpret_cast<uintptr_t>(obase) & 15) == 0) {
+        // Coalesced store: the warp's 32 x 128 block goes out through its own
+        // small staging area (8 rows per round; rows padded to 132 floats keep
+        // the row-per-thread writes and row-per-warp reads conflict-free), so
+        // every global access is 512 contiguous bytes.
+        const bool acc_mode = !part && args.epilogue == EPI_ACCUMULATE;
+        const int post = part ? static_cast<int>(POST_NONE) : args.post;
+        const int c = 4 * lane;
+        float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+        if (post == POST_BIAS_ACT && args.bias)
+          for (int x = 0; x < 4; ++x) bias4[x] = args.bias[gcol0 + c + x];
+        const int row0 = un.m0 + q * 32;
+#pragma unroll 1
+        for (int rb = 0; rb < 32; rb += C::STAGE_ROWS) {
+          if (lane >= rb && lane < rb + C::STAGE_ROWS) {
 #pragma unroll
-        for (int j = 0; j < 128; ++j)
-          if (j < ncols) dst[j] = acc_mode ? dst[j] + static_cast<double>(acc[j]) : static_cast<double>(acc[j]);
-      } else {
-        float* dst = partial ? args.ws + blockIdx.z * args.ws_zstride + static_cast<int64_t>(grow) * args.ws_ld + gcol0
-                             : static_cast<float*>(args.c) + off;
-        const int post = partial ? static_cast<int>(POST_NONE) : args.post;
-        const float* bias = args.bias ? args.bias + gcol0 : nullptr;
-        const float* aux = args.aux ? args.aux + static_cast<int64_t>(grow) * args.ldaux + gcol0 : nullptr;
-        auto finish = [&](float v, int j) -> float {
-          if (post == POST_BIAS_ACT) return act_fwd(args.act, v + (bias ? bias[j] : 0.f));
-          if (post == POST_ACT_GRAD) return v * act_grad_from_out(args.act, aux[j]);
-          return v;
-        };
-        if (ncols == 128 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-          float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            float4 v = make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+            for (int j = 0; j < 32; ++j)
+              *reinterpret_cast<float4*>(stage + (lane - rb) * C::STAGE_LD + 4 * j) =
+                  make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+          }
+          __syncwarp();
+          for (int r = 0; r < C::STAGE_ROWS && row0 + rb + r < args.m_valid; ++r) {
+            float4 v = *reinterpret_cast<const float4*>(stage + r * C::STAGE_LD + c);
+            float4* d4 = reinterpret_cast<float4*>(obase + static_cast<int64_t>(row0 + rb + r) * ldo + gcol0 + c);
             if (acc_mode) {
-              const float4 o = d4[j];
+              const float4 o = *d4;
               v.x += o.x;
               v.y += o.y;
               v.z += o.z;
               v.w += o.w;
             }
-            if (post != POST_NONE) {
-              v.x = finish(v.x, 4 * j);
-              v.y = finish(v.y, 4 * j + 1);
-              v.z = finish(v.z, 4 * j + 2);
-              v.w = finish(v.w, 4 * j + 3);
+            if (post == POST_BIAS_ACT) {
+              v.x = act_fwd(args.act, v.x + bias4[0]);
+              v.y = act_fwd(args.act, v.y + bias4[1]);
+              v.z = act_fwd(args.act, v.z + bias4[2]);
+              v.w = act_fwd(args.act, v.w + bias4[3]);
+            } else if (post == POST_ACT_GRAD) {
+              const float* ax = args.aux + static_cast<int64_t>(row0 + rb + r) * args.ldaux + gcol0 + c;
+              v.x *= act_grad_from_out(args.act, ax[0]);
+              v.y *= act_grad_from_out(args.act, ax[1]);
+              v.z *= act_grad_from_out(args.act, ax[2]);
+              v.w *= act_grad_from_out(args.act, ax[3]);
             }
-            d4[j] = v;
+            *d4 = v;
           }
-        } else {
+          __syncwarp();
+        }
+      } else if (grow < args.m_valid && gcol0 < args.n_valid) {
+        const int ncols = min(128, args.n_valid - gcol0);
+        const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
+        const bool acc_mode = !part && args.epilogue == EPI_ACCUMULATE;
+        if (args.c_f64 && !part) {
+          double* dst = static_cast<double*>(args.c) + off;
 #pragma unroll
           for (int j = 0; j < 128; ++j)
-            if (j < ncols) dst[j] = finish(acc_mode ? dst[j] + acc[j] : acc[j], j);
+            if (j < ncols) dst[j] = acc_mode ? dst[j] + static_cast<double>(acc[j]) : static_cast<double>(acc[j]);
+        } else {
+          float* dst = part ? obase + static_cast<int64_t>(grow) * ldo + gcol0 : static_cast<float*>(args.c) + off;
+          const int post = part ? static_cast<int>(POST_NONE) : args.post;
+          const float* bias = args.bias ? args.bias + gcol0 : nullptr;
+          const float* aux = args.aux ? args.aux + static_cast<int64_t>(grow) * args.ldaux + gcol0 : nullptr;
+#pragma unroll
+          for (int j = 0; j < 128; ++j) {
+            if (j >= ncols) continue;
+            float v = acc_mode ? dst[j] + acc[j] : acc[j];
+            if (post == POST_BIAS_ACT) v = act_fwd(args.act, v + (bias ? bias[j] : 0.f));
+            else if (post == POST_ACT_GRAD) v = v * act_grad_from_out(args.act, aux[j]);
+            dst[j] = v;
+          }
         }
       }
     }
@@ -368,7 +402,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 template <bool A_MN, bool B_K, int PLANES, int CG>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
-                           cudaStream_t stream) {
+                           bool persistent, cudaStream_t stream) {
   using C = Cfg<PLANES, CG>;
   auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG>;
   static std::once_flag once;
@@ -382,7 +416,14 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
     g.m_blocks[t] = ((a.m_valid + BM * CG - 1) / (BM * CG)) * CG;
     g.cta_begin[t + 1] = g.cta_begin[t] + g.m_blocks[t] * ((a.n_valid + BN - 1) / BN);
   }
-  dim3 grid(static_cast<unsigned>(g.cta_begin[g.n_tasks]), 1, k_split > 1 ? k_split : 1);
+  // persistent: one CTA (pair) per SM walks several output units; otherwise one unit per CTA
+  int ctas = g.cta_begin[g.n_tasks];
+  if (persistent) {
+    int dev = 0, sms = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = std::min(ctas, (sms / CG) * CG);
+  }
+  dim3 grid(static_cast<unsigned>(ctas), 1, k_split > 1 ? k_split : 1);
   if (CG == 1) {
     kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, g);
     return cudaGetLastError();
@@ -493,25 +534,25 @@ void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* 
 }
 
 static cudaError_t dispatch(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split, bool a_mn,
-                            bool b_kmajor, bool pair, int planes, cudaStream_t stream) {
+                            bool b_kmajor, bool pair, int planes, bool persistent, cudaStream_t stream) {
   const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (planes == 2 ? 1 : 0) | (pair ? 8 : 0);
   switch (variant) {
-    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, stream);
-    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, stream);
-    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, stream);
-    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, stream);
-    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, stream);
-    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, stream);
-    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, stream);
-    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, stream);
-    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, stream);
-    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, stream);
-    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, stream);
-    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, stream);
-    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, stream);
-    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, stream);
-    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, stream);
-    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, stream);
+    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
+    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
+    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
   }
 }
 
@@ -527,7 +568,7 @@ cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   GemmGroup g;
   g.n_tasks = 1;
   g.task[0] = args;
-  return dispatch(tmA, tmB, g, args.k_split, a_mn, b_kmajor, pair, args.planes, stream);
+  return dispatch(tmA, tmB, g, args.k_split, a_mn, b_kmajor, pair, args.planes, /*persistent=*/false, stream);
 }
 
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
@@ -539,7 +580,7 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
     if (!args_ok(a) || a.k_split > 1 || a.planes != g.task[0].planes || (a.m_valid > BM && group_pairs_enabled()) != pair)
       return cudaErrorInvalidValue;
   }
-  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, stream);
+  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent_enabled(), stream);
 }
 
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {
@@ -582,6 +623,20 @@ bool gemm_pairs_enabled() {
 }
 
 void set_gemm_pairs(bool on) { g_pairs.store(on ? 1 : 0); }
+
+static std::atomic<int> g_persistent{-1};
+
+bool persistent_enabled() {
+  int v = g_persistent.load();
+  if (v < 0) {
+    const char* e = getenv("TR_PERSISTENT");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_persistent.store(v);
+  }
+  return v != 0;
+}
+
+void set_persistent(bool on) { g_persistent.store(on ? 1 : 0); }
 
 static std::atomic<int> g_group_pairs{-1};
 

@@ -124,6 +124,11 @@ void set_gemm_pairs(bool on);
 // (TR_GROUP_PAIRS=0 or set_group_pairs(false) selects single CTAs).
 bool group_pairs_enabled();
 void set_group_pairs(bool on);
+// Grouped launches are persistent by default (one CTA / pair per SM walking
+// several output units, the store of one tile overlapping the next tile's
+// k-loop); TR_PERSISTENT=0 or set_persistent(false) launches one CTA per unit.
+bool persistent_enabled();
+void set_persistent(bool on);
 
 // K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
 // into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything
