@@ -242,6 +242,11 @@ typedef struct {
   const float* bias;   /* TR_POST_BIAS_ACT: c.cols floats (device), may be NULL */
   const float* aux;    /* TR_POST_ACT_GRAD: c.rows x c.cols activation output (device) */
   int64_t ldaux;
+  uint64_t cache_as;   /* != 0: the result will be read as an INPUT under this uid (e.g. the next
+                          layer's activations); the producing kernel also writes its converted
+                          tiles straight into the tile cache (float32 device outputs, full tiles;
+                          uncounted until requested, like a fetch-ahead), saving the later
+                          split/convert pass.  0 = off. */
 } tr_product;
 int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_report* report);
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,

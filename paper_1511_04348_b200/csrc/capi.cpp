@@ -330,6 +330,7 @@ int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_
       p.bias = q.bias;
       p.aux = q.aux;
       p.ldaux = q.ldaux;
+      p.cache_as = q.cache_as;
     }
     s->s->run_products(std::move(v), 0, 1, report);
   });

@@ -824,6 +824,7 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   grp.n_tasks = static_cast<int32_t>(gtids.size());
   std::vector<TileKey> used;
   std::vector<int32_t> used_phys;
+  std::vector<int32_t> wt_phys;  // slots the launch writes through
   const Product* p0 = nullptr;
   for (size_t q = 0; q < gtids.size(); ++q) {
     int64_t tid = 0;
@@ -867,6 +868,8 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
+    const int32_t wt = write_through(d, s, p, i, j, args);
+    if (wt >= 0) wt_phys.push_back(wt);
   }
   BoxKind ba, bb;
   gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
@@ -895,6 +898,10 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     std::lock_guard<std::mutex> g(dir_->mu);
     const EvRef ev = record(d, s);
     for (int32_t ph : used_phys) note_use(dc.slots[ph], ev);
+    for (int32_t ph : wt_phys) {  // the written-through tiles are ready when the launch is done
+      dc.slots[ph].ready = ev;
+      dc.slots[ph].uses.clear();
+    }
     for (const TileKey& k : used) dir_->release_input_locked(d, k);
     for (int64_t gt : gtids) {
       int64_t tid = 0;
@@ -914,6 +921,29 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   TR_CUDA(cudaEventRecord(sc.done, sc.stream));
   sc.task = gtids[0];
   sc.group_rest.assign(gtids.begin() + 1, gtids.end());
+}
+
+// ---------------------------------------------------------------- write-through
+// A product whose output is read later as an input (Product::cache_as) has its
+// output tiles admitted into the tile cache by the producing kernel itself: the
+// epilogue writes the K2 planes next to the float32 result, so the consumer's
+// acquire finds the tile resident (counted as the reference counts it: a host
+// fetch, the pending entry being uncounted until requested) and no split/convert
+// pass runs.  Full tiles on the coalesced epilogue path only.
+int32_t Session::write_through(int d, int s, const Product& p, int64_t i, int64_t j, GemmArgs& args) {
+  if (!p.cache_as || dryrun_ || !coherence_ || p.c.dtype != TR_DTYPE_F32 || args.k_split > 1) return -1;
+  const int64_t T = tile_;
+  if (T % 256 != 0 || std::min(T, p.M - i * T) != T || std::min(T, p.N - j * T) != T) return -1;
+  if ((args.ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(args.c) & 15) != 0) return -1;
+  std::lock_guard<std::mutex> g(dir_->mu);
+  int32_t slot = -1, source = TR_SOURCE_HOST;
+  if (!dir_->prefetch_locked(d, TileKey{p.cache_as, i, j}, &slot, &source, false)) return -1;
+  const int32_t phys = phys_of(d, slot);
+  wait_slot_free(d, s, phys);  // earlier readers / fills of this physical slot
+  args.wt = slot_ptr(d, phys);
+  args.wt_ld = ld_;
+  args.wt_plane = plane_elems_;
+  return phys;
 }
 
 // ---------------------------------------------------------------- task issue
@@ -987,6 +1017,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       used_phys.push_back(pb);
     }
     if (!dryrun_) plan_split_k(d, *scp, args);
+    const int32_t wt = (!dryrun_ && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
     if (!dryrun_ && job.async) {
       BoxKind ba, bb;
       gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
@@ -1019,6 +1050,10 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       if (!dryrun_ && coherence_) {
         const EvRef ev = record(d, s);
         for (int32_t p : used_phys) note_use(dc.slots[p], ev);
+        if (wt >= 0) {
+          dc.slots[wt].ready = ev;
+          dc.slots[wt].uses.clear();
+        }
       }
       for (const TileKey& k : used) dir_->release_input_locked(d, k);
     }

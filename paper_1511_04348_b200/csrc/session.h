@@ -60,6 +60,7 @@ struct Product {
   const float* bias = nullptr;
   const float* aux = nullptr;
   int64_t ldaux = 0;
+  uint64_t cache_as = 0;  // write-through: the output's tiles enter the cache under this uid
 };
 
 struct Job {
@@ -203,6 +204,9 @@ class Session {
   void sim_task(int d, Job& job, int64_t gtid, double t);
   double xfer_cost(int src, int dst, int64_t nbytes) const;
   void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
+  // write-through: reserve the cache slot for output tile (i, j) of p and point
+  // args at its planes; returns the physical slot (-1: not written through)
+  int32_t write_through(int d, int s, const Product& p, int64_t i, int64_t j, GemmArgs& args);
   // grouped launches: several ready tasks of one product in one K1 launch
   bool groupable(int d, Job& job, int64_t gtid);
   void issue_group(int d, Job& job, const std::vector<int64_t>& gtids, int s);

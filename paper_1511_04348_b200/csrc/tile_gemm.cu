@@ -42,6 +42,21 @@ constexpr int SMEM_BUDGET = 227 * 1024;
 //         columns of B, the leader issues M=256 MMAs over both CTAs' smem, and
 //         each CTA's TMEM holds its 128 x 256 accumulator.  Per SM this halves
 //         the B bytes fetched and the smem bytes the tensor core reads.
+// hi = bf16(v), lo = bf16(v - hi) for 4 consecutive values (the K2 split of a
+// float32 input, bit for bit), stored as 8-byte vectors into 1 or 2 planes.
+__device__ __forceinline__ void split4(uint16_t* dst, int64_t plane, int planes, float4 v) {
+  const float x[4] = {v.x, v.y, v.z, v.w};
+  uint16_t hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x[i]);
+    hi[i] = __bfloat16_as_ushort(h);
+    lo[i] = __bfloat16_as_ushort(__float2bfloat16_rn(x[i] - __bfloat162float(h)));
+  }
+  *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(hi);
+  if (planes == 2) *reinterpret_cast<uint2*>(dst + plane) = *reinterpret_cast<const uint2*>(lo);
+}
+
 template <int PLANES, int CG>
 struct Cfg {
   static constexpr int BN_LOCAL = BN / CG;                // B columns staged per CTA
@@ -360,6 +375,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               v.w *= act_grad_from_out(args.act, ax[3]);
             }
             *d4 = v;
+            if (args.wt)  // write-through: the converted planes of this row segment (as K2)
+              split4(args.wt + static_cast<int64_t>(row0 + rb + r) * args.wt_ld + gcol0 + c, args.wt_plane,
+                     PLANES, v);
           }
           __syncwarp();
         }

@@ -59,6 +59,12 @@ struct GemmArgs {
   float* ws;
   int64_t ws_ld;
   int64_t ws_zstride;
+  // Write-through (non-null wt): the final values are also split into `planes`
+  // bf16 planes at wt (row stride wt_ld, plane stride wt_plane) -- a tile-cache
+  // slot, exactly as K2 would convert them.  Full tiles, coalesced path only.
+  uint16_t* wt;
+  int64_t wt_ld;
+  int64_t wt_plane;
 };
 
 // Several tasks in ONE launch (a station's worth of ready tasks): CTAs

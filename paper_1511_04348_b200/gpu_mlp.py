@@ -62,7 +62,7 @@ class GpuMLP:
 
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
                  device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
-                 process_group=None):
+                 process_group=None, write_through: bool = True):
         import torch
 
         self.torch = torch
@@ -77,6 +77,7 @@ class GpuMLP:
             runtime = Runtime(machine, tile_size, precision=precision)
         self.rt = runtime
         self.stream_ordered = stream_ordered
+        self.write_through = write_through  # producers write the next round's operand tiles into the cache
         self.pg = process_group
         if process_group is not None:
             import torch.distributed as dist
@@ -143,10 +144,12 @@ class GpuMLP:
             xs.append(cur)
             uids.append(cur_uid)
             a = self._buf(f"a{li}", (cur.shape[0], L.w.shape[1]))
+            nxt = self.rt.fresh_uid("x")
+            # the activation is the next product's A: its tiles enter the cache as they are produced
             self._batch([dict(a=cur, b=L.w, out=a, a_uid=cur_uid, b_uid=L.weight_uid,
-                              post=("bias_act", L.b, L.activation))])
-            cur, cur_uid = a, self.rt.fresh_uid("x")
-        self._step_uids = list(uids)
+                              post=("bias_act", L.b, L.activation), cache_as=nxt if self.write_through else None)])
+            cur, cur_uid = a, nxt
+        self._step_uids = list(uids) + [cur_uid]
         pred = cur
         d_out = self._buf("dout", pred.shape)
         N.call("tr_mlp_mse_grad_global", _ptr(d_out), _ptr(pred), _ptr(target), pred.numel(),
@@ -156,15 +159,18 @@ class GpuMLP:
         N.call("tr_mlp_act_grad", _ptr(d_y), _ptr(d_out), None, _ptr(pred), d_y.numel(),
                _ACT[self.layers[last].activation], s)
         grads = [None] * len(self.layers)
+        dy_uid = self.rt.fresh_uid("dy")
         for li in range(last, -1, -1):
             L = self.layers[li]
-            dy_uid = self.rt.fresh_uid("dy")
             self._step_uids.append(dy_uid)
+            next_dy = self.rt.fresh_uid("dy")
             d_w = self._buf(f"dw{li}", L.w.shape)
             d_x = self._buf(f"dy{li - 1}" if li > 0 else "dx0", xs[li].shape)
             dx = dict(a=d_y, b=L.w, out=d_x, transpose_b=True, a_uid=dy_uid, b_uid=L.weight_uid)
             if li > 0:  # dX_l * act'(A_{l-1}) = dY_{l-1}  (xs[li] is A_{l-1})
                 dx["post"] = ("act_grad", xs[li], self.layers[li - 1].activation)
+                if self.write_through:
+                    dx["cache_as"] = next_dy  # dY_{l-1} is the next round's operand
             self._batch([dict(a=xs[li], b=d_y, out=d_w, transpose_a=True, a_uid=uids[li], b_uid=dy_uid), dx])
             d_b = None
             if L.b is not None:
@@ -172,7 +178,7 @@ class GpuMLP:
                 N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
             self._allreduce(d_w, d_b)  # overlaps the next (lower) layer's backward round
             grads[li] = (d_w, d_b)
-            d_y = d_x
+            d_y, dy_uid = d_x, next_dy
         return pred.numel(), grads
 
     def train_step(self, x, target, lr: float) -> float:

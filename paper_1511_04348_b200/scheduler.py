@@ -543,7 +543,10 @@ class Runtime:
         ``b``, ``out`` (CUDA tensors), optional ``transpose_a``/``transpose_b``,
         ``a_uid``/``b_uid``/``c_uid``, and an optional fused epilogue
         ``post=("bias_act", bias, activation)`` or ``post=("act_grad", a_prev,
-        activation)`` (float32 device outputs).  Returns the combined RunStats."""
+        activation)`` (float32 device outputs).  ``cache_as=uid`` marks an output that a
+        later product reads as an input under ``uid``: the producing kernel writes
+        its converted tiles straight into the tile cache (tr_product.cache_as).
+        Returns the combined RunStats."""
         if self.mode == "sim":
             raise ValueError("multiply_batch runs on the GPU; the simulated engine takes one product per call")
         acts = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
@@ -559,6 +562,8 @@ class Runtime:
             q.a_uid = self._uids.id(pr.get("a_uid") or self.fresh_uid())
             q.b_uid = self._uids.id(pr.get("b_uid") or self.fresh_uid())
             q.c_uid = self._uids.id(pr.get("c_uid") or self.fresh_uid("c"))
+            if pr.get("cache_as"):  # the output is read later as an input under this uid
+                q.cache_as = self._uids.id(pr["cache_as"])
             post = pr.get("post")
             if post is not None:
                 kind, ref, act = post

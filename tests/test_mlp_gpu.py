@@ -130,3 +130,35 @@ def test_data_parallel_shards_sum_to_full_batch():
         assert runs[0] == runs[1]
     finally:
         dist.destroy_process_group()
+
+
+def test_write_through_matches_convert():
+    """Producers writing the next round's operand tiles straight into the cache
+    (cache_as) give bit-identical training to converting them on demand, and
+    run fewer split/convert launches."""
+    rng = np.random.default_rng(13)
+    sizes = [256, 1024, 768, 512]
+    base = [Layer.random(sizes[i], sizes[i + 1], rng, scale=1 / np.sqrt(sizes[i]), tag=f"layer{i}") for i in range(3)]
+    x, t = O.random_regression(rng, 512, 256, 512)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    runs = {}
+    for wt in (False, True):
+        mlp = GpuMLP([Layer(L.weights.copy(), L.bias.copy(), L.activation, tag=L.tag) for L in base],
+                     tile_size=256, write_through=wt, stream_ordered=False)
+        launches = []
+        orig = mlp.rt.multiply_batch
+
+        def counting(prods, _orig=orig):
+            st = _orig(prods)
+            launches.append(st.gpu_launches)
+            return st
+
+        mlp.rt.multiply_batch = counting
+        losses = [mlp.train_step(xd, td, 0.2) for _ in range(3)]
+        runs[wt] = (losses, mlp.to_host(), sum(launches))
+        mlp.close()
+    assert runs[True][0] == runs[False][0]
+    for (w1, b1), (w0, b0) in zip(runs[True][1], runs[False][1]):
+        assert np.array_equal(w1, w0) and np.array_equal(b1, b0)
+    assert runs[True][2] < runs[False][2]
