@@ -1126,7 +1126,10 @@ void Session::run_job(int d, Job& job) {
       reap(d, job, true);
       continue;
     }
-    job.claimed.fetch_add(static_cast<int64_t>(st.refill(job.queue, dc.width - active).size()));
+    // a grouped launch takes a whole station's worth of tasks on ONE stream, so the
+    // station refills to its full width regardless of the streams in flight
+    const int room = (max_group_ > 1 && !dryrun_) ? dc.width : dc.width - active;
+    job.claimed.fetch_add(static_cast<int64_t>(st.refill(job.queue, room).size()));
     if (ahead) fetch_ahead(d, job, seen, seen_global, dc.pending_prefetch);
     uint64_t tid;
     int victim = -1;
