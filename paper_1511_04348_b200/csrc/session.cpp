@@ -739,7 +739,8 @@ bool Session::run_panels(Job& job) {
     gemm_boxes(p.ta, p.tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
     TimedLaunch tl = timing_pair(d);
     TR_CUDA(cudaEventRecord(tl.start, sc.stream));
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p.ta, p.tb, sc.stream));
+    // non-persistent: the schedule keeps several launches in flight on its streams
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p.ta, p.tb, /*persistent=*/false, sc.stream));
     TR_CUDA(cudaEventRecord(tl.end, sc.stream));
     dc.timed.push_back(tl);
     if (tracing_)

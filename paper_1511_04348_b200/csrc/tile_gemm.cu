@@ -591,6 +591,11 @@ cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
                                    bool b_kmajor, cudaStream_t stream) {
+  return launch_tile_gemm_group(tmA, tmB, g, a_mn, b_kmajor, persistent_enabled(), stream);
+}
+
+cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
+                                   bool b_kmajor, bool persistent, cudaStream_t stream) {
   if (g.n_tasks < 1 || g.n_tasks > kMaxGroup) return cudaErrorInvalidValue;
   const bool pair = g.task[0].m_valid > BM && group_pairs_enabled();
   for (int t = 0; t < g.n_tasks; ++t) {
@@ -598,7 +603,7 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
     if (!args_ok(a) || a.k_split > 1 || a.planes != g.task[0].planes || (a.m_valid > BM && group_pairs_enabled()) != pair)
       return cudaErrorInvalidValue;
   }
-  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent_enabled(), stream);
+  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent, stream);
 }
 
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {
