@@ -56,3 +56,24 @@ def test_bounded_capacity_keeps_reference_semantics():
     assert _check_slices(a, b, c, n) <= 1e-5
     assert s.cache.evictions > 0 and s.cache.input_requests == 2 * 8 ** 3
     rt.close()
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+def test_out_of_core_kpanel_blocks_integer_exact(precision):
+    """Ragged out-of-core product (A and B planes ~5x the tile budget) on one
+    device: the block-wise k-panel schedule with future-aware eviction is exact
+    on integer inputs, computes every task once and writes every C tile once."""
+    rng = np.random.default_rng(40)
+    m, k, n, T = 1400, 1900, 1250, 128  # 11 x 10 tasks, 15 k-steps; 165 + 150 input tiles
+    a = rng.integers(-4, 5, size=(m, k)).astype(np.float32)
+    b = rng.integers(-4, 5, size=(k, n)).astype(np.float32)
+    planes = 2 if precision == "fp32acc" else 1
+    slot = planes * T * T * 2
+    overhead = (4 + 2) * 2 * T * T * 8 + 4 * T * T * 8
+    rt = Runtime(homogeneous_machine(1, dtype=np.float32), T, precision=precision,
+                 hbm_budget_bytes=overhead + (60 + 8) * slot)
+    c, s = rt.multiply(a, b, a_uid="A", b_uid="B")
+    assert np.array_equal(c, a.astype(np.float64) @ b.astype(np.float64))
+    assert s.total_tasks == 110 and s.cache.writebacks == 110 and s.tasks_by_device == {0: 110}
+    assert s.cache.input_requests == 2 * 110 * 15 and s.cache.evictions > 0
+    rt.close()

@@ -18,7 +18,7 @@ for m in (a, b):
 print(f"filled {time.perf_counter() - t0:.1f} s", flush=True)
 m = tr.homogeneous_machine(1, dtype=np.float32)
 flops = 2.0 * n ** 3
-cases = [(16, "auto"), (24, "auto"), (24, "auto"), (32, "auto")]
+cases = [(16, "auto"), (24, "auto"), (24, "auto"), (24, "blocked"), (32, "auto")]
 for budget_gb, order in cases:
     rt = tr.Runtime(m, T, hbm_budget_bytes=int(budget_gb * 2**30), trace=(budget_gb == 24))
     rt.set_order(order)
