@@ -913,6 +913,11 @@ void Session::run_job(int d, Job& job) {
   uint64_t seq = 0;
   bool ahead = !dryrun_ && coherence_ && !(flags_ & TR_FLAG_NO_PREFETCH);
   for (auto& dv : devs_) ahead = ahead && dv.capacity < 0;  // bounded caches: keep eviction order exact
+  // locality priority among a station's reserved tasks (unbounded caches only:
+  // bounded ones keep the reference's FIFO pop and exact eviction order)
+  bool prio = !dryrun_ && coherence_ && !job.async && getenv("TR_PRIORITY") == nullptr;
+  for (auto& dv : devs_) prio = prio && dv.capacity < 0;
+  if (const char* e = getenv("TR_PRIORITY")) prio = !dryrun_ && e[0] == '1';
   std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.total) : 0, 0);
   std::vector<uint8_t> seen_global(seen.size(), 0);
   dc.pending_prefetch = 0;
@@ -933,7 +938,27 @@ void Session::run_job(int d, Job& job) {
     if (ahead) fetch_ahead(d, job, seen, seen_global, dc.pending_prefetch);
     uint64_t tid;
     int victim = -1;
-    if (!st.pop_for_run(&tid)) {
+    bool popped;
+    if (prio) {
+      // locality priority: the reserved task with the most input tiles already in
+      // this device's HBM (2 points) or a peer's (1 point) runs first
+      popped = st.pop_best(&tid, [&](uint64_t t) {
+        int64_t lt = 0;
+        const Product& p = job.prod_of(static_cast<int64_t>(t), &lt);
+        const int64_t i = lt / p.grid_cols, j = lt % p.grid_cols;
+        int score = 0;
+        std::lock_guard<std::mutex> g(dir_->mu);
+        for (int64_t k = 0; k < p.k_steps; ++k) {
+          const uint64_t oa = dir_->owners_locked(TileKey{p.a_uid, p.ta ? k : i, p.ta ? i : k});
+          const uint64_t ob = dir_->owners_locked(TileKey{p.b_uid, p.tb ? j : k, p.tb ? k : j});
+          for (uint64_t o : {oa, ob}) score += (o >> d & 1) ? 2 : (o ? 1 : 0);
+        }
+        return score;
+      });
+    } else {
+      popped = st.pop_for_run(&tid);
+    }
+    if (!popped) {
       if (!job.queue.is_empty()) continue;  // raced with other refills
       bool got = false;
       if (steal_) got = steal_task(d, station_ptrs_.data(), static_cast<int>(station_ptrs_.size()), &tid, &victim);

@@ -44,6 +44,25 @@ class Station {
     slots_.pop_front();
     return true;
   }
+  // Priority pop (B200 addition): the reserved id with the highest score,
+  // ties to the front (FIFO); with a constant score this is pop_for_run.
+  template <typename Score>
+  bool pop_best(uint64_t* tid, Score score) {
+    std::lock_guard<std::mutex> g(mu_);
+    if (slots_.empty()) return false;
+    size_t best = 0;
+    int best_score = score(slots_[0]);
+    for (size_t i = 1; i < slots_.size(); ++i) {
+      const int sc = score(slots_[i]);
+      if (sc > best_score) {
+        best = i;
+        best_score = sc;
+      }
+    }
+    *tid = slots_[best];
+    slots_.erase(slots_.begin() + static_cast<std::ptrdiff_t>(best));
+    return true;
+  }
   // scheduler.py:230-232
   bool try_steal(uint64_t* tid) {
     std::lock_guard<std::mutex> g(mu_);
