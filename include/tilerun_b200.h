@@ -82,6 +82,9 @@ typedef struct {
   int32_t gpu;            /* physical CUDA ordinal; -1 = device_id % visible GPUs        */
   double flops_per_unit;  /* simulated engine: flops per time unit (devices.py:255-261)   */
   double host_bandwidth;  /* simulated engine: bytes per time unit to/from host (264-283) */
+  int32_t sm_count;       /* > 0: the logical device runs on a green context of this many
+                             SMs of its GPU (disjoint from the GPU's other such devices);
+                             0 = the whole GPU.  Inhomogeneous devices on one GPU.       */
 } tr_device_spec;
 
 typedef struct {

@@ -36,7 +36,7 @@ P = C.POINTER
 
 class DeviceSpecC(C.Structure):
     _fields_ = [("device_id", i32), ("kind", i32), ("capacity_tiles", i64), ("slots", i32), ("gpu", i32),
-                ("flops_per_unit", f64), ("host_bandwidth", f64)]
+                ("flops_per_unit", f64), ("host_bandwidth", f64), ("sm_count", i32)]
 
 
 class MachineC(C.Structure):

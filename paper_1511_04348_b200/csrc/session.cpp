@@ -35,6 +35,23 @@ void pin_thread_to_core(int index) {
   pthread_setaffinity_np(pthread_self(), sizeof(one), &one);
 }
 
+// Driver entry points for green contexts (the library links the static runtime,
+// not libcuda; cuTensorMapEncodeTiled is reached the same way).
+template <typename Fn>
+Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    fail(TR_ERR_CUDA, "driver entry point %s unavailable", name);
+  }
+  return reinterpret_cast<Fn>(p);
+}
+
+void check_cu(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS) fail(TR_ERR_CUDA, "%s failed (CUresult %d)", what, static_cast<int>(r));
+}
+
 }  // namespace
 
 void Job::mark(int64_t tid) {
@@ -59,6 +76,10 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
   sim_ = flags & TR_FLAG_SIM;
   max_group_ = task_group_max();
+  // Inhomogeneous devices (green contexts of different sizes): smaller groups keep
+  // a slow device from holding several tasks at once (tools/green/probe_green_1234.py).
+  for (int d = 1; d < m.n_devices; ++d)
+    if (m.devices[d].sm_count != m.devices[0].sm_count) max_group_ = std::min(max_group_, 2);
   dryrun_ = (flags & TR_FLAG_DRYRUN) || sim_;
   steal_ = flags & TR_FLAG_STEAL;
   coherence_ = flags & TR_FLAG_COHERENCE;
@@ -129,11 +150,56 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
     return std::chrono::duration<double, std::milli>(b - a).count();
   };
   if (!dryrun_) {
+    // Inhomogeneous devices: a logical device with sm_count > 0 runs on a green
+    // context holding that many SMs of its GPU.  A GPU's SMs are split once into
+    // groups of the hardware granularity (8 SMs on B200; the remainder of a
+    // split cannot be split again), and its such devices take ceil(count / 8)
+    // consecutive groups each, in device-id order -- disjoint SM sets.
+    constexpr unsigned kSmGroup = 8;
+    std::vector<std::vector<CUdevResource>> sm_groups(static_cast<size_t>(std::max(n_gpus, 1)));
+    std::vector<size_t> sm_next(sm_groups.size(), 0);
+    for (int d = 0; d < n; ++d) {
+      const int want = m.devices[d].sm_count;
+      if (want <= 0) continue;
+      DeviceCtx& dc = devs_[d];
+      TR_CUDA(cudaSetDevice(dc.gpu));
+      TR_CUDA(cudaFree(nullptr));  // the primary context exists before the green one
+      CUdevice cudev;
+      check_cu(driver_fn<decltype(&cuDeviceGet)>("cuDeviceGet")(&cudev, dc.gpu), "cuDeviceGet");
+      auto& pool = sm_groups[dc.gpu];
+      if (pool.empty()) {
+        CUdevResource all, rest;
+        check_cu(driver_fn<decltype(&cuDeviceGetDevResource)>("cuDeviceGetDevResource")(cudev, &all,
+                                                                                       CU_DEV_RESOURCE_TYPE_SM),
+                 "cuDeviceGetDevResource");
+        unsigned n_groups = all.sm.smCount / kSmGroup;
+        pool.resize(n_groups);
+        check_cu(driver_fn<decltype(&cuDevSmResourceSplitByCount)>("cuDevSmResourceSplitByCount")(
+                     pool.data(), &n_groups, &all, &rest, 0, kSmGroup),
+                 "cuDevSmResourceSplitByCount");
+        pool.resize(n_groups);
+      }
+      const size_t take = (static_cast<size_t>(want) + kSmGroup - 1) / kSmGroup;
+      if (sm_next[dc.gpu] + take > pool.size())
+        fail(TR_ERR_CONFIG, "device %d: GPU %d has only %zu of the %zu SM groups of %u requested", d, dc.gpu,
+             pool.size() - sm_next[dc.gpu], take, kSmGroup);
+      CUdevResourceDesc desc;
+      check_cu(driver_fn<decltype(&cuDevResourceGenerateDesc)>("cuDevResourceGenerateDesc")(
+                   &desc, pool.data() + sm_next[dc.gpu], static_cast<unsigned>(take)),
+               "cuDevResourceGenerateDesc");
+      dc.green_sms = 0;
+      for (size_t k = 0; k < take; ++k) dc.green_sms += static_cast<int>(pool[sm_next[dc.gpu] + k].sm.smCount);
+      sm_next[dc.gpu] += take;
+      check_cu(driver_fn<decltype(&cuGreenCtxCreate)>("cuGreenCtxCreate")(&dc.green, desc, cudev,
+                                                                           CU_GREEN_CTX_DEFAULT_STREAM),
+               "cuGreenCtxCreate");
+    }
     for (int d = 0; d < n; ++d) {
       DeviceCtx& dc = devs_[d];
       const auto q0 = tnow();
       TR_CUDA(cudaSetDevice(dc.gpu));
       TR_CUDA(cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dc.gpu));
+      if (dc.green) dc.sms = dc.green_sms;
       size_t free_b = 0;
       TR_CUDA(DevPool::get().free_bytes(dc.gpu, &free_b));
       const double reusable = static_cast<double>(free_b) + static_cast<double>(DevPool::get().cached_bytes());
@@ -157,8 +223,15 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
         StreamCtx& sc = dc.streams[si];
         // the fill stream runs at the highest priority: its split/convert kernels
         // must not queue behind GEMM CTAs that occupy every SM
-        TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking,
-                                             static_cast<int>(si) == dc.width ? prio_high : prio_low));
+        const int prio = static_cast<int>(si) == dc.width ? prio_high : prio_low;
+        if (dc.green) {
+          CUstream cs;
+          check_cu(driver_fn<decltype(&cuGreenCtxStreamCreate)>("cuGreenCtxStreamCreate")(
+                       &cs, dc.green, CU_STREAM_NON_BLOCKING, prio), "cuGreenCtxStreamCreate");
+          sc.stream = reinterpret_cast<cudaStream_t>(cs);
+        } else {
+          TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking, prio));
+        }
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
@@ -214,6 +287,7 @@ Session::~Session() {
       cudaEventDestroy(t.start);
       cudaEventDestroy(t.end);
     }
+    if (dc.green) driver_fn<decltype(&cuGreenCtxDestroy)>("cuGreenCtxDestroy")(dc.green);  // after its streams
     DevPool::get().release(dc.gpu, dc.slab, dc.slab_cap);
     for (int k = 0; k < kStage; ++k) DevPool::get().release(dc.gpu, dc.stage[k], dc.stage_cap[k]);
     cudaEventDestroy(dc.span_start);
@@ -674,11 +748,13 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   BoxKind ba, bb;
   gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
   if (job.async) {
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, sc.stream));
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, persistent_enabled(), sc.stream,
+                                   dc.sms));
   } else {
     TimedLaunch tl = timing_pair(d);
     TR_CUDA(cudaEventRecord(tl.start, sc.stream));
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, sc.stream));
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, persistent_enabled(), sc.stream,
+                                   dc.sms));
     TR_CUDA(cudaEventRecord(tl.end, sc.stream));
     dc.timed.push_back(tl);
     if (tracing_) {
@@ -985,7 +1061,11 @@ void Session::run_job(int d, Job& job) {
       while (dc.streams[s].task >= 0) ++s;
       dc.streams[s].seq = ++seq;
     }
-    if (victim < 0 && groupable(d, job, static_cast<int64_t>(tid))) {
+    // Group only while the queue still holds a round of groups for every device:
+    // in a product's tail single tasks stay stealable, so a slow (e.g. green-
+    // context) device never holds several tasks the others could have taken.
+    const bool tail = job.n_tasks - job.claimed.load() < static_cast<int64_t>(max_group_) * n_devices();
+    if (victim < 0 && !(tail && n_devices() > 1) && groupable(d, job, static_cast<int64_t>(tid))) {
       // the station's other ready tasks of the same product join this launch
       std::vector<int64_t> grp{static_cast<int64_t>(tid)};
       int64_t t0 = 0;
@@ -1306,6 +1386,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     }
   }
   last_makespan_ = sim_ ? sim_now() - sim_before : 0.0;
+
   if (job.async) {
     for (auto& dc : devs_) {
       TR_CUDA(cudaSetDevice(dc.gpu));

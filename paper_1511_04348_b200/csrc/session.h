@@ -169,7 +169,9 @@ class Session {
   };
   struct DeviceCtx {
     int id = 0, gpu = 0, width = 4, max_inflight = 2;
-    int sms = 148;  // multiprocessors of the GPU (split-K sizing)
+    int sms = 148;  // multiprocessors this device runs on (split-K sizing, persistent grids)
+    CUgreenCtx green = nullptr;  // sm_count > 0: the green context holding its SMs
+    int green_sms = 0;
     int64_t capacity = -1;
     uint16_t* slab = nullptr;
     size_t slab_cap = 0;

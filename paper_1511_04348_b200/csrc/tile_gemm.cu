@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
 template <bool A_MN, bool B_K, int PLANES, int CG>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
-                           bool persistent, cudaStream_t stream) {
+                           bool persistent, int sm_budget, cudaStream_t stream) {
   using C = Cfg<PLANES, CG>;
   auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG>;
   static std::once_flag once;
@@ -437,9 +437,9 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
   // persistent: one CTA (pair) per SM walks several output units; otherwise one unit per CTA
   int ctas = g.cta_begin[g.n_tasks];
   if (persistent) {
-    int dev = 0, sms = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = std::min(ctas, (sms / CG) * CG);
+    int dev = 0, sms = sm_budget;
+    if (sms <= 0 && cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    ctas = std::min(ctas, std::max(CG, (sms / CG) * CG));
   }
   dim3 grid(static_cast<unsigned>(ctas), 1, k_split > 1 ? k_split : 1);
   if (CG == 1) {
@@ -552,25 +552,26 @@ void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* 
 }
 
 static cudaError_t dispatch(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split, bool a_mn,
-                            bool b_kmajor, bool pair, int planes, bool persistent, cudaStream_t stream) {
+                            bool b_kmajor, bool pair, int planes, bool persistent, cudaStream_t stream,
+                            int sm_budget = 0) {
   const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (planes == 2 ? 1 : 0) | (pair ? 8 : 0);
   switch (variant) {
-    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, persistent, stream);
-    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
-    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, persistent, stream);
-    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, persistent, stream);
+    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
   }
 }
 
@@ -595,7 +596,7 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
 }
 
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
-                                   bool b_kmajor, bool persistent, cudaStream_t stream) {
+                                   bool b_kmajor, bool persistent, cudaStream_t stream, int sm_budget) {
   if (g.n_tasks < 1 || g.n_tasks > kMaxGroup) return cudaErrorInvalidValue;
   const bool pair = g.task[0].m_valid > BM && group_pairs_enabled();
   for (int t = 0; t < g.n_tasks; ++t) {
@@ -603,7 +604,7 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
     if (!args_ok(a) || a.k_split > 1 || a.planes != g.task[0].planes || (a.m_valid > BM && group_pairs_enabled()) != pair)
       return cudaErrorInvalidValue;
   }
-  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent, stream);
+  return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent, stream, sm_budget);
 }
 
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {

@@ -114,9 +114,11 @@ cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
                                    bool b_kmajor, cudaStream_t stream);
 // Same, with the persistence choice explicit (launches that run concurrently
-// with others -- the k-panel schedule's -- do better non-persistent).
+// with others -- the k-panel schedule's -- do better non-persistent) and the
+// SMs a persistent grid may fill (0: the whole GPU; a green-context device
+// passes its own SM count).
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
-                                   bool b_kmajor, bool persistent, cudaStream_t stream);
+                                   bool b_kmajor, bool persistent, cudaStream_t stream, int sm_budget = 0);
 void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b, bool grouped = false);
 // Sums the k_split partials of a split-K launch in z order into C, then applies
 // args.epilogue (STORE / ACCUMULATE) and args.post, exactly like the kernel's own

@@ -411,3 +411,60 @@ def test_host_slices_read_in_place():
     assert np.array_equal(c[100:600, 250:830], O.reference_gemm(a_v, b_v))
     assert (c[:100] == -7).all() and (c[:, :250] == -7).all() and (c[600:] == -7).all() and (c[:, 830:] == -7).all()
     rt.close()
+
+
+def test_green_context_devices_balance_load():
+    """Two logical devices on one B200 with disjoint green-context SM groups
+    (64 and 32 SMs): the product is exact on integer inputs and the dynamic
+    scheduler (queue + stations + stealing) hands the faster device about twice
+    the tasks -- the reference's inhomogeneous-devices acceptance behaviour
+    (tests/test_acceptance.py:130-141) on real hardware."""
+    from paper_1511_04348_b200 import DeviceSpec, Machine, ProximityMatrix
+
+    rng = np.random.default_rng(50)
+    n, T = 16384, 2048  # 64 tasks, each long enough (~0.8 / 1.6 ms) for the split to show
+    a = rng.integers(-4, 5, size=(n, n)).astype(np.float32)
+    b = rng.integers(-4, 5, size=(n, n)).astype(np.float32)
+    m = Machine([DeviceSpec(0, gpu=0, sms=64), DeviceSpec(1, gpu=0, sms=32)], ProximityMatrix.uniform(2),
+                dtype=np.float32)
+    rt = Runtime(m, T)
+    ad, bd = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    c = torch.empty(n, n, device="cuda")
+    rt.multiply(ad, bd, a_uid="A", b_uid="B", out=c)  # warm: tiles resident on whichever device took them
+    counts = []
+    for _ in range(3):
+        _, s = rt.multiply(ad, bd, a_uid="A", b_uid="B", out=c)
+        counts.append((s.tasks_by_device[0], s.tasks_by_device[1]))
+    ref = O.c_oracle().gemm(a[:8].astype(np.float64), b.astype(np.float64))
+    assert np.array_equal(c[:8].double().cpu().numpy(), ref)
+    fast, slow = map(sum, zip(*counts))
+    assert fast + slow == 3 * 64
+    assert 1.4 <= fast / slow <= 2.8, counts  # 64 : 32 SMs
+    rt.close()
+
+
+def test_green_context_devices_1234():
+    """Four green-context devices of 8 / 16 / 24 / 32 SMs on one GPU: tasks are
+    shared roughly 1:2:3:4 (the reference's acceptance shape, test_acceptance.py
+    :130-141, here on hardware with dynamic sharing and stealing)."""
+    from paper_1511_04348_b200 import DeviceSpec, Machine, ProximityMatrix
+
+    n, T = 16384, 2048
+    g = torch.Generator(device="cuda").manual_seed(3)
+    a = torch.randn(n, n, device="cuda", generator=g)
+    b = torch.randn(n, n, device="cuda", generator=g)
+    c = torch.empty(n, n, device="cuda")
+    m = Machine([DeviceSpec(i, gpu=0, sms=8 * (i + 1)) for i in range(4)], ProximityMatrix.uniform(4),
+                dtype=np.float32)
+    rt = Runtime(m, T)
+    rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
+    tot = np.zeros(4)
+    for _ in range(2):
+        _, s = rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
+        tot += [s.tasks_by_device[d] for d in range(4)]
+    share = tot / tot.sum()
+    assert np.all(np.abs(share - np.array([1, 2, 3, 4]) / 10) <= 0.06), share
+    rows = torch.arange(0, n, 997, device="cuda")
+    ref = a[rows].double() @ b.double()
+    assert rel(c[rows].double().cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+    rt.close()
