@@ -307,6 +307,38 @@ def bench_ooc(args, tr, torch, peaks_tf):
     return out
 
 
+def bench_inhomogeneous(tr, torch, precision):
+    """BASELINE cfg5's inhomogeneous devices on one GPU: four logical devices on
+    green contexts of 8 / 16 / 24 / 32 SMs share a N=16384 product (T=2048, 64
+    tasks) through the dynamic scheduler; the task shares should follow the SM
+    counts (1:2:3:4)."""
+    n, T = 16384, 2048
+    g = torch.Generator(device="cuda").manual_seed(5)
+    a = torch.randn(n, n, device="cuda", generator=g)
+    b = torch.randn(n, n, device="cuda", generator=g)
+    c = torch.empty(n, n, device="cuda")
+    sms = [8, 16, 24, 32]
+    m = tr.Machine([tr.DeviceSpec(i, gpu=torch.cuda.current_device(), sms=k) for i, k in enumerate(sms)],
+                   tr.ProximityMatrix.uniform(len(sms)), dtype=np.float32)
+    with tr.Runtime(m, T, precision=precision) as rt:
+        rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
+        tasks = np.zeros(len(sms))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(3):
+            _, st = rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
+            tasks += [st.tasks_by_device[d] for d in range(len(sms))]
+        e1.record()
+        torch.cuda.synchronize()
+    share = tasks / tasks.sum()
+    ideal = np.array(sms) / sum(sms)
+    return {"workload": "4 green-context devices of 8/16/24/32 SMs on one B200, N=16384 T=2048 (64 tasks)",
+            "task_share": [round(float(x), 4) for x in share], "ideal_share": [round(float(x), 4) for x in ideal],
+            "max_share_error": float(np.abs(share - ideal).max()),
+            "ms_per_product": e0.elapsed_time(e1) / 3, "tflops": 2.0 * n ** 3 / (e0.elapsed_time(e1) / 3e3) / 1e12}
+
+
 def sim_prediction_ms(tr, n, T, world, precision):
     """The reference's own scheduler (its sim engine, scheduler.py:432-464, replayed
     bit-exactly by mode="sim") fed this B200's measured rates: what the reference's
@@ -505,6 +537,15 @@ def main():
                                                     "loss_last")}
             torch.cuda.empty_cache()
 
+    # ---- inhomogeneous devices (green contexts), N=1 only
+    inhomogeneous = None
+    if not args.no_ooc and world == 1:
+        try:
+            inhomogeneous = bench_inhomogeneous(tr, torch, args.precision)
+        except Exception as exc:  # green contexts need a recent driver; report, do not fail the bench
+            inhomogeneous = {"unavailable": str(exc)[:200]}
+        torch.cuda.empty_cache()
+
     # ---- out-of-core leg (cfg4 scaled), rank 0 at N=1 only
     ooc = None
     if not args.no_ooc and world == 1:
@@ -593,6 +634,7 @@ def main():
             "e2e": e2e,
             "mlp": mlp,
             "ooc": ooc,
+            "inhomogeneous": inhomogeneous,
             "roofline": roofline,
             "cpu_baseline": cpu,
             "gpu_launches": launches,
