@@ -69,6 +69,10 @@ def parse():
     p.add_argument("--mlp-steps", type=int, default=5)
     p.add_argument("--mlp-sizes", default="784,8192,8192,8192,10")
     p.add_argument("--mlp-batch", type=int, default=8192)
+    p.add_argument("--no-wide", action="store_true", help="skip the cfg5 65536-wide MLP leg")
+    p.add_argument("--wide-sizes", default="784,65536,65536,65536")
+    p.add_argument("--wide-steps", type=int, default=2)
+    p.add_argument("--wide-cache-gib", type=float, default=24.0)
     return p.parse_args()
 
 
@@ -249,6 +253,66 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],
             "h2d_bytes_per_step": int(x.size * 4 + t.size * 4), "d2h_bytes_per_step": 8}
+
+
+def bench_mlp_wide(args, tr, torch):
+    """BASELINE cfg5 on one GPU: the 65536-wide MLP (784-65536-65536-65536, batch
+    8192, 424.7 TFLOP per step) trained with the tile cache capped below its
+    working set (the three weight matrices alone are 528 tiles = 33 GiB of
+    converted planes), so weight tiles are evicted and re-staged every step --
+    the out-of-core schedule -- while the fp32 weights, gradients and activations
+    stay in HBM.  Per step: batch H2D from pinned host, forward / MSE / backward
+    / SGD, loss D2H.  Weights are drawn on the device (GpuMLP.random)."""
+    sizes = [int(v) for v in args.wide_sizes.split(",")]
+    batch, T = args.mlp_batch, args.tile
+    machine = tr.homogeneous_machine(1, dtype=np.float32, gpus=[torch.cuda.current_device()])
+    rt = tr.Runtime(machine, T, precision=args.precision, hbm_budget_bytes=int(args.wide_cache_gib * 2**30))
+    mlp = tr.GpuMLP.random(sizes, seed=0, device=torch.cuda.current_device(), runtime=rt)
+    g = torch.Generator(device="cuda").manual_seed(1)
+    xh = tr.matrix.pinned_empty((batch, sizes[0]), np.float32)
+    th = tr.matrix.pinned_empty((batch, sizes[-1]), np.float32)
+    xh[...] = (torch.rand(xh.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
+    th[...] = (torch.rand(th.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
+    xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
+    xd = torch.empty(xh.shape, dtype=torch.float32, device="cuda")
+    td = torch.empty(th.shape, dtype=torch.float32, device="cuda")
+    losses = []
+
+    def step():
+        xd.copy_(xs, non_blocking=True)
+        td.copy_(ts, non_blocking=True)
+        losses.append(mlp.train_step(xd, td, 0.1))
+
+    # parity: the initial loss against a plain torch fp32 forward (cuBLAS SGEMM, TF32 off)
+    torch.backends.cuda.matmul.allow_tf32 = False
+    xd.copy_(xs)
+    td.copy_(ts)
+    h = xd
+    for L in mlp.layers:
+        h = torch.sigmoid(torch.addmm(L.b, h, L.w))
+    ref_loss0 = float(((h.double() - td.double()) ** 2).mean())
+    del h
+    step()  # warm-up: slab, pools
+    before = dict(mlp.cache_counts)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.wide_steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    dt = e0.elapsed_time(e1) / 1e3 / args.wide_steps
+    counts = {k: (v - before[k]) // args.wide_steps for k, v in mlp.cache_counts.items()}
+    mlp.close()
+    flops = mlp_flops(sizes, batch)
+    return {"workload": f"cfg5 MLP {'-'.join(map(str, sizes))} batch {batch}, sigmoid, MSE, SGD lr 0.1, one B200, "
+                        f"tile cache capped at {args.wide_cache_gib:g} GiB (weights' planes 33 GiB + activations)",
+            "precision": args.precision, "samples_per_s": batch / dt, "ms_per_step": dt * 1e3,
+            "tflops": flops / dt / 1e12, "algorithmic_tflop_per_step": flops / 1e12, "steps": args.wide_steps,
+            "loss": losses, "cache_per_step": counts,
+            "loss0_rel_err_vs_torch_fp32": abs(losses[0] - ref_loss0) / ref_loss0,
+            "h2d_bytes_per_step": int(xh.nbytes + th.nbytes), "d2h_bytes_per_step": 8,
+            "cpu_baseline": None}
 
 
 def bench_ooc(args, tr, torch, peaks_tf):
@@ -537,6 +601,12 @@ def main():
                                                     "loss_last")}
             torch.cuda.empty_cache()
 
+    # ---- cfg5: the 65536-wide MLP out-of-core on the tile cache, N=1 only
+    wide = None
+    if not args.no_wide and world == 1:
+        wide = bench_mlp_wide(args, tr, torch)
+        torch.cuda.empty_cache()
+
     # ---- inhomogeneous devices (green contexts), N=1 only
     inhomogeneous = None
     if not args.no_ooc and world == 1:
@@ -618,6 +688,8 @@ def main():
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": desc}
         if mlp is not None:
             mlp["cpu_baseline"] = mlp_cpu_baseline([int(v) for v in args.mlp_sizes.split(",")], args.mlp_batch)
+        if wide is not None:
+            wide["cpu_baseline"] = mlp_cpu_baseline([int(v) for v in args.wide_sizes.split(",")], args.mlp_batch)
 
     if rank == 0:
         line = {
@@ -633,6 +705,7 @@ def main():
                        "parallelism": f"task-sharded x{world}", "warm_cache": "all input tiles L1-resident"},
             "e2e": e2e,
             "mlp": mlp,
+            "mlp_wide": wide,
             "ooc": ooc,
             "inhomogeneous": inhomogeneous,
             "roofline": roofline,

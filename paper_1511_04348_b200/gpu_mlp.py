@@ -69,6 +69,9 @@ class GpuMLP:
         self.dev = torch.device("cuda", device)
         self.layers: list[DeviceLayer] = []
         for i, L in enumerate(layers):
+            if isinstance(L, DeviceLayer):  # already in HBM (GpuMLP.random): taken as is
+                self.layers.append(L)
+                continue
             w = torch.as_tensor(np.asarray(L.weights), dtype=torch.float32).to(self.dev).contiguous()
             b = None if L.bias is None else torch.as_tensor(np.asarray(L.bias), dtype=torch.float32).to(self.dev)
             self.layers.append(DeviceLayer(w, b, L.activation, getattr(L, "tag", f"layer{i}")))
@@ -89,6 +92,27 @@ class GpuMLP:
         self._loss = torch.zeros(1, dtype=torch.float64, device=self.dev)
         self._bufs: dict = {}
         self.products = 0
+        # tile-cache counters summed over every product (directory bookkeeping, exact
+        # at enqueue even when the products run stream-ordered)
+        self.cache_counts = dict.fromkeys(("l1_hits", "host_fetches", "evictions", "writebacks"), 0)
+
+    @classmethod
+    def random(cls, sizes, activation: str = "sigmoid", seed: int = 0, device: int = 0, **kw) -> "GpuMLP":
+        """Layers initialised in HBM: uniform(-1/sqrt(fan_in), 1/sqrt(fan_in)) weights
+        then bias per layer, as ``Layer.random`` with the per-layer scale (SURVEY
+        §8d), drawn by a seeded device generator -- for widths (BASELINE cfg5,
+        65536) whose host-side f64 initialisation would take minutes."""
+        import torch
+
+        dev = torch.device("cuda", device)
+        g = torch.Generator(device=dev).manual_seed(seed)
+        layers = []
+        for i in range(len(sizes) - 1):
+            s = 1.0 / float(np.sqrt(sizes[i]))
+            w = torch.empty((sizes[i], sizes[i + 1]), dtype=torch.float32, device=dev).uniform_(-s, s, generator=g)
+            b = torch.empty(sizes[i + 1], dtype=torch.float32, device=dev).uniform_(-s, s, generator=g)
+            layers.append(DeviceLayer(w, b, activation, f"layer{i}"))
+        return cls(layers, device=device, **kw)
 
     # -- helpers -----------------------------------------------------------
     def _buf(self, name, shape):
@@ -110,7 +134,9 @@ class GpuMLP:
         """
         self.rt.set_stream(self._stream(), ordered=self.stream_ordered)
         try:
-            self.rt.multiply_batch(prods)
+            cs = self.rt.multiply_batch(prods).cache
+            for k in self.cache_counts:
+                self.cache_counts[k] += getattr(cs, k)
         finally:
             self.rt.set_stream(self._stream(), ordered=False)
         self.products += len(prods)

@@ -9,7 +9,7 @@ import pytest
 import torch
 
 from oracle import tilerun_oracle as O
-from paper_1511_04348_b200 import GpuMLP, Layer, homogeneous_machine
+from paper_1511_04348_b200 import GpuMLP, Layer, Runtime, homogeneous_machine
 
 pytestmark = pytest.mark.gpu
 G = Path(__file__).resolve().parent / "golden"
@@ -61,6 +61,42 @@ def test_wide_net_against_blas_oracle():
     for (w, b), L in zip(mlp.to_host(), oracle_layers):
         assert relerr(w, L.weights) <= 1e-5 and relerr(b, L.bias) <= 1e-5
     mlp.close()
+
+
+@pytest.mark.parametrize("capacity", [0, 40])
+def test_wide_out_of_core_against_blas_oracle(capacity):
+    """BASELINE cfg5's shape scaled by 1/32 (784-2048-2048-2048, batch 1024, T=256,
+    weights drawn on the device by GpuMLP.random) with the tile cache bounded to
+    40 tiles -- below the 144 weight tiles alone, so tiles are evicted and
+    re-staged inside every step -- against the float64 oracle; the bounded run
+    must also equal the unbounded one bit for bit (eviction changes where a
+    tile comes from, never how a product is summed)."""
+    sizes = [784, 2048, 2048, 2048]
+    rt = Runtime(homogeneous_machine(1, capacity_tiles=capacity or None, dtype=np.float32), 256)
+    mlp = GpuMLP.random(sizes, seed=11, runtime=rt)
+    oracle_layers = [O.OracleLayer(w, b, "sigmoid") for w, b in mlp.to_host()]
+    g = torch.Generator(device="cuda").manual_seed(12)
+    xd = torch.rand((1024, sizes[0]), device="cuda", generator=g) * 2 - 1
+    td = torch.rand((1024, sizes[-1]), device="cuda", generator=g) * 2 - 1
+    x, t = xd.double().cpu().numpy(), td.double().cpu().numpy()
+    losses = []
+    for step in range(3):
+        losses.append(mlp.train_step(xd, td, 0.5))
+        lo = O.train_step(oracle_layers, x, t, 0.5, matmul=O.blas_matmul)
+        assert abs(losses[-1] - lo) <= 1e-5 * lo, (step, losses[-1], lo)
+    for (w, b), L in zip(mlp.to_host(), oracle_layers):
+        assert relerr(w, L.weights) <= 1e-5 and relerr(b, L.bias) <= 1e-5
+    _WIDE_RUNS[capacity] = (losses, mlp.to_host(), mlp.cache_counts["evictions"])
+    if len(_WIDE_RUNS) == 2:  # the bounded run evicts far more and computes the same bits
+        (l0, p0, e0), (l1, p1, e1) = _WIDE_RUNS[0], _WIDE_RUNS[40]
+        assert e1 > 10 * max(e0, 1), (e0, e1)
+        assert l0 == l1
+        for (w0, b0), (w1, b1) in zip(p0, p1):
+            assert np.array_equal(w0, w1) and np.array_equal(b0, b1)
+    mlp.close()
+
+
+_WIDE_RUNS: dict = {}
 
 
 def test_stream_ordered_matches_blocking():
