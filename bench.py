@@ -488,6 +488,10 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    def free_hbm():  # between legs: closed sessions' cached blocks and torch's cache
+        tr.release_cached_memory()
+        torch.cuda.empty_cache()
+
     def barrier():
         if world > 1:
             dist.barrier()
@@ -588,24 +592,24 @@ def main():
     roofline["bf16_mode"] = roofline_bf16
     rt.close()
     del rt
-    torch.cuda.empty_cache()
+    free_hbm()
 
     # ---- MLP (cfg3): the metric's second half
     mlp = None
     if not args.no_mlp:
         mlp = bench_mlp(args, tr, torch, local, barrier, max_over_ranks)
-        torch.cuda.empty_cache()
+        free_hbm()
         if args.precision == "fp32acc":  # the native BF16 mode the north star also names (tolerance 1e-2)
             m16 = bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="bf16")
             mlp["bf16_mode"] = {k: m16[k] for k in ("samples_per_s", "ms_per_step", "tflops", "loss_first",
                                                     "loss_last")}
-            torch.cuda.empty_cache()
+            free_hbm()
 
     # ---- cfg5: the 65536-wide MLP out-of-core on the tile cache, N=1 only
     wide = None
     if not args.no_wide and world == 1:
         wide = bench_mlp_wide(args, tr, torch)
-        torch.cuda.empty_cache()
+        free_hbm()
 
     # ---- inhomogeneous devices (green contexts), N=1 only
     inhomogeneous = None
@@ -614,13 +618,13 @@ def main():
             inhomogeneous = bench_inhomogeneous(tr, torch, args.precision)
         except Exception as exc:  # green contexts need a recent driver; report, do not fail the bench
             inhomogeneous = {"unavailable": str(exc)[:200]}
-        torch.cuda.empty_cache()
+        free_hbm()
 
     # ---- out-of-core leg (cfg4 scaled), rank 0 at N=1 only
     ooc = None
     if not args.no_ooc and world == 1:
         ooc = bench_ooc(args, tr, torch, peak)
-        torch.cuda.empty_cache()
+        free_hbm()
 
     # ---- e2e: reference-facing one-shot run() with pinned host numpy arrays
     e2e = None
@@ -630,7 +634,7 @@ def main():
         a_host[...] = A.cpu().numpy()
         b_host[...] = B.cpu().numpy()
         del A, B, C
-        torch.cuda.empty_cache()
+        free_hbm()
         # Under torchrun each rank computes one block of a pr x pc partition of the
         # task grid: it reads its A row panel and B column panel in place (row /
         # column slices of the pinned matrices) over its own host link.

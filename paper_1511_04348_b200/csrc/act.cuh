@@ -12,7 +12,10 @@ enum Activation : int32_t { ACT_IDENTITY = 0, ACT_SIGMOID = 1, ACT_RELU = 2 };
 
 #ifdef __CUDACC__
 __device__ __forceinline__ float act_fwd(int act, float y) {
-  if (act == ACT_SIGMOID) return 1.0f / (1.0f + __expf(-y));
+  // y clamped at -80 keeps e^-y finite (<= 5.5e34 < 2^126), the range where the
+  // fast reciprocal-based division is accurate to 2 ulp; sigmoid(-80) = 1.8e-35,
+  // so the clamp moves no result by more than that.
+  if (act == ACT_SIGMOID) return __fdividef(1.0f, 1.0f + __expf(-fmaxf(y, -80.f)));
   if (act == ACT_RELU) return y > 0.f ? y : 0.f;
   return y;
 }

@@ -1,11 +1,15 @@
 // K1 tile GEMM and K2 split/convert for sm_100a.  See tile_gemm.h for the contract.
 //
-// Kernel anatomy (one CTA per 128 x 256 output block, 352 threads):
+// Kernel anatomy (one CTA per 128 x 256 output block, 384 threads = 3 warpgroups):
 //   warp 0       TMA producer  (one elected lane; STAGES-deep smem ring, mbarrier full/empty)
 //   warp 1       MMA issuer    (one lane issues tcgen05.mma; commits free smem stages)
 //   warp 2       TMEM allocator (512 columns = two 128 x 256 fp32 partial-sum buffers)
-//   warps 3..10  epilogue      (every seg_kb k-blocks: tcgen05.ld TMEM -> fp32 registers,
+//   warp 3       idle (completes warpgroup 0, which hands registers to the epilogue)
+//   warps 4..11  epilogue      (every seg_kb k-blocks: tcgen05.ld TMEM -> fp32 registers,
 //                               round-to-nearest add; at the end: registers -> global)
+// setmaxnreg moves registers from warpgroup 0 (64 each) to the epilogue
+// warpgroups (216 each): 128 accumulators per thread plus room to keep several
+// rows of global reads (C, activations) in flight in the store phase.
 // All k-steps of a task (each a separate tile-cache slot, i.e. a different TMA
 // dim-2 coordinate) stream through the same ring; C is written exactly once.
 #include <algorithm>
@@ -30,7 +34,7 @@ constexpr int BN = 256;                   // output cols per CTA / per CTA pair
 constexpr int BK = 64;                    // bf16 elements = 128 B = one SW128 row
 constexpr int A_BYTES = BM * BK * 2;      // 16 KiB per plane
 constexpr int MN_GROUP_BYTES = 64 * BK * 2;  // one 64-wide MN-major TMA box (8 KiB)
-constexpr int EPI_WARP0 = 3;                 // warps 3..10: epilogue (2 per TMEM lane quadrant)
+constexpr int EPI_WARP0 = 4;                 // warps 4..11: epilogue (2 per TMEM lane quadrant)
 constexpr int EPI_WARPS = 8;
 constexpr int NUM_THREADS = (EPI_WARP0 + EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;             // double-buffered 128 x 256 fp32 partial sums
@@ -162,6 +166,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
+  if (warp < EPI_WARP0) {
+  ptx::setmaxnreg_dec<64>();
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both CTAs of a pair load their halves)
@@ -287,7 +293,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
       }
     }
-  } else if (warp >= EPI_WARP0) {
+  }
+  } else {
+    ptx::setmaxnreg_inc<216>();
     // ---------------- epilogue: TMEM partial sums -> fp32 registers (RNE) -> global
     const int q = warp & 3;                      // TMEM lane quadrant this warp may access
     const int half = (warp - EPI_WARP0) >> 2;    // column half of the 256-wide tile
@@ -311,12 +319,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         ptx::mbar_wait(&acc_full[buf], (seg >> 1) & 1);
         ptx::tc_fence_after();
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          uint32_t r[16];
-          ptx::tmem_ld_32x32b_x16(tlane + static_cast<uint32_t>(buf * BN + c * 16), r);
+        for (int c0 = 0; c0 < 8; c0 += 4) {  // four loads in flight per wait
+          uint32_t r[4][16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) ptx::tmem_ld_32x32b_x16(tlane + static_cast<uint32_t>(buf * BN + (c0 + c) * 16), r[c]);
           ptx::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(r[j]);
+          for (int c = 0; c < 4; ++c)
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[(c0 + c) * 16 + j] += __uint_as_float(r[c][j]);
         }
         ptx::tc_fence_before();
         __syncwarp();
@@ -352,32 +363,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
           }
           __syncwarp();
-          for (int r = 0; r < C::STAGE_ROWS && row0 + rb + r < args.m_valid; ++r) {
-            float4 v = *reinterpret_cast<const float4*>(stage + r * C::STAGE_LD + c);
-            float4* d4 = reinterpret_cast<float4*>(obase + static_cast<int64_t>(row0 + rb + r) * ldo + gcol0 + c);
-            if (acc_mode) {
-              const float4 o = *d4;
-              v.x += o.x;
-              v.y += o.y;
-              v.z += o.z;
-              v.w += o.w;
+          // Rows go out in batches of PRE: the batch's global reads (C when
+          // accumulating, the activation for act_grad) are all issued before the
+          // first use, so a warp waits one memory latency per batch, not per row.
+          constexpr int PRE = 8;
+#pragma unroll 1
+          for (int r0 = 0; r0 < C::STAGE_ROWS; r0 += PRE) {
+            // pre[]: the activation rows for act_grad, else the C rows when accumulating
+            // (both at once -- an accumulating act_grad product -- reads C inline)
+            const bool pre_aux = post == POST_ACT_GRAD;
+            float4 pre[PRE];
+#pragma unroll
+            for (int i = 0; i < PRE; ++i) {
+              const int64_t grow_i = row0 + rb + r0 + i;
+              pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (grow_i < args.m_valid) {
+                if (pre_aux) pre[i] = __ldg(reinterpret_cast<const float4*>(args.aux + grow_i * args.ldaux + gcol0 + c));
+                else if (acc_mode) pre[i] = *reinterpret_cast<const float4*>(obase + grow_i * ldo + gcol0 + c);
+              }
             }
-            if (post == POST_BIAS_ACT) {
-              v.x = act_fwd(args.act, v.x + bias4[0]);
-              v.y = act_fwd(args.act, v.y + bias4[1]);
-              v.z = act_fwd(args.act, v.z + bias4[2]);
-              v.w = act_fwd(args.act, v.w + bias4[3]);
-            } else if (post == POST_ACT_GRAD) {
-              const float* ax = args.aux + static_cast<int64_t>(row0 + rb + r) * args.ldaux + gcol0 + c;
-              v.x *= act_grad_from_out(args.act, ax[0]);
-              v.y *= act_grad_from_out(args.act, ax[1]);
-              v.z *= act_grad_from_out(args.act, ax[2]);
-              v.w *= act_grad_from_out(args.act, ax[3]);
+#pragma unroll
+            for (int i = 0; i < PRE; ++i) {
+              const int64_t grow_i = row0 + rb + r0 + i;
+              if (grow_i >= args.m_valid) break;
+              float4* d4 = reinterpret_cast<float4*>(obase + grow_i * ldo + gcol0 + c);
+              float4 v = *reinterpret_cast<const float4*>(stage + (r0 + i) * C::STAGE_LD + c);
+              if (acc_mode) {
+                const float4 o = pre_aux ? *d4 : pre[i];
+                v.x += o.x;
+                v.y += o.y;
+                v.z += o.z;
+                v.w += o.w;
+              }
+              if (post == POST_BIAS_ACT) {
+                v.x = act_fwd(args.act, v.x + bias4[0]);
+                v.y = act_fwd(args.act, v.y + bias4[1]);
+                v.z = act_fwd(args.act, v.z + bias4[2]);
+                v.w = act_fwd(args.act, v.w + bias4[3]);
+              } else if (post == POST_ACT_GRAD) {
+                v.x *= act_grad_from_out(args.act, pre[i].x);
+                v.y *= act_grad_from_out(args.act, pre[i].y);
+                v.z *= act_grad_from_out(args.act, pre[i].z);
+                v.w *= act_grad_from_out(args.act, pre[i].w);
+              }
+              *d4 = v;
+              if (args.wt)  // write-through: the converted planes of this row segment (as K2)
+                split4(args.wt + grow_i * args.wt_ld + gcol0 + c, args.wt_plane, PLANES, v);
             }
-            *d4 = v;
-            if (args.wt)  // write-through: the converted planes of this row segment (as K2)
-              split4(args.wt + static_cast<int64_t>(row0 + rb + r) * args.wt_ld + gcol0 + c, args.wt_plane,
-                     PLANES, v);
           }
           __syncwarp();
         }

@@ -662,3 +662,10 @@ def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool =
         return rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C")
     finally:
         rt.close()
+
+
+def release_cached_memory() -> None:
+    """Hand every HBM block cached by closed sessions back to CUDA (devpool.h):
+    one-shot ``run()`` calls reuse those blocks, a workload switching to very
+    different buffer sizes wants them freed first."""
+    N.call("tr_release_cached_memory")
