@@ -351,6 +351,13 @@ int tr_set_gemm_pairs(int32_t on);
  * or TR_SPLITK=<n> in the environment. */
 int tr_set_splitk(int32_t max_splits);
 
+/* CUDA-core tile GEMM (process-wide): tasks whose output tile is at most 32
+ * columns wide, or whose total contraction is at most 32, run on a CUDA-core
+ * kernel instead of a mostly padded 128 x 256 tensor-core tile (the MLP's
+ * 10-wide output layer).  Default on; 0 sends every task to the tensor cores;
+ * TR_SMALL_GEMM=0 in the environment sets the default. */
+int tr_set_small_gemm(int32_t on);
+
 /* Grouped launches (process-wide, sessions created afterwards): up to
  * `max_tasks` (1..8) ready tasks of one product from a device's reservation
  * station run as ONE tile-GEMM launch (device outputs, unchunked tasks).  Each

@@ -142,6 +142,7 @@ _PROTOS = {
     "tr_dense_gemm": [P(MatrixC), i32, P(MatrixC), i32, P(MatrixC), i32, i32, vp],
     "tr_set_gemm_pairs": [i32],
     "tr_set_splitk": [i32],
+    "tr_set_small_gemm": [i32],
     "tr_set_task_group": [i32],
     "tr_mlp_bias_act": [vp, vp, vp, i64, i64, i32, vp],
     "tr_mlp_act_grad": [vp, vp, vp, vp, i64, i32, vp],

@@ -487,4 +487,8 @@ int tr_set_splitk(int32_t max_splits) {
   });
 }
 
+int tr_set_small_gemm(int32_t on) {
+  return guarded([&] { tr::set_small_gemm(on != 0); });
+}
+
 }  // extern "C"

@@ -629,11 +629,31 @@ void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
   for (int k = 0; k < args.n_ksteps; ++k) total_kb += (args.k_len[k] + 63) / 64;
   const int64_t ctas = ((args.m_valid + 127) / 128) * static_cast<int64_t>((args.n_valid + 255) / 256);
   const int s = split_factor(ctas, total_kb, devs_[d].sms);
-  if (s < 2) return;
-  const int64_t ws_ld = (args.n_valid + 255) / 256 * 256;
+  if (s >= 2) use_workspace(d, sc, args, s, (args.n_valid + 255) / 256 * 256);
+}
+
+// The CUDA-core kernel's split: ~4 CTAs per SM for a narrow tile's long k.
+void Session::plan_split_small(int d, StreamCtx& sc, GemmArgs& args) {
+  args.k_split = 1;
+  const int s = small_gemm_split(args, static_cast<int>(devs_[d].sms));
+  if (s >= 2) use_workspace(d, sc, args, s, (args.n_valid + 15) / 16 * 16);
+}
+
+// Points args at stream s's split-K workspace (grown on demand) for `splits`
+// partials of ws_ld-wide rows; leaves the launch unsplit when HBM is short.
+void Session::use_workspace(int d, StreamCtx& sc, GemmArgs& args, int splits, int64_t ws_ld) {
   const int64_t zstride = static_cast<int64_t>(args.m_valid) * ws_ld;
-  const size_t need = static_cast<size_t>(s * zstride) * sizeof(float);
-  if (need > sc.ws_cap) {
+  float* ws = workspace(d, sc, static_cast<size_t>(splits * zstride) * sizeof(float));
+  if (!ws) return;  // no room: run unsplit
+  args.k_split = splits;
+  args.ws = ws;
+  args.ws_ld = ws_ld;
+  args.ws_zstride = zstride;
+}
+
+// Stream s's split-K workspace, grown to >= bytes (nullptr when HBM is short).
+float* Session::workspace(int d, StreamCtx& sc, size_t bytes) {
+  if (bytes > sc.ws_cap) {
     DeviceCtx& dc = devs_[d];
     if (sc.ws) {
       TR_CUDA(cudaStreamSynchronize(sc.stream));  // the old workspace may still be read
@@ -643,17 +663,45 @@ void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
     }
     void* p = nullptr;
     size_t cap = 0;
-    if (DevPool::get().alloc(dc.gpu, need, &p, &cap) != cudaSuccess) {
+    if (DevPool::get().alloc(dc.gpu, bytes, &p, &cap) != cudaSuccess) {
       cudaGetLastError();
-      return;  // no room: run unsplit
+      return nullptr;
     }
     sc.ws = static_cast<float*>(p);
     sc.ws_cap = cap;
   }
-  args.k_split = s;
-  args.ws = sc.ws;
-  args.ws_ld = ws_ld;
-  args.ws_zstride = zstride;
+  return sc.ws;
+}
+
+// Split-K for a grouped launch: the k-share count that minimises the
+// persistent grid's wave count per unit of work -- tiles * s units over the
+// device's CTA (pair) slots, each 1/s of the k-loop -- when that beats the
+// unsplit launch by 10% (784-row tiles: 2 tasks x 112 CTAs on 148 SMs).
+int Session::group_split(int d, const GemmGroup& grp, bool pair) const {
+  const int smax = splitk_max();
+  if (smax < 2) return 1;
+  const int cg = pair ? 2 : 1;
+  int64_t tiles = 0;
+  int kb = 1 << 30;
+  for (int t = 0; t < grp.n_tasks; ++t) {
+    const GemmArgs& a = grp.task[t];
+    tiles += ceil_div(a.m_valid, 128 * cg) * ceil_div(a.n_valid, 256);
+    int k = 0;
+    for (int q = 0; q < a.n_ksteps; ++q) k += (a.k_len[q] + 63) / 64;
+    kb = std::min(kb, k);
+  }
+  const int64_t slots = std::max<int64_t>(1, devs_[d].sms / cg);
+  const double base = static_cast<double>(ceil_div(tiles, slots));
+  double best = base;
+  int best_s = 1;
+  for (int sp = 2; sp <= smax && kb / sp >= 8; ++sp) {
+    const double cost = static_cast<double>(ceil_div(tiles * sp, slots)) / sp;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_s = sp;
+    }
+  }
+  return best <= 0.9 * base ? best_s : 1;
 }
 
 // ---------------------------------------------------------------- grouped issue
@@ -683,8 +731,9 @@ bool Session::groupable(int d, Job& job, int64_t gtid) {
   const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
   int total_kb = 0;
   for (int64_t k = 0; k < p.k_steps; ++k) total_kb += static_cast<int>((std::min(T, p.K - k * T) + 63) / 64);
-  const int64_t ctas = ((mt + 127) / 128) * ((nt + 255) / 256);
-  return split_factor(ctas, total_kb, devs_[d].sms) < 2;  // launches that split along K run alone
+  (void)mt;
+  (void)total_kb;
+  return !(small_gemm_enabled() && (nt <= kSmallMaxN || p.K <= kSmallMaxK));  // else the CUDA-core kernel
 }
 
 // _execute_task for several tasks at once: each task's directory sequence is the
@@ -696,6 +745,7 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   const int64_t T = tile_;
   GemmGroup grp;
   grp.n_tasks = static_cast<int32_t>(gtids.size());
+  grp.k_split = 1;
   std::vector<TileKey> used;
   std::vector<int32_t> used_phys;
   std::vector<int32_t> wt_phys;  // slots the launch writes through
@@ -742,19 +792,47 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
-    const int32_t wt = write_through(d, s, p, i, j, args);
+  }
+  // split-K across the group (k-shares folded into the persistent unit walk);
+  // the partials of task t go to its own region of the stream's workspace
+  const int split = group_split(d, grp, group_uses_pairs(grp.task[0].m_valid));
+  if (split > 1) {
+    size_t total = 0;
+    for (int t = 0; t < grp.n_tasks; ++t)
+      total += static_cast<size_t>(split) * grp.task[t].m_valid * ((grp.task[t].n_valid + 255) / 256 * 256);
+    if (float* ws = workspace(d, sc, total * sizeof(float))) {
+      grp.k_split = split;
+      for (int t = 0; t < grp.n_tasks; ++t) {
+        GemmArgs& a = grp.task[t];
+        a.k_split = split;
+        a.ws = ws;
+        a.ws_ld = (a.n_valid + 255) / 256 * 256;
+        a.ws_zstride = static_cast<int64_t>(a.m_valid) * a.ws_ld;
+        ws += split * a.ws_zstride;
+      }
+    }
+  }
+  for (size_t q = 0; q < gtids.size(); ++q) {  // write-through: unsplit full tiles only
+    int64_t tid = 0;
+    const Product& p = job.prod_of(gtids[q], &tid);
+    const int32_t wt = write_through(d, s, p, tid / p.grid_cols, tid % p.grid_cols, grp.task[q]);
     if (wt >= 0) wt_phys.push_back(wt);
   }
   BoxKind ba, bb;
   gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
-  if (job.async) {
+  auto launch = [&] {
     TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, persistent_enabled(), sc.stream,
                                    dc.sms));
+    if (grp.k_split > 1)
+      for (int t = 0; t < grp.n_tasks; ++t) TR_CUDA(launch_splitk_reduce(grp.task[t], sc.stream));
+    job.launches.fetch_add(grp.k_split > 1 ? grp.n_tasks : 0);
+  };
+  if (job.async) {
+    launch();
   } else {
     TimedLaunch tl = timing_pair(d);
     TR_CUDA(cudaEventRecord(tl.start, sc.stream));
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, persistent_enabled(), sc.stream,
-                                   dc.sms));
+    launch();
     TR_CUDA(cudaEventRecord(tl.end, sc.stream));
     dc.timed.push_back(tl);
     if (tracing_) {
@@ -892,20 +970,29 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
-    if (!dryrun_) plan_split_k(d, *scp, args);
+    const bool small = !dryrun_ && small_gemm_enabled() && small_gemm_eligible(args);
+    if (!dryrun_) {
+      if (small) plan_split_small(d, *scp, args);
+      else plan_split_k(d, *scp, args);
+    }
     const int32_t wt = (!dryrun_ && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
-    if (!dryrun_ && job.async) {
+    auto launch = [&] {
+      if (small) {
+        TR_CUDA(launch_small_gemm(dc.slab, ld_, plane_elems_, args, p.ta, p.tb, scp->stream));
+        return;
+      }
       BoxKind ba, bb;
       gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
       TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+    };
+    if (!dryrun_ && job.async) {
+      launch();
       if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
       job.launches.fetch_add(args.k_split > 1 ? 2 : 1);
     } else if (!dryrun_) {
-      BoxKind ba, bb;
-      gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
       TimedLaunch tl = timing_pair(d);
       TR_CUDA(cudaEventRecord(tl.start, scp->stream));
-      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+      launch();
       if (args.k_split > 1) {
         TR_CUDA(launch_splitk_reduce(args, scp->stream));
         job.launches.fetch_add(1);
@@ -1070,12 +1157,12 @@ void Session::run_job(int d, Job& job) {
       std::vector<int64_t> grp{static_cast<int64_t>(tid)};
       int64_t t0 = 0;
       const Product* p0 = &job.prod_of(grp[0], &t0);
-      const bool tall0 = std::min<int64_t>(tile_, p0->M - (t0 / p0->grid_cols) * tile_) > 128;
+      const bool tall0 = group_uses_pairs(static_cast<int>(std::min<int64_t>(tile_, p0->M - (t0 / p0->grid_cols) * tile_)));
       uint64_t more;
       while (static_cast<int>(grp.size()) < std::min(max_group_, kMaxGroup) && st.peek_front(&more)) {
         int64_t t1 = 0;
         const Product* p1 = &job.prod_of(static_cast<int64_t>(more), &t1);
-        const bool tall1 = std::min<int64_t>(tile_, p1->M - (t1 / p1->grid_cols) * tile_) > 128;
+        const bool tall1 = group_uses_pairs(static_cast<int>(std::min<int64_t>(tile_, p1->M - (t1 / p1->grid_cols) * tile_)));
         if (p1 != p0 || tall1 != tall0 || !groupable(d, job, static_cast<int64_t>(more))) break;
         if (!st.pop_for_run(&more)) break;
         grp.push_back(static_cast<int64_t>(more));

@@ -206,6 +206,10 @@ class Session {
   void sim_task(int d, Job& job, int64_t gtid, double t);
   double xfer_cost(int src, int dst, int64_t nbytes) const;
   void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
+  void plan_split_small(int d, StreamCtx& sc, GemmArgs& args);
+  void use_workspace(int d, StreamCtx& sc, GemmArgs& args, int splits, int64_t ws_ld);
+  float* workspace(int d, StreamCtx& sc, size_t bytes);
+  int group_split(int d, const GemmGroup& grp, bool pair) const;
   // write-through: reserve the cache slot for output tile (i, j) of p and point
   // args at its planes; returns the physical slot (-1: not written through)
   int32_t write_through(int d, int s, const Product& p, int64_t i, int64_t j, GemmArgs& args);

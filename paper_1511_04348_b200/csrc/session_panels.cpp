@@ -39,6 +39,7 @@ bool Session::panels_apply(const Job& job) const {
   const Product& p = job.prods[0];
   if (p.a.location != TR_LOC_HOST || p.b.location != TR_LOC_HOST || p.c.location != TR_LOC_HOST) return false;
   if (p.post != POST_NONE || p.k_steps < 2 || p.k_steps > kMaxKSteps) return false;
+  if (small_gemm_enabled() && (tile_ <= kSmallMaxN || p.N <= kSmallMaxN)) return false;  // CUDA-core tasks
   if (order_ == -1 && job.n_tasks < 16) return false;  // small products gain nothing
   // in-core, or out-of-core with the future-aware directory (blocks, see run_panels)
   const int64_t T = tile_;
@@ -104,7 +105,7 @@ bool Session::run_panels(Job& job) {
   if (const char* e = getenv("TR_PANEL_GROUP")) gb = std::max(1, std::min(G, atoi(e)));
   auto a_key = [&](int64_t i, int64_t k) { return p.ta ? std::make_pair(k, i) : std::make_pair(i, k); };
   auto b_key = [&](int64_t k, int64_t j) { return p.tb ? std::make_pair(j, k) : std::make_pair(k, j); };
-  auto tall = [&](size_t q) { return std::min(T, p.M - ti[q] * T) > 128; };
+  auto tall = [&](size_t q) { return group_uses_pairs(static_cast<int>(std::min(T, p.M - ti[q] * T))); };
   struct Unit {
     size_t q;
     int64_t k0, k1;
@@ -154,6 +155,7 @@ bool Session::run_panels(Job& job) {
       StreamCtx& sc = dc.streams[s];
       GemmGroup grp;
       grp.n_tasks = static_cast<int32_t>(e - b);
+      grp.k_split = 1;
       std::vector<TileKey> used;
       std::vector<int32_t> used_phys;
       for (size_t x = b; x < e; ++x) {

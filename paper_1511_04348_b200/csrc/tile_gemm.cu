@@ -73,37 +73,49 @@ struct Cfg {
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
 };
 
-// Output unit u of a group launch -> (task, row/column origin).  A unit is one
-// 128 x 256 CTA tile (CG = 1) or one 256 x 256 pair tile (CG = 2).
+// Output unit u of a group launch -> (task, row/column origin, split-K share).
+// A unit is one 128 x 256 CTA tile (CG = 1) or one 256 x 256 pair tile (CG = 2)
+// over the k-blocks of share z of nz.  Grouped launches fold split-K into the
+// unit index (grp.k_split shares of every tile: u = z * tiles + tile), so a
+// persistent grid balances them like any other units; single-task launches
+// split along the grid's z dimension.
 struct Unit {
-  int t, m0, n0;
+  int t, m0, n0, z, nz;
 };
 template <int CG>
 __device__ __forceinline__ Unit unit_of(const GemmGroup& grp, int u, uint32_t rank) {
-  const int cta = u * CG;  // the unit's first CTA index in the flattened (non-persistent) grid
+  Unit r;
+  const int tiles = grp.cta_begin[grp.n_tasks] / CG;
+  if (grp.k_split > 1) {
+    r.z = u / tiles;
+    r.nz = grp.k_split;
+    u -= r.z * tiles;
+  } else {
+    r.z = static_cast<int>(blockIdx.z);
+    r.nz = static_cast<int>(gridDim.z);
+  }
+  const int cta = u * CG;  // the tile's first CTA index in the flattened (non-persistent) grid
   int t = 0;
   while (t + 1 < grp.n_tasks && cta >= grp.cta_begin[t + 1]) ++t;
   const int local = cta - grp.cta_begin[t];
   const int m_cta = local % grp.m_blocks[t];
-  Unit r;
   r.t = t;
   r.m0 = (m_cta / CG) * (BM * CG) + static_cast<int>(rank) * BM;
   r.n0 = (local / grp.m_blocks[t]) * BN;
   return r;
 }
 
-// k-blocks of a task and this CTA's split-K share of them
+// k-blocks of a task and share z of nz of them
 struct KRange {
   int total, lo, hi;
 };
-__device__ __forceinline__ KRange krange(const GemmArgs& args) {
+__device__ __forceinline__ KRange krange(const GemmArgs& args, int z, int nz) {
   int total_kb = 0;
   for (int ks = 0; ks < args.n_ksteps; ++ks) total_kb += (args.k_len[ks] + BK - 1) / BK;
-  const int n_split = static_cast<int>(gridDim.z);
   KRange r;
   r.total = total_kb;
-  r.lo = static_cast<int>((static_cast<int64_t>(blockIdx.z) * total_kb) / n_split);
-  r.hi = static_cast<int>((static_cast<int64_t>(blockIdx.z + 1) * total_kb) / n_split);
+  r.lo = static_cast<int>((static_cast<int64_t>(z) * total_kb) / nz);
+  r.hi = static_cast<int>((static_cast<int64_t>(z + 1) * total_kb) / nz);
   return r;
 }
 
@@ -136,7 +148,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   const int lane = threadIdx.x & 31;
   const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;  // 0 = leader of the pair
   const bool leader = rank == 0;
-  const int n_units = grp.cta_begin[grp.n_tasks] / CG;
+  const int n_units = (grp.cta_begin[grp.n_tasks] / CG) * (grp.k_split > 1 ? grp.k_split : 1);
   const int first_unit = static_cast<int>(blockIdx.x) / CG;
   const int unit_stride = static_cast<int>(gridDim.x) / CG;
 
@@ -178,7 +190,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const Unit un = unit_of<CG>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
         const int nb0 = un.n0 + static_cast<int>(rank) * BN_LOCAL;  // B columns this CTA stages
-        const KRange kr = krange(args);
+        const KRange kr = krange(args, un.z, un.nz);
         int g = 0;  // global k-block index
         for (int ks = 0; ks < args.n_ksteps; ++ks) {
           const int nkb = (args.k_len[ks] + BK - 1) / BK;
@@ -232,7 +244,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       for (int u = first_unit; u < n_units; u += unit_stride) {
         const Unit un = unit_of<CG>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
-        const KRange kr = krange(args);
+        const KRange kr = krange(args, un.z, un.nz);
         const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(kr.hi - kr.lo, 1);
         int kb_in_seg = 0;
         uint32_t tmem_d = tmem_base;
@@ -307,7 +319,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     for (int u = first_unit; u < n_units; u += unit_stride) {
       const Unit un = unit_of<CG>(grp, u, rank);
       const GemmArgs& args = grp.task[un.t];
-      const KRange kr = krange(args);
+      const KRange kr = krange(args, un.z, un.nz);
       const int my_kb = kr.hi - kr.lo;
       const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(my_kb, 1);
       const int n_seg = (my_kb + seg_kb - 1) / seg_kb;
@@ -338,8 +350,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
       const int grow = un.m0 + row;
       const int gcol0 = un.n0 + half * 128;
-      const bool part = gridDim.z > 1;  // split-K: raw fp32 partials into the workspace
-      float* obase = part ? args.ws + blockIdx.z * args.ws_zstride : static_cast<float*>(args.c);
+      const bool part = un.nz > 1;  // split-K: raw fp32 partials into the workspace
+      float* obase = part ? args.ws + un.z * args.ws_zstride : static_cast<float*>(args.c);
       const int64_t ldo = part ? args.ws_ld : args.ldc;
       if ((part || !args.c_f64) && gcol0 + 128 <= args.n_valid && (ldo & 3) == 0 &&
           (reinterpret_cast<uintptr_t>(obase) & 15) == 0) {
@@ -467,13 +479,13 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
     g.cta_begin[t + 1] = g.cta_begin[t] + g.m_blocks[t] * ((a.n_valid + BN - 1) / BN);
   }
   // persistent: one CTA (pair) per SM walks several output units; otherwise one unit per CTA
-  int ctas = g.cta_begin[g.n_tasks];
+  int ctas = g.cta_begin[g.n_tasks] * (g.k_split > 1 ? g.k_split : 1);
   if (persistent) {
     int dev = 0, sms = sm_budget;
     if (sms <= 0 && cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     ctas = std::min(ctas, std::max(CG, (sms / CG) * CG));
   }
-  dim3 grid(static_cast<unsigned>(ctas), 1, k_split > 1 ? k_split : 1);
+  dim3 grid(static_cast<unsigned>(ctas), 1, (k_split > 1 && g.k_split <= 1) ? k_split : 1);
   if (CG == 1) {
     kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, g);
     return cudaGetLastError();
@@ -577,8 +589,14 @@ int make_plane_tmap(CUtensorMap* out, const PlaneGeom& g, BoxKind box) {
   return r == CUDA_SUCCESS ? 0 : static_cast<int>(r);
 }
 
+bool group_uses_pairs(int m_valid) {
+  // pairs (256-row units) unless they pad more rows than 128-row CTAs would
+  const int r = m_valid % (2 * BM);
+  return m_valid > BM && group_pairs_enabled() && (r == 0 || r > BM);
+}
+
 void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b, bool grouped) {
-  const bool pair = m_valid > BM && (grouped ? group_pairs_enabled() : gemm_pairs_enabled());
+  const bool pair = grouped ? group_uses_pairs(m_valid) : (m_valid > BM && gemm_pairs_enabled());
   *box_a = a_mn ? BOX_MN64 : BOX_K128;
   *box_b = b_kmajor ? (pair ? BOX_K128 : BOX_K256) : BOX_MN64;
 }
@@ -618,6 +636,7 @@ cudaError_t launch_tile_gemm(const CUtensorMap& tmA, const CUtensorMap& tmB, con
   const bool pair = args.m_valid > BM && gemm_pairs_enabled();
   GemmGroup g;
   g.n_tasks = 1;
+  g.k_split = 1;  // split along the grid's z dimension instead
   g.task[0] = args;
   return dispatch(tmA, tmB, g, args.k_split, a_mn, b_kmajor, pair, args.planes, /*persistent=*/false, stream);
 }
@@ -630,10 +649,12 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
                                    bool b_kmajor, bool persistent, cudaStream_t stream, int sm_budget) {
   if (g.n_tasks < 1 || g.n_tasks > kMaxGroup) return cudaErrorInvalidValue;
-  const bool pair = g.task[0].m_valid > BM && group_pairs_enabled();
+  const bool pair = group_uses_pairs(g.task[0].m_valid);
+  const int split = g.k_split > 1 ? g.k_split : 1;
   for (int t = 0; t < g.n_tasks; ++t) {
     const GemmArgs& a = g.task[t];
-    if (!args_ok(a) || a.k_split > 1 || a.planes != g.task[0].planes || (a.m_valid > BM && group_pairs_enabled()) != pair)
+    if (!args_ok(a) || (a.k_split > 1 ? a.k_split : 1) != split || (split > 1 && !a.ws) ||
+        a.planes != g.task[0].planes || group_uses_pairs(a.m_valid) != pair)
       return cudaErrorInvalidValue;
   }
   return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent, stream, sm_budget);

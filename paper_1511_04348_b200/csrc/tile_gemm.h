@@ -76,6 +76,7 @@ struct GemmArgs {
 constexpr int kMaxGroup = 8;
 struct GemmGroup {
   int32_t n_tasks;
+  int32_t k_split;  // > 1: every task split into k_split k-shares (units z * tiles + tile; partials to task.ws)
   int32_t cta_begin[kMaxGroup + 1];
   int32_t m_blocks[kMaxGroup];
   GemmArgs task[kMaxGroup];
@@ -136,11 +137,34 @@ void set_gemm_pairs(bool on);
 // (TR_GROUP_PAIRS=0 or set_group_pairs(false) selects single CTAs).
 bool group_pairs_enabled();
 void set_group_pairs(bool on);
+// Whether a grouped launch of tiles with m_valid rows runs CTA pairs: enabled,
+// taller than 128 rows, and no more row padding than single CTAs (784 rows:
+// 7 x 128 singles, not 4 x 256 pairs).  Every task of a group must agree.
+bool group_uses_pairs(int m_valid);
 // Grouped launches are persistent by default (one CTA / pair per SM walking
 // several output units, the store of one tile overlapping the next tile's
 // k-loop); TR_PERSISTENT=0 or set_persistent(false) launches one CTA per unit.
 bool persistent_enabled();
 void set_persistent(bool on);
+
+// K1s (small_gemm.cu): the task GEMM on CUDA cores for tiles a 128 x 256
+// tensor-core tile would mostly pad -- outputs at most kSmallMaxN columns wide
+// (the MLP's 10-wide output layer) or a total contraction of at most kSmallMaxK
+// (its dX = dY W^T).  Same operands (tile-cache planes at slab + z * plane_stride,
+// row stride ld; hi + lo re-assembled in fp32), same GemmArgs contract
+// (epilogue, post-op, write-through, split-K partials into args.ws for
+// launch_splitk_reduce), fp32 FMA in ascending k.
+constexpr int kSmallMaxN = 32;
+constexpr int kSmallMaxK = 32;
+bool small_gemm_eligible(const GemmArgs& args);
+// split-K factor for a narrow task on `sms` SMs (1: no split)
+int small_gemm_split(const GemmArgs& args, int sms);
+cudaError_t launch_small_gemm(const uint16_t* slab, int64_t ld, int64_t plane_stride, const GemmArgs& args,
+                              bool a_mn, bool b_kmajor, cudaStream_t stream);
+// Process-wide switch (default on; TR_SMALL_GEMM=0 or set_small_gemm(false)
+// sends every task to the tensor-core kernel).
+bool small_gemm_enabled();
+void set_small_gemm(bool on);
 
 // K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
 // into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything

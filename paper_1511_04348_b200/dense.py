@@ -37,6 +37,11 @@ def set_splitk(max_splits: int) -> None:
     N.call("tr_set_splitk", int(max_splits))
 
 
+def set_small_gemm(on: bool) -> None:
+    """CUDA-core kernel for tasks with output tiles <= 32 columns or contractions <= 32 (default on)."""
+    N.call("tr_set_small_gemm", int(bool(on)))
+
+
 def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,
                stream=None):
     """``out (+)= op(a) @ op(b)`` for torch CUDA tensors (float32/float64).
