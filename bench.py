@@ -193,6 +193,44 @@ def mlp_flops(sizes, batch):
     return sum(3 * 2.0 * batch * sizes[i] * sizes[i + 1] for i in range(len(sizes) - 1))
 
 
+def train_steps(torch, mlp, xs, ts, steps, lr=0.1):
+    """``steps`` SGD steps of ``mlp`` on the pinned batch (xs, ts); returns the
+    losses.  Every step copies its batch H2D and reads its loss back D2H, both
+    overlapped with compute the way a training loop would: the next batch is
+    copied on a side stream into the other of two device buffers while the
+    current step runs, and step i's loss is read after step i+1 is enqueued."""
+    cur = torch.cuda.current_stream()
+    side = torch.cuda.Stream()
+    bufs = [(torch.empty(xs.shape, dtype=torch.float32, device="cuda"),
+             torch.empty(ts.shape, dtype=torch.float32, device="cuda")) for _ in range(2)]
+    ready, free = [None, None], [None, None]
+
+    def prefetch(k):
+        with torch.cuda.stream(side):
+            if free[k] is not None:
+                side.wait_event(free[k])  # the step that last read buffer k has run
+            bufs[k][0].copy_(xs, non_blocking=True)
+            bufs[k][1].copy_(ts, non_blocking=True)
+            ready[k] = torch.cuda.Event()
+            ready[k].record(side)
+
+    losses, pending = [], None
+    prefetch(0)
+    for i in range(steps):
+        k = i % 2
+        cur.wait_event(ready[k])
+        if i + 1 < steps:
+            prefetch(1 - k)
+        nxt = mlp.train_step_async(bufs[k][0], bufs[k][1], lr)
+        free[k] = torch.cuda.Event()
+        free[k].record(cur)
+        if pending is not None:
+            losses.append(pending.result())
+        pending = nxt
+    losses.append(pending.result())
+    return losses
+
+
 def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32acc"):
     """cfg3: MLP training through the tiled runtime, device-resident (GpuMLP).
 
@@ -222,23 +260,13 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
     th[...] = t
     mlp = tr.GpuMLP(layers, tile_size=args.tile, device=local, precision=precision,
                     process_group=dist.group.WORLD if world > 1 else None)
-    dev = torch.device("cuda", local)
-    xd = torch.empty(x.shape, dtype=torch.float32, device=dev)
-    td = torch.empty(t.shape, dtype=torch.float32, device=dev)
     xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
-    losses = []
-    for _ in range(2):  # warm-up: slab sizing, kernel attributes
-        xd.copy_(xs, non_blocking=True)
-        td.copy_(ts, non_blocking=True)
-        losses.append(mlp.train_step(xd, td, 0.1))
+    losses = train_steps(torch, mlp, xs, ts, 2)  # warm-up: slab sizing, kernel attributes
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(args.mlp_steps):
-        xd.copy_(xs, non_blocking=True)
-        td.copy_(ts, non_blocking=True)
-        losses.append(mlp.train_step(xd, td, 0.1))
+    losses += train_steps(torch, mlp, xs, ts, args.mlp_steps)
     e1.record()
     torch.cuda.synchronize()
     dt = max_over_ranks(e0.elapsed_time(e1) / 1e3 / args.mlp_steps)
@@ -274,31 +302,20 @@ def bench_mlp_wide(args, tr, torch):
     xh[...] = (torch.rand(xh.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
     th[...] = (torch.rand(th.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
     xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
-    xd = torch.empty(xh.shape, dtype=torch.float32, device="cuda")
-    td = torch.empty(th.shape, dtype=torch.float32, device="cuda")
-    losses = []
-
-    def step():
-        xd.copy_(xs, non_blocking=True)
-        td.copy_(ts, non_blocking=True)
-        losses.append(mlp.train_step(xd, td, 0.1))
-
+    xd, td = xs.cuda(), ts.cuda()
     # parity: the initial loss against a plain torch fp32 forward (cuBLAS SGEMM, TF32 off)
     torch.backends.cuda.matmul.allow_tf32 = False
-    xd.copy_(xs)
-    td.copy_(ts)
     h = xd
     for L in mlp.layers:
         h = torch.sigmoid(torch.addmm(L.b, h, L.w))
     ref_loss0 = float(((h.double() - td.double()) ** 2).mean())
-    del h
-    step()  # warm-up: slab, pools
+    del h, xd, td
+    losses = train_steps(torch, mlp, xs, ts, 1)  # warm-up: slab, pools
     before = dict(mlp.cache_counts)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     e0.record()
-    for _ in range(args.wide_steps):
-        step()
+    losses += train_steps(torch, mlp, xs, ts, args.wide_steps)
     e1.record()
     torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) / 1e3 / args.wide_steps

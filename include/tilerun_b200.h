@@ -250,6 +250,9 @@ typedef struct {
                           tiles straight into the tile cache (float32 device outputs, full tiles;
                           uncounted until requested, like a fetch-ahead), saving the later
                           split/convert pass.  0 = off. */
+  int32_t axpy;        /* != 0: C += alpha * A.B (float32 device C, post-op NONE) -- e.g. the fused SGD
+                          update W += (-lr) X^T dY of ann.py:247 without a gradient buffer */
+  float alpha;
 } tr_product;
 int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_report* report);
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,

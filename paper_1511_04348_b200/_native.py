@@ -73,7 +73,8 @@ class StealEventC(C.Structure):
 class ProductC(C.Structure):
     _fields_ = [("a", MatrixC), ("a_uid", u64), ("transpose_a", i32), ("b", MatrixC), ("b_uid", u64),
                 ("transpose_b", i32), ("c", MatrixC), ("c_uid", u64), ("post", i32), ("act", i32),
-                ("bias", C.c_void_p), ("aux", C.c_void_p), ("ldaux", i64), ("cache_as", u64)]
+                ("bias", C.c_void_p), ("aux", C.c_void_p), ("ldaux", i64), ("cache_as", u64),
+                ("axpy", i32), ("alpha", C.c_float)]
 
 
 TR_POST_NONE, TR_POST_BIAS_ACT, TR_POST_ACT_GRAD = 0, 1, 2

@@ -331,6 +331,8 @@ int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_
       p.aux = q.aux;
       p.ldaux = q.ldaux;
       p.cache_as = q.cache_as;
+      p.axpy = q.axpy != 0;
+      p.alpha = q.alpha;
     }
     s->s->run_products(std::move(v), 0, 1, report);
   });

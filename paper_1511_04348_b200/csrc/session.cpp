@@ -769,7 +769,9 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     args.c = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * p.c.esize();
     args.ldc = p.c.ld;
     args.c_f64 = p.c.dtype == TR_DTYPE_F64;
-    args.epilogue = EPI_STORE;
+    args.epilogue = p.axpy ? EPI_ACCUMULATE : EPI_STORE;
+    args.scaled = p.axpy;
+    args.alpha = p.alpha;
     args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
     args.k_split = 1;
     if (p.post != POST_NONE) {
@@ -945,7 +947,9 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     args.c = cptr;
     args.ldc = ldc;
     args.c_f64 = p.c.dtype == TR_DTYPE_F64;
-    args.epilogue = k0 == 0 ? EPI_STORE : EPI_ACCUMULATE;
+    args.epilogue = (k0 == 0 && !p.axpy) ? EPI_STORE : EPI_ACCUMULATE;
+    args.scaled = p.axpy;
+    args.alpha = p.alpha;
     args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
     if (p.post != POST_NONE && k0 + kc == ks) {  // fused post-op on the final chunk only
       args.post = p.post;
@@ -1315,6 +1319,8 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     if (p.post != POST_NONE && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
       fail(TR_ERR_VALUE, "fused epilogues need a float32 device output");
     if (p.post == POST_ACT_GRAD && !p.aux) fail(TR_ERR_VALUE, "POST_ACT_GRAD needs the activation (aux) matrix");
+    if (p.axpy && (p.post != POST_NONE || c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
+      fail(TR_ERR_VALUE, "axpy products accumulate into a float32 device matrix, without a post-op");
     p.grid_rows = ceil_div(p.M, T);
     p.grid_cols = ceil_div(p.N, T);
     p.k_steps = ceil_div(p.K, T);

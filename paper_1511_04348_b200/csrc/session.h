@@ -61,6 +61,8 @@ struct Product {
   const float* aux = nullptr;
   int64_t ldaux = 0;
   uint64_t cache_as = 0;  // write-through: the output's tiles enter the cache under this uid
+  bool axpy = false;      // C += alpha * A.B (every k-chunk accumulates)
+  float alpha = 1.f;
 };
 
 struct Job {

@@ -400,6 +400,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
               if (grow_i >= args.m_valid) break;
               float4* d4 = reinterpret_cast<float4*>(obase + grow_i * ldo + gcol0 + c);
               float4 v = *reinterpret_cast<const float4*>(stage + (r0 + i) * C::STAGE_LD + c);
+              if (args.scaled && !part) v = make_float4(args.alpha * v.x, args.alpha * v.y, args.alpha * v.z, args.alpha * v.w);
               if (acc_mode) {
                 const float4 o = pre_aux ? *d4 : pre[i];
                 v.x += o.x;
@@ -429,6 +430,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         const int ncols = min(128, args.n_valid - gcol0);
         const int64_t off = static_cast<int64_t>(grow) * args.ldc + gcol0;
         const bool acc_mode = !part && args.epilogue == EPI_ACCUMULATE;
+        if (args.scaled && !part)
+#pragma unroll
+          for (int j = 0; j < 128; ++j) acc[j] *= args.alpha;
         if (args.c_f64 && !part) {
           double* dst = static_cast<double*>(args.c) + off;
 #pragma unroll
@@ -543,6 +547,7 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmArgs args) {
     const float* w = args.ws + r * args.ws_ld + c;
     float v = w[0];
     for (int z = 1; z < args.k_split; ++z) v += w[z * args.ws_zstride];
+    if (args.scaled) v *= args.alpha;
     const int64_t off = r * args.ldc + c;
     if (args.c_f64) {
       double* dst = static_cast<double*>(args.c) + off;

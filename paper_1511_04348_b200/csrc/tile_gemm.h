@@ -47,6 +47,8 @@ struct GemmArgs {
   int32_t epilogue;              // Epilogue
   int32_t seg_kb;                // k-blocks (of 64) per TMEM partial sum; see below
   int32_t post;                  // PostOp
+  int32_t scaled;                // non-zero: the product is alpha * A.B (before STORE / ACCUMULATE)
+  float alpha;
   int32_t act;                   // Activation of the post-op
   const float* bias;             // POST_BIAS_ACT: bias of this tile's first column
   const float* aux;              // POST_ACT_GRAD: activation output at this tile's origin

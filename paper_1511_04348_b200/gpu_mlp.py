@@ -57,12 +57,23 @@ class DeviceLayer:
         return f"{self.tag}.w.v{self.version}"
 
 
+class PendingLoss:
+    """The loss of an enqueued training step: ``result()`` waits for its D2H copy."""
+
+    def __init__(self, host, event, n):
+        self._host, self._event, self._n = host, event, n
+
+    def result(self) -> float:
+        self._event.synchronize()
+        return float(self._host[0]) / self._n
+
+
 class GpuMLP:
     """A float32 MLP living in HBM, trained through a tiled ``Runtime`` session."""
 
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
                  device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
-                 process_group=None, write_through: bool = True):
+                 process_group=None, write_through: bool = True, fused_sgd: bool = True):
         import torch
 
         self.torch = torch
@@ -81,6 +92,7 @@ class GpuMLP:
         self.rt = runtime
         self.stream_ordered = stream_ordered
         self.write_through = write_through  # producers write the next round's operand tiles into the cache
+        self.fused_sgd = fused_sgd  # one process: dW products accumulate straight into W (no gradient buffer)
         self.pg = process_group
         if process_group is not None:
             import torch.distributed as dist
@@ -153,7 +165,7 @@ class GpuMLP:
             if t is not None:
                 self._pending.append(dist.all_reduce(t, group=self.pg, async_op=True))
 
-    def loss_gradients(self, x, target):
+    def loss_gradients(self, x, target, lr: float | None = None):
         """Forward + backward without update; returns (n, [(dW, db)]) with the loss
         sum left in ``self._loss`` (device).
 
@@ -162,6 +174,11 @@ class GpuMLP:
         is all act'() needs); the backward dX product of layer l multiplies by
         act'(A_{l-1}) in its epilogue, producing dY_{l-1} directly; dW_l and
         dX_l are independent and share one scheduling round.
+
+        With ``lr`` (the fused SGD step, one process): no dW is materialised --
+        the dW_l product accumulates straight into the weights, W_l += (-lr)
+        X_l^T dY_l (an axpy product), one round later, next to dX_{l-1}, so it
+        runs after dX_l has read W_l; the returned dW entries are None.
         """
         s = self._stream()
         xs, uids = [], []
@@ -186,18 +203,26 @@ class GpuMLP:
                _ACT[self.layers[last].activation], s)
         grads = [None] * len(self.layers)
         dy_uid = self.rt.fresh_uid("dy")
+        update = None  # fused SGD: the layer above's W += (-lr) X^T dY, run with this layer's round
         for li in range(last, -1, -1):
             L = self.layers[li]
             self._step_uids.append(dy_uid)
             next_dy = self.rt.fresh_uid("dy")
-            d_w = self._buf(f"dw{li}", L.w.shape)
             d_x = self._buf(f"dy{li - 1}" if li > 0 else "dx0", xs[li].shape)
             dx = dict(a=d_y, b=L.w, out=d_x, transpose_b=True, a_uid=dy_uid, b_uid=L.weight_uid)
             if li > 0:  # dX_l * act'(A_{l-1}) = dY_{l-1}  (xs[li] is A_{l-1})
                 dx["post"] = ("act_grad", xs[li], self.layers[li - 1].activation)
                 if self.write_through:
                     dx["cache_as"] = next_dy  # dY_{l-1} is the next round's operand
-            self._batch([dict(a=xs[li], b=d_y, out=d_w, transpose_a=True, a_uid=uids[li], b_uid=dy_uid), dx])
+            dw = dict(a=xs[li], b=d_y, transpose_a=True, a_uid=uids[li], b_uid=dy_uid)
+            if lr is None:
+                d_w = dw["out"] = self._buf(f"dw{li}", L.w.shape)
+                self._batch([dw, dx])
+            else:
+                d_w = None
+                dw.update(out=L.w, axpy=-float(lr))
+                self._batch([dx] + ([update] if update else []))
+                update = dw
             d_b = None
             if L.b is not None:
                 d_b = self._buf(f"db{li}", L.b.shape)
@@ -205,11 +230,20 @@ class GpuMLP:
             self._allreduce(d_w, d_b)  # overlaps the next (lower) layer's backward round
             grads[li] = (d_w, d_b)
             d_y, dy_uid = d_x, next_dy
+        if update:
+            self._batch([update])
         return pred.numel(), grads
 
     def train_step(self, x, target, lr: float) -> float:
         """One SGD step (ann.py:239-248); returns the MSE loss (read back to the host)."""
-        n, grads = self.loss_gradients(x, target)
+        return self.train_step_async(x, target, lr).result()
+
+    def train_step_async(self, x, target, lr: float) -> "PendingLoss":
+        """``train_step`` without the host wait: the step is enqueued, its loss is
+        copied to pinned host memory in stream order, and ``.result()`` waits for
+        that copy only -- so the host prepares step i+1 while step i runs."""
+        fused = self.fused_sgd and self.world == 1  # data parallel: all-reduce dW first
+        n, grads = self.loss_gradients(x, target, lr if fused else None)
         for h in self._pending:  # the current stream waits for every gradient all-reduce
             h.wait()
         self._pending = []
@@ -220,14 +254,19 @@ class GpuMLP:
         n *= self.world
         s = self._stream()
         for L, (d_w, d_b) in zip(self.layers, grads):
-            N.call("tr_mlp_sgd", _ptr(L.w), _ptr(d_w), L.w.numel(), float(lr), s)
+            if d_w is not None:
+                N.call("tr_mlp_sgd", _ptr(L.w), _ptr(d_w), L.w.numel(), float(lr), s)
             if L.b is not None:
                 N.call("tr_mlp_sgd", _ptr(L.b), _ptr(d_b), L.b.numel(), float(lr), s)
             self.rt.forget(L.weight_uid)  # this version is dead after the update
             L.version += 1
         for uid in self._step_uids:  # this step's activations and gradients are dead too
             self.rt.forget(uid)
-        return float(self._loss.item()) / n
+        host = self.torch.empty(1, dtype=self.torch.float64, pin_memory=True)  # torch's cached pinned pool
+        host.copy_(self._loss, non_blocking=True)
+        ev = self.torch.cuda.Event()
+        ev.record(self.torch.cuda.current_stream(self.dev))
+        return PendingLoss(host, ev, n)
 
     def to_host(self):
         """[(W, b)] as float64 numpy arrays."""

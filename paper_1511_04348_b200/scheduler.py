@@ -546,7 +546,8 @@ class Runtime:
         activation)`` (float32 device outputs).  ``cache_as=uid`` marks an output that a
         later product reads as an input under ``uid``: the producing kernel writes
         its converted tiles straight into the tile cache (tr_product.cache_as).
-        Returns the combined RunStats."""
+        ``axpy=alpha`` accumulates instead: out += alpha * a.b (tr_product.axpy; the
+        fused SGD update W += (-lr) X^T dY).  Returns the combined RunStats."""
         if self.mode == "sim":
             raise ValueError("multiply_batch runs on the GPU; the simulated engine takes one product per call")
         acts = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
@@ -564,6 +565,8 @@ class Runtime:
             q.c_uid = self._uids.id(pr.get("c_uid") or self.fresh_uid("c"))
             if pr.get("cache_as"):  # the output is read later as an input under this uid
                 q.cache_as = self._uids.id(pr["cache_as"])
+            if pr.get("axpy") is not None:  # out += alpha * a.b (float32 device out, no post-op)
+                q.axpy, q.alpha = 1, float(pr["axpy"])
             post = pr.get("post")
             if post is not None:
                 kind, ref, act = post

@@ -198,3 +198,44 @@ def test_write_through_matches_convert():
     for (w1, b1), (w0, b0) in zip(runs[True][1], runs[False][1]):
         assert np.array_equal(w1, w0) and np.array_equal(b1, b0)
     assert runs[True][2] < runs[False][2]
+
+
+def test_async_steps_match_blocking():
+    """train_step_async (loss read after the next step is enqueued) computes the
+    same trajectory as train_step, bit for bit."""
+    sizes = [784, 512, 512, 10]
+    runs = []
+    for use_async in (False, True):
+        mlp = GpuMLP.random(sizes, seed=21, runtime=Runtime(homogeneous_machine(1, dtype=np.float32), 256))
+        g = torch.Generator(device="cuda").manual_seed(22)
+        x = torch.rand((512, 784), device="cuda", generator=g)
+        t = torch.rand((512, 10), device="cuda", generator=g)
+        if use_async:
+            pend = [mlp.train_step_async(x, t, 0.3) for _ in range(6)]
+            losses = [p.result() for p in pend]
+        else:
+            losses = [mlp.train_step(x, t, 0.3) for _ in range(6)]
+        runs.append((losses, mlp.to_host()))
+        mlp.close()
+    assert runs[0][0] == runs[1][0]
+    for (w0, b0), (w1, b1) in zip(runs[0][1], runs[1][1]):
+        assert np.array_equal(w0, w1) and np.array_equal(b0, b1)
+
+
+def test_fused_sgd_matches_gradient_buffers():
+    """The fused update (dW products accumulating straight into W) trains like
+    the dW-buffer + SGD-kernel path, to fp32 rounding."""
+    sizes = [784, 1024, 1024, 10]
+    runs = []
+    for fused in (True, False):
+        mlp = GpuMLP.random(sizes, seed=31, runtime=Runtime(homogeneous_machine(1, dtype=np.float32), 512),
+                            fused_sgd=fused)
+        g = torch.Generator(device="cuda").manual_seed(32)
+        x = torch.rand((1024, 784), device="cuda", generator=g) * 2 - 1
+        t = torch.rand((1024, 10), device="cuda", generator=g) * 2 - 1
+        runs.append(([mlp.train_step(x, t, 0.5) for _ in range(4)], mlp.to_host()))
+        mlp.close()
+    (l0, p0), (l1, p1) = runs
+    assert np.allclose(l0, l1, rtol=1e-6, atol=0)
+    for (w0, b0), (w1, b1) in zip(p0, p1):
+        assert relerr(w0, w1) <= 1e-6 and np.array_equal(b0, b1)

@@ -109,3 +109,20 @@ def test_fused_posts_and_write_through():
     assert rel(res[0][1].numpy(), ref_dx.numpy()) <= 1e-5
     for u, v in zip(res[0], res[1]):
         assert torch.equal(u, v)
+
+
+@pytest.mark.parametrize("m,k,n,tile,ta", [(700, 4000, 10, 256, True), (1000, 3000, 700, 256, True),
+                                            (2048, 2048, 2048, 1024, True), (600, 12, 900, 256, False)])
+def test_axpy_products(m, k, n, tile, ta):
+    """out += alpha * a.b (the fused SGD update W += (-lr) X^T dY) on every
+    kernel path: CUDA-core (narrow, split), tensor-core (single / grouped,
+    split-K) -- against float64."""
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    a = torch.randn((k, m) if ta else (m, k), device="cuda", generator=g)
+    b = torch.randn(k, n, device="cuda", generator=g)
+    w = torch.randn(m, n, device="cuda", generator=g)
+    ref = w.double() - 0.125 * ((a.double().T if ta else a.double()) @ b.double())
+    rt = Runtime(homogeneous_machine(1, dtype=np.float32), tile)
+    rt.multiply_batch([dict(a=a, b=b, out=w, transpose_a=ta, axpy=-0.125)])
+    assert rel(w.double().cpu().numpy(), ref.cpu().numpy()) <= 1e-5
+    rt.close()
