@@ -73,7 +73,8 @@ class GpuMLP:
 
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
                  device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
-                 process_group=None, write_through: bool = True, fused_sgd: bool = True):
+                 process_group=None, write_through: bool = True, fused_sgd: bool = True,
+                 write_through_weights: bool | None = None):
         import torch
 
         self.torch = torch
@@ -93,6 +94,8 @@ class GpuMLP:
         self.stream_ordered = stream_ordered
         self.write_through = write_through  # producers write the next round's operand tiles into the cache
         self.fused_sgd = fused_sgd  # one process: dW products accumulate straight into W (no gradient buffer)
+        # fused SGD: the update product also writes the new weights' tiles into the cache
+        self.write_through_weights = write_through if write_through_weights is None else write_through_weights
         self.pg = process_group
         if process_group is not None:
             import torch.distributed as dist
@@ -221,6 +224,8 @@ class GpuMLP:
             else:
                 d_w = None
                 dw.update(out=L.w, axpy=-float(lr))
+                if self.write_through_weights:  # the updated weights' tiles enter the cache as the next version
+                    dw["cache_as"] = f"{L.tag}.w.v{L.version + 1}"
                 self._batch([dx] + ([update] if update else []))
                 update = dw
             d_b = None
