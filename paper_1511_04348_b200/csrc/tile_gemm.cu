@@ -49,16 +49,24 @@ constexpr int SMEM_BUDGET = 227 * 1024;
 // hi = bf16(v), lo = bf16(v - hi) for 4 consecutive values (the K2 split of a
 // float32 input, bit for bit), stored as 8-byte vectors into 1 or 2 planes.
 __device__ __forceinline__ void split4(uint16_t* dst, int64_t plane, int planes, float4 v) {
-  const float x[4] = {v.x, v.y, v.z, v.w};
-  uint16_t hi[4], lo[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat16 h = __float2bfloat16_rn(x[i]);
-    hi[i] = __bfloat16_as_ushort(h);
-    lo[i] = __bfloat16_as_ushort(__float2bfloat16_rn(x[i] - __bfloat162float(h)));
+  // packed conversions (one cvt.rn.bf16x2.f32 per pair): the epilogue's store
+  // phase is instruction-bound when it also writes the planes
+  const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y);
+  const __nv_bfloat162 h23 = __floats2bfloat162_rn(v.z, v.w);
+  uint2 hi;
+  hi.x = *reinterpret_cast<const uint32_t*>(&h01);
+  hi.y = *reinterpret_cast<const uint32_t*>(&h23);
+  *reinterpret_cast<uint2*>(dst) = hi;
+  if (planes == 2) {
+    const float2 f01 = __bfloat1622float2(h01);
+    const float2 f23 = __bfloat1622float2(h23);
+    const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
+    const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
+    uint2 lo;
+    lo.x = *reinterpret_cast<const uint32_t*>(&l01);
+    lo.y = *reinterpret_cast<const uint32_t*>(&l23);
+    *reinterpret_cast<uint2*>(dst + plane) = lo;
   }
-  *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(hi);
-  if (planes == 2) *reinterpret_cast<uint2*>(dst + plane) = *reinterpret_cast<const uint2*>(lo);
 }
 
 template <int PLANES, int CG>
