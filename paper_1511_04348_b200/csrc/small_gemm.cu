@@ -117,26 +117,27 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
     }
     ++g;
   }
-  for (; g < hi; ++g) {
-    const int klen = args.k_len[ks];
-    const uint16_t* pa = slab + static_cast<int64_t>(args.a_z[ks]) * ps;
-    const uint16_t* pb = slab + static_cast<int64_t>(args.b_z[ks]) * ps;
-    // ---- fetch the chunk: A (BM x KC) and B (KC x BN), all loads in flight
-    constexpr int AIT = (BM * KC / 8 + NTH - 1) / NTH;
-    constexpr int BIT = (KC * BN / 8 + NTH - 1) / NTH;
-    uint4 ah[AIT], al[AIT], bh[BIT], bl[BIT];
+  // Software pipeline: chunk g+1's global loads are in flight (registers)
+  // while chunk g is multiplied out of shared memory.
+  constexpr int AIT = (BM * KC / 8 + NTH - 1) / NTH;
+  constexpr int BIT = (KC * BN / 8 + NTH - 1) / NTH;
+  uint4 ah[AIT], al[AIT], bh[BIT], bl[BIT];
+  auto fetch = [&](int fks, int fkk) {  // A (BM x KC) and B (KC x BN) of chunk (fks, fkk)
+    const int klen = args.k_len[fks];
+    const uint16_t* pa = slab + static_cast<int64_t>(args.a_z[fks]) * ps;
+    const uint16_t* pb = slab + static_cast<int64_t>(args.b_z[fks]) * ps;
 #pragma unroll
     for (int it = 0; it < AIT; ++it) {
       const int idx = it * NTH + tid;
       if (idx >= BM * KC / 8) break;
       if (!A_MN) {  // stored M x K: 8 consecutive k of one row
         const int r = idx / (KC / 8), kq = (idx % (KC / 8)) * 8;
-        const int n = (m0 + r < args.m_valid) ? klen - (kk + kq) : 0;
-        fetch8(pa + static_cast<int64_t>(m0 + r) * ld + kk + kq, ps, planes, n, ah[it], al[it]);
+        const int n = (m0 + r < args.m_valid) ? klen - (fkk + kq) : 0;
+        fetch8(pa + static_cast<int64_t>(m0 + r) * ld + fkk + kq, ps, planes, n, ah[it], al[it]);
       } else {      // stored K x M: 8 consecutive m of one k
         const int k = idx / (BM / 8), mq = (idx % (BM / 8)) * 8;
-        const int n = (kk + k < klen) ? args.m_valid - (m0 + mq) : 0;
-        fetch8(pa + static_cast<int64_t>(kk + k) * ld + m0 + mq, ps, planes, n, ah[it], al[it]);
+        const int n = (fkk + k < klen) ? args.m_valid - (m0 + mq) : 0;
+        fetch8(pa + static_cast<int64_t>(fkk + k) * ld + m0 + mq, ps, planes, n, ah[it], al[it]);
       }
     }
 #pragma unroll
@@ -145,15 +146,16 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
       if (idx >= KC * BN / 8) break;
       if (B_K) {    // stored N x K: 8 consecutive k of one column
         const int c = idx / (KC / 8), kq = (idx % (KC / 8)) * 8;
-        const int n = (n0 + c < args.n_valid) ? klen - (kk + kq) : 0;
-        fetch8(pb + static_cast<int64_t>(n0 + c) * ld + kk + kq, ps, planes, n, bh[it], bl[it]);
+        const int n = (n0 + c < args.n_valid) ? klen - (fkk + kq) : 0;
+        fetch8(pb + static_cast<int64_t>(n0 + c) * ld + fkk + kq, ps, planes, n, bh[it], bl[it]);
       } else {      // stored K x N: 8 consecutive n of one k
         const int k = idx / (BN / 8), nq = (idx % (BN / 8)) * 8;
-        const int n = (kk + k < klen) ? args.n_valid - (n0 + nq) : 0;
-        fetch8(pb + static_cast<int64_t>(kk + k) * ld + n0 + nq, ps, planes, n, bh[it], bl[it]);
+        const int n = (fkk + k < klen) ? args.n_valid - (n0 + nq) : 0;
+        fetch8(pb + static_cast<int64_t>(fkk + k) * ld + n0 + nq, ps, planes, n, bh[it], bl[it]);
       }
     }
-    // ---- fp32 into shared memory: As[k][m], Bs[k][n]
+  };
+  auto stash = [&] {  // the fetched chunk, fp32, into As[k][m] and Bs[k][n]
 #pragma unroll
     for (int it = 0; it < AIT; ++it) {
       const int idx = it * NTH + tid;
@@ -186,8 +188,18 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
         for (int j = 0; j < 8; ++j) Bs[k][nq + j] = v[j];
       }
     }
+  };
+  if (g < hi) fetch(ks, kk);
+  for (; g < hi; ++g) {
+    stash();
     __syncthreads();
-    const int kn = min(KC, klen - kk);
+    const int kn = min(KC, args.k_len[ks] - kk);  // this chunk's extent
+    kk += KC;
+    if (kk >= args.k_len[ks]) {
+      ++ks;
+      kk = 0;
+    }
+    if (g + 1 < hi) fetch(ks, kk);  // the next chunk, while this one is multiplied
 #pragma unroll 8
     for (int k = 0; k < kn; ++k) {
       const float4 a = *reinterpret_cast<const float4*>(&As[k][ty * 4]);
@@ -199,11 +211,6 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
-    kk += KC;
-    if (kk >= klen) {
-      ++ks;
-      kk = 0;
-    }
   }
 
   // ---- epilogue: the same contract as the tensor-core kernel's.  A thread's 4
