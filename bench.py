@@ -231,6 +231,24 @@ def train_steps(torch, mlp, xs, ts, steps, lr=0.1):
     return losses
 
 
+def first_step_reference(torch, mlp, xs, n_rows=256):
+    """Parity sample for an MLP leg: a plain torch fp32 forward (cuBLAS SGEMM,
+    TF32 off) of the first rows of the batch with the initial weights."""
+    torch.backends.cuda.matmul.allow_tf32 = False
+    rows = slice(0, min(n_rows, xs.shape[0]))
+    h = xs[rows].cuda()
+    for L in mlp.layers:
+        h = torch.sigmoid(torch.addmm(L.b, h, L.w))
+    return h.double(), rows
+
+
+def pred_error(torch, mlp, ref_pred, rows):
+    """Relative Frobenius error of the first step's predictions (the forward
+    output the step left in its last activation buffer) against ref_pred."""
+    pred = mlp._bufs[f"a{len(mlp.layers) - 1}"][rows].double()
+    return float(torch.linalg.norm(pred - ref_pred) / torch.linalg.norm(ref_pred))
+
+
 def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32acc"):
     """cfg3: MLP training through the tiled runtime, device-resident (GpuMLP).
 
@@ -261,7 +279,10 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
     mlp = tr.GpuMLP(layers, tile_size=args.tile, device=local, precision=precision,
                     process_group=dist.group.WORLD if world > 1 else None)
     xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
-    losses = train_steps(torch, mlp, xs, ts, 2)  # warm-up: slab sizing, kernel attributes
+    ref_pred, rows = first_step_reference(torch, mlp, xs)
+    losses = train_steps(torch, mlp, xs, ts, 1)  # warm-up: slab sizing, kernel attributes
+    pred_err = pred_error(torch, mlp, ref_pred, rows)
+    losses += train_steps(torch, mlp, xs, ts, 1)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -280,6 +301,8 @@ def bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="fp32ac
             "samples_per_s": batch / dt, "ms_per_step": dt * 1e3, "tflops": flops / dt / 1e12,
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],
+            "pred_rel_err_vs_torch_fp32": pred_err,
+            "pred_parity_sample": "first step's predictions, batch rows 0..255 (of this rank's shard), vs a torch fp32 forward",
             "h2d_bytes_per_step": int(x.size * 4 + t.size * 4), "d2h_bytes_per_step": 8}
 
 
@@ -302,19 +325,9 @@ def bench_mlp_wide(args, tr, torch):
     xh[...] = (torch.rand(xh.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
     th[...] = (torch.rand(th.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
     xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
-    # parity: the first step's predictions for a slice of the batch against a plain
-    # torch fp32 forward of those rows (cuBLAS SGEMM, TF32 off), initial weights
-    torch.backends.cuda.matmul.allow_tf32 = False
-    rows = slice(0, 256)
-    h = xs[rows].cuda()
-    for L in mlp.layers:
-        h = torch.sigmoid(torch.addmm(L.b, h, L.w))
-    ref_pred = h.double()
-    del h
+    ref_pred, rows = first_step_reference(torch, mlp, xs)
     losses = train_steps(torch, mlp, xs, ts, 1)  # warm-up: slab, pools
-    pred = mlp._bufs[f"a{len(mlp.layers) - 1}"][rows].double()  # the warm-up step's forward output
-    pred_err = float(torch.linalg.norm(pred - ref_pred) / torch.linalg.norm(ref_pred))
-    del pred, ref_pred
+    pred_err = pred_error(torch, mlp, ref_pred, rows)
     before = dict(mlp.cache_counts)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -624,7 +637,7 @@ def main():
         if args.precision == "fp32acc":  # the native BF16 mode the north star also names (tolerance 1e-2)
             m16 = bench_mlp(args, tr, torch, local, barrier, max_over_ranks, precision="bf16")
             mlp["bf16_mode"] = {k: m16[k] for k in ("samples_per_s", "ms_per_step", "tflops", "loss_first",
-                                                    "loss_last")}
+                                                    "loss_last", "pred_rel_err_vs_torch_fp32")}
             free_hbm()
 
     # ---- cfg5: the 65536-wide MLP out-of-core on the tile cache, N=1 only
