@@ -726,14 +726,9 @@ bool Session::groupable(int d, Job& job, int64_t gtid) {
   int64_t tid = 0;
   const Product& p = job.prod_of(gtid, &tid);
   if (p.c.location != TR_LOC_DEVICE || p.k_steps > kMaxKSteps) return false;
-  const int64_t T = tile_;
-  const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
-  const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
-  int total_kb = 0;
-  for (int64_t k = 0; k < p.k_steps; ++k) total_kb += static_cast<int>((std::min(T, p.K - k * T) + 63) / 64);
-  (void)mt;
-  (void)total_kb;
-  return !(small_gemm_enabled() && (nt <= kSmallMaxN || p.K <= kSmallMaxK));  // else the CUDA-core kernel
+  // tasks for the CUDA-core kernel launch alone; k-splits are planned per group
+  const int64_t nt = std::min<int64_t>(tile_, p.N - (tid % p.grid_cols) * tile_);
+  return !(small_gemm_enabled() && (nt <= kSmallMaxN || p.K <= kSmallMaxK));
 }
 
 // _execute_task for several tasks at once: each task's directory sequence is the
