@@ -5,6 +5,7 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 #include <functional>
@@ -673,29 +674,39 @@ float* Session::workspace(int d, StreamCtx& sc, size_t bytes) {
   return sc.ws;
 }
 
-// Split-K for a grouped launch: the k-share count that minimises the
-// persistent grid's wave count per unit of work -- tiles * s units over the
-// device's CTA (pair) slots, each 1/s of the k-loop -- when that beats the
-// unsplit launch by 10% (784-row tiles: 2 tasks x 112 CTAs on 148 SMs).
+// Split-K for a grouped launch: the k-share count s that minimises the
+// estimated time -- the persistent grid's waves (tiles * s units over the
+// device's CTA (pair) slots, each 1/s of the k-loop) plus the partials'
+// round trip through HBM (written by the kernel, read by the reduction: 2 * s
+// fp32 output tiles) -- when that beats the unsplit launch by 10 %.
 int Session::group_split(int d, const GemmGroup& grp, bool pair) const {
   const int smax = splitk_max();
   if (smax < 2) return 1;
   const int cg = pair ? 2 : 1;
   int64_t tiles = 0;
+  double out_bytes = 0;
   int kb = 1 << 30;
   for (int t = 0; t < grp.n_tasks; ++t) {
     const GemmArgs& a = grp.task[t];
     tiles += ceil_div(a.m_valid, 128 * cg) * ceil_div(a.n_valid, 256);
+    out_bytes += 4.0 * a.m_valid * ((a.n_valid + 255) / 256 * 256);
     int k = 0;
     for (int q = 0; q < a.n_ksteps; ++q) k += (a.k_len[q] + 63) / 64;
     kb = std::min(kb, k);
   }
   const int64_t slots = std::max<int64_t>(1, devs_[d].sms / cg);
-  const double base = static_cast<double>(ceil_div(tiles, slots));
+  // time of one unit's full k-loop (µs; ~1.35 µs per split-bf16x3 k-block under
+  // the power cap, a third of that in bf16) and the partials' HBM round trip
+  // at ~5 TB/s (µs per byte)
+  const double unit_us = kb * (grp.task[0].planes == 2 ? 1.35 : 0.45);
+  const double us_per_byte = 1.0 / 5e6;
+  const bool with_reduce = !(getenv("TR_SPLIT_REDUCE_COST") && getenv("TR_SPLIT_REDUCE_COST")[0] == '0');
+  const double base = static_cast<double>(ceil_div(tiles, slots)) * unit_us;
   double best = base;
   int best_s = 1;
   for (int sp = 2; sp <= smax && kb / sp >= 8; ++sp) {
-    const double cost = static_cast<double>(ceil_div(tiles * sp, slots)) / sp;
+    const double cost = static_cast<double>(ceil_div(tiles * sp, slots)) / sp * unit_us +
+                        (with_reduce ? 2.0 * sp * out_bytes * us_per_byte : 0.0);
     if (cost < best - 1e-9) {
       best = cost;
       best_s = sp;
