@@ -227,7 +227,8 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
 #pragma unroll
       for (int j = 0; j < 4; ++j) acc[i][j] *= args.alpha;
   const bool vec = (part || !args.c_f64) && c0 + 4 <= args.n_valid && (ldo & 3) == 0 &&
-                   (reinterpret_cast<uintptr_t>(base) & 15) == 0 && (!args.aux || (args.ldaux & 3) == 0) &&
+                   (reinterpret_cast<uintptr_t>(base) & 15) == 0 &&
+                   (!args.aux || ((args.ldaux & 3) == 0 && (reinterpret_cast<uintptr_t>(args.aux) & 15) == 0)) &&
                    (!args.wt || (args.wt_ld & 3) == 0);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {

@@ -392,13 +392,18 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // pre[]: the activation rows for act_grad, else the C rows when accumulating
             // (both at once -- an accumulating act_grad product -- reads C inline)
             const bool pre_aux = post == POST_ACT_GRAD;
+            const bool aux_vec = (args.ldaux & 3) == 0 && (reinterpret_cast<uintptr_t>(args.aux) & 15) == 0;
             float4 pre[PRE];
 #pragma unroll
             for (int i = 0; i < PRE; ++i) {
               const int64_t grow_i = row0 + rb + r0 + i;
               pre[i] = make_float4(0.f, 0.f, 0.f, 0.f);
               if (grow_i < args.m_valid) {
-                if (pre_aux) pre[i] = __ldg(reinterpret_cast<const float4*>(args.aux + grow_i * args.ldaux + gcol0 + c));
+                if (pre_aux) {
+                  const float* ax = args.aux + grow_i * args.ldaux + gcol0 + c;
+                  pre[i] = aux_vec ? __ldg(reinterpret_cast<const float4*>(ax))
+                                   : make_float4(__ldg(ax), __ldg(ax + 1), __ldg(ax + 2), __ldg(ax + 3));
+                }
                 else if (acc_mode) pre[i] = *reinterpret_cast<const float4*>(obase + grow_i * ldo + gcol0 + c);
               }
             }

@@ -223,6 +223,27 @@ def test_batch_with_fused_epilogues(act):
     rt.close()
 
 
+@pytest.mark.parametrize("tile", [128, 16])
+def test_fused_epilogue_operands_with_odd_strides(tile):
+    """Fused post-op operands need not be 16-byte aligned: an activation that is
+    a column slice of a wider buffer (row stride 523 floats, offset 1) feeds the
+    act_grad epilogue of both kernels (tile 128: tensor cores; 16: CUDA cores)."""
+    g = torch.Generator().manual_seed(13)
+    dy, w = torch.randn(300, 270, generator=g, dtype=torch.float64), torch.randn(520, 270, generator=g, dtype=torch.float64)
+    wide = torch.rand(300, 523, generator=g, dtype=torch.float64)
+    a_prev = wide[:, 1:521]
+    dev = lambda t: t.float().cuda().contiguous()
+    aux = wide.float().cuda()[:, 1:521]
+    assert aux.stride(0) == 523 and aux.data_ptr() % 16 != 0
+    out = torch.empty(300, 520, device="cuda")
+    rt = Runtime(homogeneous_machine(1, dtype=np.float32), tile)
+    rt.multiply_batch([dict(a=dev(dy), b=dev(w), out=out, transpose_b=True, post=("act_grad", aux, "sigmoid"))])
+    r32 = lambda t: t.float().double()
+    ref = (r32(dy) @ r32(w).T) * (r32(a_prev) * (1 - r32(a_prev)))
+    assert rel(out.double().cpu().numpy(), ref.numpy()) <= 1e-5
+    rt.close()
+
+
 @pytest.mark.parametrize("side", [True, False])
 def test_stream_ordered_chain_with_torch_ops(side):
     """Runtime.set_stream(ordered=True): products return once enqueued; a chain
