@@ -215,7 +215,8 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       if (slots < 2) fail(TR_ERR_CAPACITY, "device %d: HBM budget too small for tile size %d", d, tile);
       dc.max_slots = static_cast<int32_t>(slots);
       const auto q1 = tnow();
-      dc.streams.resize(dc.width + 2);  // + fill (convert) stream [width] + copy stream [width+1]
+      // + fill (convert) stream [width] + copy stream [width+1] + writeback stream [width+2]
+      dc.streams.resize(dc.width + 3);
       TR_CUDA(cudaEventCreate(&dc.span_start));
       TR_CUDA(cudaEventCreate(&dc.span_end));
       int prio_low = 0, prio_high = 0;
@@ -234,6 +235,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
           TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking, prio));
         }
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
+        if (static_cast<int>(si) > dc.width + 1) continue;  // the writeback stream only copies
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
         TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
       }

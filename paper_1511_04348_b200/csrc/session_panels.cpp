@@ -101,6 +101,10 @@ bool Session::run_panels(Job& job) {
   std::vector<EvRef> task_last(nt_tasks);   // completion of each task's previous unit
   int64_t P = std::max<int64_t>(1, ks / 4);  // measured best on cfg2 (tools/probe_panels.py)
   if (const char* e = getenv("TR_PANELS")) P = std::max<int64_t>(0, std::min<int64_t>(ks, atoi(e)));
+  // k-steps per finishing unit: a unit starts as soon as ITS tiles are in, so
+  // short units let the last shell's compute follow its tiles in
+  int64_t F = ks;
+  if (const char* e = getenv("TR_PANEL_FINISH")) F = std::max<int64_t>(1, atoi(e));
   int gb = 1;  // tasks per finishing launch: each starts as soon as its own tiles are in
   if (const char* e = getenv("TR_PANEL_GROUP")) gb = std::max(1, std::min(G, atoi(e)));
   auto a_key = [&](int64_t i, int64_t k) { return p.ta ? std::make_pair(k, i) : std::make_pair(i, k); };
@@ -130,7 +134,12 @@ bool Session::run_panels(Job& job) {
       ++launch;
     };
     for (int64_t k = 0; k < P; ++k) add_grouped(k, k + 1, G);
-    if (P < ks) add_grouped(P, ks, gb);
+    if (P < ks && F >= ks - P) {
+      add_grouped(P, ks, gb);
+    } else if (P < ks) {  // finishing in chunks of F k-steps, task by task (same fill order)
+      for (size_t q = blk.first; q < blk.second; ++q)
+        for (int64_t k0 = P; k0 < ks; k0 += F) units.push_back(Unit{q, k0, std::min(ks, k0 + F), launch++});
+    }
     // ---- 2. fills in first-need order (uncounted, like fetch-ahead; the unit's acquire counts them)
     for (const Unit& u : units)
       for (int64_t k = u.k0; k < u.k1; ++k)
@@ -218,19 +227,23 @@ bool Session::run_panels(Job& job) {
         for (const TileKey& key : used) dir_->release_input_locked(d, key);
         for (size_t x = b; x < e; ++x) task_last[units[x].q] = ev;
       }
-      for (size_t x = b; x < e; ++x) {  // finished tasks: one pitched D2H each, then release C
+      // finished tasks: one pitched D2H each on the writeback stream (so the
+      // compute stream's next launch does not queue behind it), then release C
+      const int wb = W + 2;
+      for (size_t x = b; x < e; ++x) {
         const size_t q = units[x].q;
         if (--units_left[q] != 0) continue;
         const int64_t i = ti[q], j = tj[q];
         const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
         char* dst = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * ces;
+        wait_on(d, wb, task_last[q]);
         TimedLaunch tw{};
-        trace_begin(d, s, &tw);
+        trace_begin(d, wb, &tw);
         TR_CUDA(cudaMemcpy2DAsync(dst, p.c.ld * ces, static_cast<char*>(guard.p) + (q - blk.first) * ctile, nt * ces,
-                                  nt * ces, mt, cudaMemcpyDeviceToHost, sc.stream));
-        trace_end(d, s, tw, TR_TRACE_D2H, order[q], p.c_uid, i, j);
+                                  nt * ces, mt, cudaMemcpyDeviceToHost, dc.streams[wb].stream));
+        trace_end(d, wb, tw, TR_TRACE_D2H, order[q], p.c_uid, i, j);
         std::lock_guard<std::mutex> lk(dir_->mu);
-        cbuf_free[q - blk.first] = record(d, s);
+        cbuf_free[q - blk.first] = record(d, wb);
         dir_->release_output_locked(d, TileKey{p.c_uid, i, j}, mt * nt * element_bytes_);  // coherence.py:263-280
       }
       b = e;
