@@ -23,6 +23,9 @@ variants = {
     "write_through": dict(cache_as="WT"),
     "bias_act+wt": dict(post=("bias_act", bias, "sigmoid"), cache_as="WT"),
     "tb+act_grad+wt": dict(transpose_b=True, post=("act_grad", aux, "sigmoid"), cache_as="WT"),
+    "ta+axpy": dict(transpose_a=True, axpy=-0.01),
+    "ta+axpy+wt": dict(transpose_a=True, axpy=-0.01, cache_as="WT"),
+    "axpy": dict(axpy=-0.01),
 }
 for name, kw in variants.items():
     ts = []

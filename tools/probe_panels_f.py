@@ -1,5 +1,5 @@
-"""Probe: cold cfg2 run() time vs k-steps per finishing unit (TR_PANEL_FINISH,
-read per run) for the k-panel schedule.  Dev tool."""
+"""Probe: cold cfg2 run() time vs (k-steps per finishing unit, k-major panels):
+COMBOS="F:P,..." (TR_PANEL_FINISH / TR_PANELS, read per run).  Dev tool."""
 import os
 import numpy as np
 import torch
@@ -18,8 +18,8 @@ for _ in range(2):
     del c
 res = {}
 for rep in range(3):
-    for f in ("8", "1", "2", "3"):
-        os.environ["TR_PANEL_FINISH"] = f
+    for f in os.environ.get("COMBOS", "8:2,1:2,2:2,3:2").split(","):
+        os.environ["TR_PANEL_FINISH"], os.environ["TR_PANELS"] = f.split(":")
         c = None
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -10,7 +10,8 @@ gib = float(sys.argv[1]) if len(sys.argv) > 1 else 24.0
 sizes = [784, 65536, 65536, 65536]
 batch = 8192
 rt = tr.Runtime(tr.homogeneous_machine(1, dtype=np.float32), 4096, hbm_budget_bytes=int(gib * 2**30))
-mlp = tr.GpuMLP.random(sizes, seed=0, runtime=rt)
+import os
+mlp = tr.GpuMLP.random(sizes, seed=0, runtime=rt, write_through_weights=os.environ.get("WTW", "1") == "1")
 g = torch.Generator(device="cuda").manual_seed(1)
 x = torch.rand(batch, sizes[0], device="cuda", generator=g) * 2 - 1
 t = torch.rand(batch, sizes[-1], device="cuda", generator=g) * 2 - 1
