@@ -361,6 +361,13 @@ int tr_set_splitk(int32_t max_splits);
  * TR_SMALL_GEMM=0 in the environment sets the default. */
 int tr_set_small_gemm(int32_t on);
 
+/* Narrow outputs on the tensor cores (process-wide): a task whose output tile
+ * is at most 32 columns wide (contraction longer than 32) runs as the
+ * transposed product Bᵀ·Aᵀ -- its long side on the MMA's N dimension -- split
+ * along k, and a reduction writes C.  Default on; 0 leaves such tasks to the
+ * CUDA-core kernel; TR_NARROW_TC=0 in the environment sets the default. */
+int tr_set_narrow_tc(int32_t on);
+
 /* Grouped launches (process-wide, sessions created afterwards): up to
  * `max_tasks` (1..8) ready tasks of one product from a device's reservation
  * station run as ONE tile-GEMM launch (device outputs, unchunked tasks).  Each

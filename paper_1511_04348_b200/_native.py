@@ -144,6 +144,7 @@ _PROTOS = {
     "tr_set_gemm_pairs": [i32],
     "tr_set_splitk": [i32],
     "tr_set_small_gemm": [i32],
+    "tr_set_narrow_tc": [i32],
     "tr_set_task_group": [i32],
     "tr_mlp_bias_act": [vp, vp, vp, i64, i64, i32, vp],
     "tr_mlp_act_grad": [vp, vp, vp, vp, i64, i32, vp],

@@ -493,4 +493,8 @@ int tr_set_small_gemm(int32_t on) {
   return guarded([&] { tr::set_small_gemm(on != 0); });
 }
 
+int tr_set_narrow_tc(int32_t on) {
+  return guarded([&] { tr::set_narrow_tc(on != 0); });
+}
+
 }  // extern "C"

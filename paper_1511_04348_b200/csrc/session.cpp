@@ -635,6 +635,52 @@ void Session::plan_split_k(int d, StreamCtx& sc, GemmArgs& args) {
   if (s >= 2) use_workspace(d, sc, args, s, (args.n_valid + 255) / 256 * 256);
 }
 
+// A narrow task on the tensor cores (tile_gemm.h, narrow_tc): t is the
+// transposed product P = Bᵀ·Aᵀ (operand planes swapped, raw fp32 out) split
+// along k to about two waves of CTAs; args gets P's partials (args.ws, ws_ld,
+// ws_zstride, k_split) for launch_splitk_reduce_t.  False without workspace.
+bool Session::plan_narrow(int d, StreamCtx& sc, GemmArgs& args, GemmArgs& t) {
+  t = args;
+  t.m_valid = args.n_valid;
+  t.n_valid = args.m_valid;
+  int kb = 0;
+  for (int k = 0; k < args.n_ksteps; ++k) {
+    t.a_z[k] = args.b_z[k];
+    t.b_z[k] = args.a_z[k];
+    kb += (args.k_len[k] + 63) / 64;
+  }
+  t.c_f64 = 0;
+  t.epilogue = EPI_STORE;
+  t.post = POST_NONE;
+  t.scaled = 0;
+  t.bias = nullptr;
+  t.aux = nullptr;
+  t.wt = nullptr;
+  const int64_t ctas = ceil_div(t.n_valid, 256);  // P has <= 32 rows: one 128-row block
+  int splits = splitk_max() < 2 ? 1 : static_cast<int>(std::max<int64_t>(
+                   1, std::min<int64_t>({ceil_div(2 * devs_[d].sms, ctas), 16, kb / 8})));
+  const int64_t ws_ld = (t.n_valid + 255) / 256 * 256;
+  const int64_t zstride = static_cast<int64_t>(t.m_valid) * ws_ld;
+  float* ws = workspace(d, sc, static_cast<size_t>(splits * zstride) * sizeof(float));
+  if (!ws) return false;
+  if (splits > 1) {
+    t.k_split = splits;
+    t.ws = ws;
+    t.ws_ld = ws_ld;
+    t.ws_zstride = zstride;
+    t.c = nullptr;
+  } else {  // one share: P is stored straight into the workspace
+    t.k_split = 1;
+    t.c = ws;
+    t.ldc = ws_ld;
+  }
+  args.k_split = splits;
+  args.ws = ws;
+  args.ws_ld = ws_ld;
+  args.ws_zstride = zstride;
+  return true;
+}
+
 // The CUDA-core kernel's split: ~4 CTAs per SM for a narrow tile's long k.
 void Session::plan_split_small(int d, StreamCtx& sc, GemmArgs& args) {
   args.k_split = 1;
@@ -982,33 +1028,44 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       used_phys.push_back(pa);
       used_phys.push_back(pb);
     }
-    const bool small = !dryrun_ && small_gemm_enabled() && small_gemm_eligible(args);
-    if (!dryrun_) {
+    int64_t k_total = 0;
+    for (int64_t k = 0; k < kc; ++k) k_total += args.k_len[k];
+    // narrow C tile (the MLP's 10-wide output layer): Bᵀ·Aᵀ on the tensor cores
+    GemmArgs targs;
+    const bool narrow = !dryrun_ && narrow_tc_enabled() && T > kSmallMaxN && args.n_valid <= kSmallMaxN &&
+                        k_total > kSmallMaxK && plan_narrow(d, *scp, args, targs);
+    const bool small = !dryrun_ && !narrow && small_gemm_enabled() && small_gemm_eligible(args);
+    if (!dryrun_ && !narrow) {
       if (small) plan_split_small(d, *scp, args);
       else plan_split_k(d, *scp, args);
     }
-    const int32_t wt = (!dryrun_ && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
+    const int32_t wt = (!dryrun_ && !narrow && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
+    const bool reduce = narrow || args.k_split > 1;
     auto launch = [&] {
-      if (small) {
-        TR_CUDA(launch_small_gemm(dc.slab, ld_, plane_elems_, args, p.ta, p.tb, scp->stream));
+      if (narrow) {  // A' = Bᵀ, B' = Aᵀ: the layouts swap roles
+        BoxKind ba, bb;
+        gemm_boxes(!p.tb, !p.ta, targs.m_valid, &ba, &bb);
+        TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], targs, !p.tb, !p.ta, scp->stream));
+        TR_CUDA(launch_splitk_reduce_t(args, scp->stream));
         return;
       }
-      BoxKind ba, bb;
-      gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
-      TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+      if (small) {
+        TR_CUDA(launch_small_gemm(dc.slab, ld_, plane_elems_, args, p.ta, p.tb, scp->stream));
+      } else {
+        BoxKind ba, bb;
+        gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
+        TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+      }
+      if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
     };
     if (!dryrun_ && job.async) {
       launch();
-      if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
-      job.launches.fetch_add(args.k_split > 1 ? 2 : 1);
+      job.launches.fetch_add(reduce ? 2 : 1);
     } else if (!dryrun_) {
       TimedLaunch tl = timing_pair(d);
       TR_CUDA(cudaEventRecord(tl.start, scp->stream));
       launch();
-      if (args.k_split > 1) {
-        TR_CUDA(launch_splitk_reduce(args, scp->stream));
-        job.launches.fetch_add(1);
-      }
+      if (reduce) job.launches.fetch_add(1);
       TR_CUDA(cudaEventRecord(tl.end, scp->stream));
       dc.timed.push_back(tl);
       if (tracing_) {

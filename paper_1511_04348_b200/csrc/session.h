@@ -209,6 +209,7 @@ class Session {
   double xfer_cost(int src, int dst, int64_t nbytes) const;
   void plan_split_k(int d, StreamCtx& sc, GemmArgs& args);
   void plan_split_small(int d, StreamCtx& sc, GemmArgs& args);
+  bool plan_narrow(int d, StreamCtx& sc, GemmArgs& args, GemmArgs& t);
   void use_workspace(int d, StreamCtx& sc, GemmArgs& args, int splits, int64_t ws_ld);
   float* workspace(int d, StreamCtx& sc, size_t bytes);
   int group_split(int d, const GemmGroup& grp, bool pair) const;

@@ -575,6 +575,35 @@ __global__ void splitk_reduce_kernel(const __grid_constant__ GemmArgs args) {
   }
 }
 
+// The transposed-product reduction: the partials of P = Bᵀ·Aᵀ (narrow C
+// computed with its long side on the MMA's N) sit at ws + z*ws_zstride as
+// rows = C's columns; C[r, c] (+)= alpha * sum_z P_z[c, r] in z order, then the
+// post-op -- the same epilogue contract as splitk_reduce_kernel.
+__global__ void splitk_reduce_t_kernel(const __grid_constant__ GemmArgs args) {
+  const int64_t m = args.m_valid;
+  const int64_t total = m * args.n_valid;
+  const bool acc_mode = args.epilogue == EPI_ACCUMULATE;
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = idx % m, c = idx / m;  // r fastest: the partials are read along their rows
+    const float* w = args.ws + c * args.ws_ld + r;
+    float v = w[0];
+    for (int z = 1; z < args.k_split; ++z) v += w[z * args.ws_zstride];
+    if (args.scaled) v *= args.alpha;
+    const int64_t off = r * args.ldc + c;
+    if (args.c_f64) {
+      double* dst = static_cast<double*>(args.c) + off;
+      *dst = acc_mode ? *dst + static_cast<double>(v) : static_cast<double>(v);
+      continue;
+    }
+    float* dst = static_cast<float*>(args.c) + off;
+    if (acc_mode) v += *dst;
+    if (args.post == POST_BIAS_ACT) v = act_fwd(args.act, v + (args.bias ? args.bias[c] : 0.f));
+    else if (args.post == POST_ACT_GRAD) v = v * act_grad_from_out(args.act, args.aux[r * args.ldaux + c]);
+    *dst = v;
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -686,6 +715,29 @@ cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {
   splitk_reduce_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
   return cudaGetLastError();
 }
+
+cudaError_t launch_splitk_reduce_t(const GemmArgs& args, cudaStream_t stream) {
+  if (args.k_split < 1 || !args.ws || args.wt) return cudaErrorInvalidValue;
+  const int64_t total = static_cast<int64_t>(args.m_valid) * args.n_valid;
+  const int threads = 256;
+  const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((total + threads - 1) / threads, 148 * 8));
+  splitk_reduce_t_kernel<<<static_cast<unsigned>(blocks), threads, 0, stream>>>(args);
+  return cudaGetLastError();
+}
+
+static std::atomic<int> g_narrow_tc{-1};
+
+bool narrow_tc_enabled() {
+  int v = g_narrow_tc.load();
+  if (v < 0) {
+    const char* e = getenv("TR_NARROW_TC");
+    v = (e && e[0] == '0') ? 0 : 1;
+    g_narrow_tc.store(v);
+  }
+  return v == 1;
+}
+
+void set_narrow_tc(bool on) { g_narrow_tc.store(on ? 1 : 0); }
 
 static std::atomic<int> g_splitk{-1};
 

@@ -127,6 +127,17 @@ void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* 
 // args.epilogue (STORE / ACCUMULATE) and args.post, exactly like the kernel's own
 // epilogue would have (same argument block).
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream);
+// Narrow outputs on the tensor cores: a task whose C tile is at most
+// kSmallMaxN columns wide (and whose contraction is longer than kSmallMaxK) is
+// computed as P = Bᵀ·Aᵀ -- the long side on the MMA's N, the narrow side on its
+// 128 rows -- with the k-loop split over the grid; P's partials go to args.ws
+// (rows = C's columns, ws_ld) and launch_splitk_reduce_t sums them in z order
+// into C[r, c] with the task's epilogue / post-op.  Process-wide switch,
+// default on (TR_NARROW_TC=0 or set_narrow_tc(false): such tasks run on the
+// CUDA-core kernel instead).
+cudaError_t launch_splitk_reduce_t(const GemmArgs& args, cudaStream_t stream);
+bool narrow_tc_enabled();
+void set_narrow_tc(bool on);
 // Split-K policy switch (process-wide): max splits per launch, 1 disables.
 // Default 8; TR_SPLITK=<n> in the environment overrides.
 int splitk_max();

@@ -42,6 +42,11 @@ def set_small_gemm(on: bool) -> None:
     N.call("tr_set_small_gemm", int(bool(on)))
 
 
+def set_narrow_tc(on: bool) -> None:
+    """Narrow output tiles (<= 32 columns) as the transposed product on the tensor cores (default on)."""
+    N.call("tr_set_narrow_tc", int(bool(on)))
+
+
 def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,
                stream=None):
     """``out (+)= op(a) @ op(b)`` for torch CUDA tensors (float32/float64).

@@ -303,7 +303,20 @@ def test_split_k_exact_on_integers(no_split, precision, m, k, n, tile, cap):
     assert np.array_equal(outs[0], outs[1])
 
 
-def test_split_k_normal_data_and_fused_posts(no_split):
+@pytest.fixture
+def tensor_cores_only():
+    """Every task on the tensor-core kernel in its plain orientation (no CUDA-core
+    or transposed narrow path): the split-K tests below are about that kernel."""
+    from paper_1511_04348_b200.dense import set_narrow_tc, set_small_gemm
+
+    set_small_gemm(False)
+    set_narrow_tc(False)
+    yield
+    set_small_gemm(True)
+    set_narrow_tc(True)
+
+
+def test_split_k_normal_data_and_fused_posts(no_split, tensor_cores_only):
     g = torch.Generator().manual_seed(11)
     f = lambda *s: torch.randn(*s, generator=g, dtype=torch.float64)
     x, w, bias = f(1000, 8192), f(8192, 10), f(10)

@@ -10,7 +10,7 @@ from torch.profiler import ProfilerActivity, profile
 
 from oracle import tilerun_oracle as O
 from paper_1511_04348_b200 import Runtime, homogeneous_machine, run
-from paper_1511_04348_b200.dense import set_small_gemm, set_splitk
+from paper_1511_04348_b200.dense import set_narrow_tc, set_small_gemm, set_splitk
 
 pytestmark = pytest.mark.gpu
 
@@ -23,6 +23,7 @@ def rel(x, ref):
 def small():
     yield set_small_gemm
     set_small_gemm(True)
+    set_narrow_tc(True)
     set_splitk(8)
 
 
@@ -51,18 +52,30 @@ def test_matches_f64_and_tensor_cores(small, precision, m, k, n, tile, ta, tb):
     b = torch.randn((n, k) if tb else (k, n), device="cuda", generator=g)
     ref = (a.double().T if ta else a.double()) @ (b.double().T if tb else b.double())
     outs = {}
-    for on in (True, False):
-        small(on)
+    narrow = n <= 32 and k > 32
+    # default: narrow tiles as the transposed tensor-core product, tiny contractions
+    # on CUDA cores; "cuda": narrow tiles on CUDA cores too; "tc": everything on
+    # the tensor cores in the plain orientation
+    for mode in ("default", "cuda", "tc"):
+        small(mode != "tc")
+        set_narrow_tc(mode == "default")
         rt = Runtime(homogeneous_machine(1, dtype=np.float32), tile, precision=precision)
         c = torch.empty(m, n, device="cuda")
         names = kernels_run(lambda: rt.multiply(a, b, transpose_a=ta, transpose_b=tb, out=c))
-        assert any("small_gemm" in x for x in names) == on, names
-        outs[on] = c.double()
+        used_small = any("small_gemm" in x for x in names)
+        used_t = any("reduce_t" in x for x in names)
+        if mode == "default":
+            assert used_t == narrow and used_small == (not narrow), names
+        elif mode == "cuda":
+            assert used_small and not used_t, names
+        else:
+            assert not used_small and not used_t, names
+        outs[mode] = c.double()
         rt.close()
     tol = 1e-5 if precision == "fp32acc" else 1e-2
     for c in outs.values():
         assert rel(c.cpu().numpy(), ref.cpu().numpy()) <= tol
-    assert rel(outs[True].cpu().numpy(), outs[False].cpu().numpy()) <= tol
+    assert rel(outs["default"].cpu().numpy(), outs["tc"].cpu().numpy()) <= tol
 
 
 @pytest.mark.parametrize("m,k,n,tile,cap", [(700, 4000, 10, 256, None), (600, 12, 900, 256, None),
@@ -74,8 +87,9 @@ def test_integer_exact_split_and_chunked(small, m, k, n, tile, cap):
     a = rng.integers(-4, 5, size=(m, k)).astype(np.float64)
     b = rng.integers(-4, 5, size=(k, n)).astype(np.float64)
     machine = homogeneous_machine(2, capacity_tiles=cap)
-    for splits in (8, 1):
+    for splits, narrow in ((8, True), (1, True), (8, False)):
         set_splitk(splits)
+        set_narrow_tc(narrow)
         c, s = run(machine, a, b, tile)
         assert np.array_equal(c, O.reference_gemm(a, b))
         assert s.cache.input_requests == 2 * s.total_tasks * -(-k // tile)
