@@ -280,6 +280,7 @@ Session::~Session() {
       DevPool::get().release(dc.gpu, sc.staging, sc.staging_cap);
       DevPool::get().release(dc.gpu, sc.outbuf, sc.outbuf_cap);
       if (sc.ws) DevPool::get().release(dc.gpu, sc.ws, sc.ws_cap);
+      if (sc.gout) DevPool::get().release(dc.gpu, sc.gout, sc.gout_cap);
       cudaStreamDestroy(sc.stream);
     }
     for (auto& t : dc.timed) {
@@ -595,8 +596,12 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vect
                           int64_t& pending) {
   DeviceCtx& dc = devs_[d];
   // unclaimed prefetched tiles per device / tasks looked ahead past the queue
-  // head; out-of-core jobs look further (the next task block's panels)
-  const int64_t kBudget = job.out_of_core ? 96 : 32;
+  // head; out-of-core jobs look further (the next task block's panels).  Long
+  // contractions (cfg4: 32 k-steps) need two tasks' panels in flight: a new
+  // shell's first task brings a whole row panel (k tiles) before it can run.
+  int64_t max_ks = 0;
+  for (const Product& p : job.prods) max_ks = std::max<int64_t>(max_ks, p.k_steps);
+  const int64_t kBudget = std::max<int64_t>(job.out_of_core ? 96 : 32, 4 * max_ks);
   const int64_t kLookahead = job.out_of_core ? 48 : 16;
   for (uint64_t tid : dc.station->peek()) {
     if (seen[tid]) continue;
@@ -722,6 +727,27 @@ float* Session::workspace(int d, StreamCtx& sc, size_t bytes) {
   return sc.ws;
 }
 
+// Stream s's C tiles for a grouped launch with host outputs, grown to >= bytes
+// (false when HBM is short: the tasks then run one launch each).
+bool Session::group_outbuf(int d, int s, size_t bytes) {
+  StreamCtx& sc = devs_[d].streams[s];
+  if (bytes <= sc.gout_cap) return true;
+  DeviceCtx& dc = devs_[d];
+  if (sc.gout) {
+    TR_CUDA(cudaDeviceSynchronize());  // earlier launches and writebacks may still use it
+    DevPool::get().release(dc.gpu, sc.gout, sc.gout_cap);
+    sc.gout = nullptr;
+    sc.gout_cap = 0;
+  }
+  if (DevPool::get().alloc(dc.gpu, bytes, &sc.gout, &sc.gout_cap) != cudaSuccess) {
+    cudaGetLastError();
+    sc.gout = nullptr;
+    sc.gout_cap = 0;
+    return false;
+  }
+  return true;
+}
+
 // Split-K for a grouped launch: the k-share count s that minimises the
 // estimated time -- the persistent grid's waves (tiles * s units over the
 // device's CTA (pair) slots, each 1/s of the k-loop) plus the partials'
@@ -779,12 +805,13 @@ int task_group_max() {
 void set_task_group_max(int n) { g_task_group.store(std::max(1, std::min(kMaxGroup, n))); }
 
 // A task qualifies for a grouped launch when it runs as ONE launch (coherence on,
-// capacity unbounded), writes a device output and would not be split along K.
+// capacity unbounded) and would not be split along K.  Host outputs land in the
+// stream's group buffer and are written back on the writeback stream.
 bool Session::groupable(int d, Job& job, int64_t gtid) {
   if (dryrun_ || !coherence_ || devs_[d].capacity >= 0 || max_group_ < 2) return false;
   int64_t tid = 0;
   const Product& p = job.prod_of(gtid, &tid);
-  if (p.c.location != TR_LOC_DEVICE || p.k_steps > kMaxKSteps) return false;
+  if (p.k_steps > kMaxKSteps) return false;
   // tasks for the CUDA-core kernel launch alone; k-splits are planned per group
   const int64_t nt = std::min<int64_t>(tile_, p.N - (tid % p.grid_cols) * tile_);
   return !(small_gemm_enabled() && (nt <= kSmallMaxN || p.K <= kSmallMaxK));
@@ -804,6 +831,8 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   std::vector<int32_t> used_phys;
   std::vector<int32_t> wt_phys;  // slots the launch writes through
   const Product* p0 = nullptr;
+  int64_t tid0 = 0;
+  const size_t gtile = static_cast<size_t>(T * T * job.prod_of(gtids[0], &tid0).c.esize());
   for (size_t q = 0; q < gtids.size(); ++q) {
     int64_t tid = 0;
     const Product& p = job.prod_of(gtids[q], &tid);
@@ -820,8 +849,13 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     args.n_valid = static_cast<int32_t>(nt);
     args.n_ksteps = static_cast<int32_t>(p.k_steps);
     args.planes = planes_;
-    args.c = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * p.c.esize();
-    args.ldc = p.c.ld;
+    if (p.c.location == TR_LOC_HOST) {  // the group buffer; written back after the launch
+      args.c = static_cast<char*>(sc.gout) + q * gtile;
+      args.ldc = nt;
+    } else {
+      args.c = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * p.c.esize();
+      args.ldc = p.c.ld;
+    }
     args.c_f64 = p.c.dtype == TR_DTYPE_F64;
     args.epilogue = p.axpy ? EPI_ACCUMULATE : EPI_STORE;
     args.scaled = p.axpy;
@@ -874,10 +908,13 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     const int32_t wt = write_through(d, s, p, tid / p.grid_cols, tid % p.grid_cols, grp.task[q]);
     if (wt >= 0) wt_phys.push_back(wt);
   }
+  const bool host_c = p0->c.location == TR_LOC_HOST;
+  if (host_c) wait_on(d, s, sc.gout_free);  // the previous group's writeback has read the buffer
   BoxKind ba, bb;
   gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
   auto launch = [&] {
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb, persistent_enabled(), sc.stream,
+    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb,
+                                   persistent_enabled() && !dc.host_fills, sc.stream,
                                    dc.sms));
     if (grp.k_split > 1)
       for (int t = 0; t < grp.n_tasks; ++t) TR_CUDA(launch_splitk_reduce(grp.task[t], sc.stream));
@@ -904,9 +941,11 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     }
   }
   job.launches.fetch_add(1);
+  EvRef kernel_done;
   {
     std::lock_guard<std::mutex> g(dir_->mu);
     const EvRef ev = record(d, s);
+    kernel_done = ev;
     for (int32_t ph : used_phys) note_use(dc.slots[ph], ev);
     for (int32_t ph : wt_phys) {  // the written-through tiles are ready when the launch is done
       dc.slots[ph].ready = ev;
@@ -920,6 +959,28 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
       const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
       dir_->release_output_locked(d, TileKey{p.c_uid, i, j}, mt * nt * element_bytes_);  // coherence.py:263-280
     }
+  }
+  if (host_c) {
+    // one pitched D2H per C tile on the writeback stream, so this stream (and the
+    // next grouped launch, which waits for every other stream's kernel) does not
+    // queue behind the copies; the job's final sync covers the writeback stream
+    const int wb = dc.width + 2;
+    wait_on(d, wb, kernel_done);
+    for (size_t q = 0; q < gtids.size(); ++q) {
+      int64_t tid = 0;
+      const Product& p = job.prod_of(gtids[q], &tid);
+      const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
+      const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
+      const int64_t ces = p.c.esize();
+      char* dst = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * ces;
+      TimedLaunch tw{};
+      trace_begin(d, wb, &tw);
+      TR_CUDA(cudaMemcpy2DAsync(dst, p.c.ld * ces, static_cast<char*>(sc.gout) + q * gtile, nt * ces, nt * ces, mt,
+                                cudaMemcpyDeviceToHost, dc.streams[wb].stream));
+      trace_end(d, wb, tw, TR_TRACE_D2H, gtids[q], p.c_uid, i, j);
+    }
+    std::lock_guard<std::mutex> g(dir_->mu);
+    sc.gout_free = record(d, wb);
   }
   if (job.async) {
     for (int64_t gt : gtids) {
@@ -1150,6 +1211,29 @@ void Session::run_job(int d, Job& job) {
   bool prio = !dryrun_ && coherence_ && !job.async && getenv("TR_PRIORITY") == nullptr;
   for (auto& dv : devs_) prio = prio && dv.capacity < 0;
   if (const char* e = getenv("TR_PRIORITY")) prio = !dryrun_ && e[0] == '1';
+  // A job that still has host tiles to fill runs its grouped launches
+  // non-persistent: a persistent grid holds every SM for the whole launch, so the
+  // fill stream's split/convert blocks (top priority) only start between launches
+  // and the next group's tiles arrive late (cfg4 N=131072 cold: 0.75 s of idle
+  // tensor cores per 11.6 s product persistent, 0.13 s non-persistent).
+  dc.host_fills = false;
+  if (!dryrun_) {
+    std::lock_guard<std::mutex> g(dir_->mu);
+    for (const Product& p : job.prods) {
+      for (int which = 0; which < 2 && !dc.host_fills; ++which) {
+        const Mat& m = which == 0 ? p.a : p.b;
+        if (m.location != TR_LOC_HOST) continue;
+        const uint64_t uid = which == 0 ? p.a_uid : p.b_uid;
+        for (int64_t r = 0; r < (m.rows + tile_ - 1) / tile_ && !dc.host_fills; ++r)
+          for (int64_t c = 0; c < (m.cols + tile_ - 1) / tile_; ++c)
+            if (!(dir_->owners_locked(TileKey{uid, r, c}) >> d & 1)) {
+              dc.host_fills = true;
+              break;
+            }
+      }
+      if (dc.host_fills) break;
+    }
+  }
   std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.total) : 0, 0);
   std::vector<uint8_t> seen_global(seen.size(), 0);
   dc.pending_prefetch = 0;
@@ -1221,11 +1305,13 @@ void Session::run_job(int d, Job& job) {
     // in a product's tail single tasks stay stealable, so a slow (e.g. green-
     // context) device never holds several tasks the others could have taken.
     const bool tail = job.n_tasks - job.claimed.load() < static_cast<int64_t>(max_group_) * n_devices();
-    if (victim < 0 && !(tail && n_devices() > 1) && groupable(d, job, static_cast<int64_t>(tid))) {
+    int64_t t0 = 0;
+    const Product* p0 = &job.prod_of(static_cast<int64_t>(tid), &t0);
+    if (victim < 0 && !(tail && n_devices() > 1) && groupable(d, job, static_cast<int64_t>(tid)) &&
+        (p0->c.location != TR_LOC_HOST ||
+         group_outbuf(d, s, static_cast<size_t>(std::min(max_group_, kMaxGroup)) * tile_ * tile_ * p0->c.esize()))) {
       // the station's other ready tasks of the same product join this launch
       std::vector<int64_t> grp{static_cast<int64_t>(tid)};
-      int64_t t0 = 0;
-      const Product* p0 = &job.prod_of(grp[0], &t0);
       const bool tall0 = group_uses_pairs(static_cast<int>(std::min<int64_t>(tile_, p0->M - (t0 / p0->grid_cols) * tile_)));
       uint64_t more;
       while (static_cast<int>(grp.size()) < std::min(max_group_, kMaxGroup) && st.peek_front(&more)) {

@@ -161,6 +161,9 @@ class Session {
     size_t staging_cap = 0, outbuf_cap = 0;
     float* ws = nullptr;      // split-K partial sums (grown on demand)
     size_t ws_cap = 0;
+    void* gout = nullptr;     // C tiles of a grouped launch with host outputs (grown on demand)
+    size_t gout_cap = 0;
+    EvRef gout_free;          // the writeback stream's D2H of gout's previous contents
   };
   struct TimedLaunch {
     cudaEvent_t start, end;
@@ -172,6 +175,7 @@ class Session {
   struct DeviceCtx {
     int id = 0, gpu = 0, width = 4, max_inflight = 2;
     int sms = 148;  // multiprocessors this device runs on (split-K sizing, persistent grids)
+    bool host_fills = false;  // the current job still fills tiles from host memory (see run_job)
     CUgreenCtx green = nullptr;  // sm_count > 0: the green context holding its SMs
     int green_sms = 0;
     int64_t capacity = -1;
@@ -212,6 +216,7 @@ class Session {
   bool plan_narrow(int d, StreamCtx& sc, GemmArgs& args, GemmArgs& t);
   void use_workspace(int d, StreamCtx& sc, GemmArgs& args, int splits, int64_t ws_ld);
   float* workspace(int d, StreamCtx& sc, size_t bytes);
+  bool group_outbuf(int d, int s, size_t bytes);
   int group_split(int d, const GemmGroup& grp, bool pair) const;
   // write-through: reserve the cache slot for output tile (i, j) of p and point
   // args at its planes; returns the physical slot (-1: not written through)
