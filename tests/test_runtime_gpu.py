@@ -431,6 +431,30 @@ def test_kpanel_schedule_cold_product(precision):
     assert rel(res["auto"], res["shells"]) <= 1e-6 if precision == "fp32acc" else 1e-3
 
 
+def test_host_output_grouped_launches():
+    """Tasks with HOST outputs run as grouped launches (C tiles in the stream's
+    group buffer, written back on the writeback stream): non-persistent while
+    host tiles are still being filled (cold), persistent once every input is
+    resident (warm re-multiply).  Integer inputs are exact, ragged edges
+    included; both runs give the same bits and the reference's counters."""
+    rng = np.random.default_rng(41)
+    m, k, n, T = 1100, 1300, 1000, 256  # 5 x 4 tasks, 6 k-steps, ragged edges
+    a, b = int_matrix(rng, m, k).astype(np.float32), int_matrix(rng, k, n).astype(np.float32)
+    gm, gn, gk = -(-m // T), -(-n // T), -(-k // T)
+    ref = O.reference_gemm(a.astype(np.float64), b.astype(np.float64))
+    with Runtime(homogeneous_machine(1, dtype=np.float32), T) as rt:
+        rt.set_order("shells")  # the task path (not the k-panel schedule)
+        c1, s1 = rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C1")
+        assert np.array_equal(c1, ref)
+        assert s1.cache.host_fetches == gm * gk + gk * gn and s1.cache.writebacks == gm * gn
+        assert s1.gpu_launches - s1.cache.host_fetches < gm * gn  # converts + fewer GEMM launches than tasks
+        c2, s2 = rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C2")
+        assert s2.cache.host_fetches == 0 and s2.cache.writebacks == gm * gn
+        assert s2.gpu_launches < gm * gn
+        assert np.array_equal(c1, c2)
+        assert s2.tasks_by_device == {0: gm * gn}
+
+
 def test_host_slices_read_in_place():
     """Row slices of A, column slices of B and a sub-block of C are read and
     written in place (pitched copies with the parent's row stride)."""
