@@ -475,7 +475,10 @@ def bench_ooc_full(args, tr, torch, peaks_tf):
            "gpu_launches": stats.gpu_launches,
            "roofline": {"time_ms": t_roof * 1e3, "frac": t_roof / t,
                         "def": "max(2N^3 / (bf16 burst peak / 3), bytes_host / 55.6 GB/s, bytes_writeback / 56 GB/s)"},
-           "parity_rel_fro_sampled": parity}
+           "parity_rel_fro_sampled": parity,
+           "sim_reference_schedule_ms": {str(w): sim_prediction_ms(tr, n, T, w, args.precision) for w in (1, 2, 4, 8)},
+           "sim_note": "the reference's own schedule (its sim engine, replayed bit-exactly) on this B200's measured "
+                       "rates at 1/2/4/8 GPUs (NVLink assumed 720 GB/s): a model, not a measurement"}
     del a, c, at
     torch._C._host_emptyCache()
     return out
@@ -518,7 +521,8 @@ def sim_prediction_ms(tr, n, T, world, precision):
     bit-exactly by mode="sim") fed this B200's measured rates: what the reference's
     schedule -- no fetch-ahead, fetch/writeback on one transfer clock -- would take
     for the same cold product.  A model, not a measurement."""
-    z = np.lib.stride_tricks.as_strided(np.zeros(1, np.float32), (n, n), (0, 0))  # never read
+    # a row-major descriptor over one element: mode="sim" with compute=False never reads it
+    z = np.lib.stride_tricks.as_strided(np.zeros(1, np.float32), (n, n), (n * 4, 4))
     with tr.Runtime(tr.b200_sim_machine(world, precision), T, mode="sim", compute=False) as rt:
         _, s = rt.multiply(z, z)
     return s.makespan * 1e3
