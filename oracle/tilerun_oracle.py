@@ -100,6 +100,36 @@ def gemm_slice(a, b, rows, cols, dtype=np.float64):
     return reference_gemm(sa, sb)
 
 
+def band_samples(n: int, tile: int, per_band: int = 8, seed: int = 0) -> np.ndarray:
+    """Sample indices for a sampled-slice check: at least
+    ``per_band`` distinct indices in EVERY tile band [b*T, min((b+1)*T, n)) --
+    both band edges plus seeded interior picks -- so every tile row/column of
+    the task grid, the ragged last band included, is checked.  Sorted, unique."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for lo in range(0, n, tile):
+        hi = min(lo + tile, n)
+        width = hi - lo
+        if width <= per_band:
+            out.extend(range(lo, hi))
+            continue
+        pick = {lo, hi - 1}
+        while len(pick) < per_band:
+            pick.add(lo + int(rng.integers(0, width)))
+        out.extend(sorted(pick))
+    return np.unique(np.asarray(out, dtype=np.int64))
+
+
+def sampled_rel_error(a_rows, b_cols, got) -> float:
+    """Relative Frobenius error of a sampled block ``got`` = C[rows][:, cols]
+    against the k-ascending float64 product of A[rows, :] and B[:, cols]
+    (the C restatement; bit-identical to reference_gemm on float64)."""
+    ref = gemm_slice(np.asarray(a_rows, np.float64), np.asarray(b_cols, np.float64),
+                     np.arange(np.shape(a_rows)[0]), np.arange(np.shape(b_cols)[1]))
+    den = np.linalg.norm(ref)
+    return float(np.linalg.norm(np.asarray(got, np.float64) - ref) / (den if den else 1.0))
+
+
 # ----------------------------------------------------------------- scheduler.py: plan
 
 

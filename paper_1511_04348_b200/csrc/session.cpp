@@ -335,6 +335,8 @@ void Session::ensure_slab(int d, int64_t needed) {
   }
   if (e != cudaSuccess) {
     cudaGetLastError();
+    // a slab that cannot grow still serves the job: the directory evicts into it
+    if (dc.slab_slots >= 3) return;
     fail(TR_ERR_CAPACITY, "device %d: cannot allocate a %lld-slot tile slab (%s)", d, (long long)grow,
          cudaGetErrorString(e));
   }
@@ -1557,10 +1559,23 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
       reg.ensure(p.b);
       reg.ensure(p.c);
     }
-    int64_t in_tiles = 0;
-    for (const Product& p : job.prods)
-      in_tiles += ceil_div(p.a.rows, T) * ceil_div(p.a.cols, T) + ceil_div(p.b.rows, T) * ceil_div(p.b.cols, T);
-    for (int d = 0; d < n_devices(); ++d) ensure_slab(d, dir_->used_tiles(d) + in_tiles);
+    // slab room for this job: the tiles already cached plus the job's input tiles
+    // not yet resident on the device (a warm re-multiply needs no growth)
+    for (int d = 0; d < n_devices(); ++d) {
+      int64_t missing = 0;
+      {
+        std::lock_guard<std::mutex> g(dir_->mu);
+        for (const Product& p : job.prods)
+          for (int which = 0; which < 2; ++which) {
+            const Mat& m = which == 0 ? p.a : p.b;
+            const uint64_t uid = which == 0 ? p.a_uid : p.b_uid;
+            for (int64_t r = 0; r < ceil_div(m.rows, T); ++r)
+              for (int64_t c = 0; c < ceil_div(m.cols, T); ++c)
+                missing += !(dir_->owners_locked(TileKey{uid, r, c}) >> d & 1);
+          }
+      }
+      ensure_slab(d, dir_->used_tiles(d) + missing);
+    }
   }
   // out-of-core (the inputs exceed the HBM slab, capacity unbounded): the
   // directory learns every input tile's remaining requests so that physical

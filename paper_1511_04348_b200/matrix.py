@@ -18,6 +18,22 @@ def _torch():
     return torch
 
 
+class ShapeOnly:
+    """A matrix known by shape and dtype only, with no data: an operand for
+    ``mode="sim"`` / ``"dryrun"`` runs with ``compute=False``, which schedule,
+    count and time a product without reading it.  A computing run rejects it
+    (ValueError) instead of reading memory that does not exist."""
+
+    ndim = 2
+
+    def __init__(self, rows: int, cols: int, dtype=np.float32):
+        if rows < 1 or cols < 1:
+            raise ValueError(f"need a non-empty 2-D shape, got ({rows}, {cols})")
+        self.shape = (int(rows), int(cols))
+        self.dtype = np.dtype(dtype)
+        dtype_code(self.dtype)
+
+
 def is_device_tensor(x) -> bool:
     t = type(x)
     return t.__module__.startswith("torch") and getattr(x, "is_cuda", False)

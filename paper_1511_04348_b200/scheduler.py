@@ -34,7 +34,7 @@ from .coherence import CacheDirectory, CacheStats, UidTable
 from .dense import precision_code
 from .devices import Machine
 from .errors import NoDeviceError
-from .matrix import describe, is_device_tensor, pinned_empty, pinned_zeros
+from .matrix import ShapeOnly, describe, is_device_tensor, pinned_empty, pinned_zeros
 from .msqueue import MichaelScottQueue
 from .tiles import TiledMatrix, TileKey, decode_task, partition
 
@@ -508,6 +508,8 @@ class Runtime:
 
         stats = self._execute(call, total, lambda t: t % task_stride == task_offset)
         if self.mode == "sim" and self.compute:
+            if isinstance(a_op.tiled.base, ShapeOnly) or isinstance(b_op.tiled.base, ShapeOnly):
+                raise ValueError("ShapeOnly operands carry no data: use Runtime(..., compute=False)")
             out = self._sim_product(a_op, b_op, out)
         return out, stats
 
@@ -644,10 +646,14 @@ class Runtime:
 
     @staticmethod
     def _prep(x):
-        return x if is_device_tensor(x) else _host_matrix(x)
+        return x if is_device_tensor(x) or isinstance(x, ShapeOnly) else _host_matrix(x)
 
     @staticmethod
     def _desc(x, dry, shape=None, dtype=None) -> N.MatrixC:
+        if isinstance(x, ShapeOnly):
+            if not dry:
+                raise ValueError("ShapeOnly operands carry no data: only mode='sim'/'dryrun' runs take them")
+            shape, dtype, x = x.shape, x.dtype, None
         if x is None:  # dry run: shape-only descriptor
             from .matrix import dtype_code
 

@@ -180,3 +180,11 @@ def test_cfg1_sampled_slices_and_checksums(c_lib):
     host_fetches, bytes_host, hits, writebacks, bytes_wb, tasks = g["stats"]
     assert host_fetches == 2 * 4 * 4 and bytes_host == 32 * 512 * 512 * 4
     assert hits + host_fetches == 2 * 16 * 4 and writebacks == tasks == 16
+
+
+def test_band_samples_cover_every_band():
+    """Sampled-slice indices: >= 8 per tile band, band edges included (ragged last band too)."""
+    idx = O.band_samples(10000, 4096, per_band=8, seed=3)
+    for lo in range(0, 10000, 4096):
+        band = idx[(idx >= lo) & (idx < min(lo + 4096, 10000))]
+        assert len(band) >= 8 and band[0] == lo and band[-1] == min(lo + 4096, 10000) - 1
