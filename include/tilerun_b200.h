@@ -177,6 +177,7 @@ typedef struct {
 
 typedef struct {
   int64_t tasks_completed, steals_performed, steals_suffered; /* scheduler.py:261-267 */
+  int64_t peer_copies_served; /* B200 addition: L2 fills this device sourced over NVLink / D2D */
 } tr_device_stats;
 
 typedef struct {

@@ -63,7 +63,8 @@ class MatrixC(C.Structure):
 
 
 class DeviceStatsC(C.Structure):
-    _fields_ = [("tasks_completed", i64), ("steals_performed", i64), ("steals_suffered", i64)]
+    _fields_ = [("tasks_completed", i64), ("steals_performed", i64), ("steals_suffered", i64),
+                ("peer_copies_served", i64)]
 
 
 class StealEventC(C.Structure):

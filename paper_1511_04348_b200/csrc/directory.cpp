@@ -63,6 +63,24 @@ int Directory::closest_owner(int requester, uint64_t owners) const {
   return best;
 }
 
+int32_t Directory::balanced_source_locked(int requester, const TileKey& key, const std::vector<int64_t>& load) const {
+  auto it = residency_.find(key);
+  const uint64_t owners = (it == residency_.end() ? 0 : it->second) & ~(1ull << requester);
+  int best = -1;
+  int64_t best_h = 0, best_l = 0;
+  for (int o = 0; o < n_; ++o) {
+    if (!(owners >> o & 1)) continue;
+    const int64_t h = hops_[static_cast<int64_t>(requester) * n_ + o];
+    const int64_t l = o < static_cast<int>(load.size()) ? load[o] : 0;
+    if (best < 0 || h < best_h || (h == best_h && l < best_l)) {
+      best = o;
+      best_h = h;
+      best_l = l;
+    }
+  }
+  return best;
+}
+
 void Directory::attach_slots(int device, int32_t n_slots) {
   Dev& d = dev_[device];
   // stack: the lowest new index is handed out first

@@ -106,6 +106,12 @@ class Directory {
   void set_future_locked(std::unordered_map<TileKey, int64_t, TileKeyHash> future);
   void clear_future_locked();
   int32_t slot_of_locked(int device, const TileKey& key) const;
+  // Physical source of an L2 fill of `key` into `requester` on a uniform
+  // (NVSwitch) fabric: among the other owners with the fewest hops, the one
+  // with the least `load` (copies it has served in this job), ties to the lowest
+  // id.  The reference's closest_owner (devices.py:285-291) sends every fill to
+  // the lowest-id owner; counters do not depend on the choice.  -1: no owner.
+  int32_t balanced_source_locked(int requester, const TileKey& key, const std::vector<int64_t>& load) const;
   // Owners of `key` (bitmask over device ids).
   uint64_t owners_locked(const TileKey& key) const;
   // Bind device `d` to `n_slots` physical slots [0, n_slots).  May be called again to grow.

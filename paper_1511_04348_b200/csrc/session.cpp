@@ -502,7 +502,12 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
   if (level == HIT_L2) {
     // peer copy of the already-converted planes, on the copy stream
     wait_slot_free(d, X, phys);
-    const int o = source;
+    // load-aware source: the directory's closest owner (the reference's choice)
+    // unless another equally close owner has served fewer copies in this job
+    int o = dir_->balanced_source_locked(d, key, peer_served_);
+    if (o < 0) o = source;
+    peer_served_[o] += 1;
+    devs_[o].stats.peer_copies_served += 1;
     const int32_t src_phys = phys_of(o, dir_->slot_of_locked(o, key));
     SlotState& ss = devs_[o].slots[src_phys];
     wait_on(d, X, ss.ready);
@@ -1542,6 +1547,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     dc.station->clear();
     dc.stats = tr_device_stats{};
   }
+  peer_served_.assign(devs_.size(), 0);
 
   int prev_dev = 0;
   if (!dryrun_) cudaGetDevice(&prev_dev);

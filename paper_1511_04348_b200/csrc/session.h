@@ -285,6 +285,7 @@ class Session {
   std::unique_ptr<Directory> dir_;
   std::vector<DeviceCtx> devs_;
   std::vector<Station*> station_ptrs_;
+  std::vector<int64_t> peer_served_;  // L2 fills each device sourced in the current job (under dir_->mu)
 
   // worker coordination
   std::mutex mu_;

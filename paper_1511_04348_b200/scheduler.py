@@ -274,6 +274,7 @@ class DeviceStats:
     tasks_completed: int = 0
     steals_performed: int = 0
     steals_suffered: int = 0
+    peer_copies_served: int = 0  # B200: L2 fills sourced from this device (not in report schema v1)
 
 
 @dataclass
@@ -617,7 +618,8 @@ class Runtime:
             k_steps=int(rep.k_steps), total_tasks=int(rep.total_tasks), steal_enabled=self.steal,
             coherence_enabled=self.coherence, seed=self.seed,
             devices={d: DeviceStats(d, self.machine.devices[d].kind, int(per_dev[d].tasks_completed),
-                                    int(per_dev[d].steals_performed), int(per_dev[d].steals_suffered))
+                                    int(per_dev[d].steals_performed), int(per_dev[d].steals_suffered),
+                                    int(per_dev[d].peer_copies_served))
                      for d in range(n)},
             cache=CacheStats.from_c(rep.cache),
             cache_per_device={d: CacheStats.from_c(per_cache[d]) for d in range(n)},

@@ -53,3 +53,40 @@ def test_two_rank_task_sharding(tmp_path):
         assert requests == 2 * 63 * 5 and writebacks == 63
         assert r["tmax"] == 2.0
     assert [r["mine"] for r in res] == [32, 31]
+
+
+def _bench_worker(rank, world, port, out_dir):
+    """bench.py's torchrun plumbing: rank 0 alone drives the N-GPU machine (here a
+    dry-run machine of N logical devices), the other ranks only join the max."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import bench
+    import paper_1511_04348_b200 as tr
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    coord = bench.Coordinator(env={"WORLD_SIZE": str(world), "RANK": str(rank)})
+    args = bench.parse(["--gpus", "1"])
+    ng = bench.n_gpus_for(args, coord.world)
+    t_local, tasks = 0.0, None
+    if coord.rank == 0:
+        with tr.Runtime(tr.homogeneous_machine(ng), 4, mode="dryrun") as rt:
+            _, s = rt.multiply(np.zeros((36, 20)), np.zeros((20, 28)), a_uid="A", b_uid="B")
+        tasks = s.tasks_by_device
+        t_local = 2.5
+    t = coord.max_over_ranks(t_local)
+    coord.close()
+    with open(os.path.join(out_dir, f"b{rank}.json"), "w") as f:
+        json.dump({"ng": ng, "t": t, "tasks": tasks}, f)
+
+
+@pytest.mark.timeout(180)
+def test_bench_one_process_drives_all_gpus(tmp_path):
+    world = 2
+    mp.start_processes(_bench_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True,
+                       start_method="spawn")
+    r0, r1 = (json.loads((tmp_path / f"b{r}.json").read_text()) for r in range(world))
+    assert r0["ng"] == r1["ng"] == 2  # --gpus 1 under WORLD_SIZE=2: one process, two GPUs
+    assert r0["t"] == r1["t"] == 2.5  # max over ranks; rank 1 did no work
+    assert r1["tasks"] is None and sum(r0["tasks"].values()) == 9 * 7 and len(r0["tasks"]) == 2
