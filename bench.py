@@ -771,36 +771,15 @@ def bench_mlp_wide(args, tr, torch, gpus):
             "h2d_bytes_per_step": int(xh.nbytes + th.nbytes), "d2h_bytes_per_step": 8}
 
 
-def standalone_rates(tr, torch, sms, gpu, a, b, c, T, precision, reps=2):
-    """Each green-context device size's own throughput (flop/s): the product on a
-    one-device machine of that many SMs, warm, best of ``reps``."""
-    rates = []
-    flops = 2.0 * a.shape[0] * a.shape[1] * b.shape[1]
-    for k in sms:
-        m = tr.Machine([tr.DeviceSpec(0, gpu=gpu, sms=k)], tr.ProximityMatrix.uniform(1), dtype=np.float32)
-        with tr.Runtime(m, T, precision=precision) as rt:
-            rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
-            best = float("inf")
-            for _ in range(reps):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                torch.cuda.synchronize()
-                e0.record()
-                rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
-                e1.record()
-                torch.cuda.synchronize()
-                best = min(best, e0.elapsed_time(e1) / 1e3)
-        rates.append(flops / best)
-    return rates
-
-
 def bench_inhomogeneous(tr, torch, precision, gpu):
     """BASELINE cfg5's inhomogeneous devices on one GPU: four logical devices on
-    green contexts of 8 / 16 / 24 / 32 SMs share a N=16384 product (T=2048, 64
-    tasks) through the dynamic scheduler.  Each device's standalone rate is
-    measured first (the same product on that device alone); its task share in
-    the shared run must be within 10 % (relative) of its share of the summed
-    standalone rates (tests/test_acceptance.py:130-141)."""
-    n, T = 16384, 2048
+    green contexts of 8 / 16 / 24 / 32 SMs share a 32 x 32 task grid (N=32768,
+    T=1024: the reference's acceptance shape, test_acceptance.py:130-141)
+    through the dynamic scheduler.  Each device's standalone throughput is
+    measured first (tr.standalone_rates on a 256-task row slab of the same
+    product); its share of the work (rows x cols x K of its tasks) in the shared
+    run must be within 10 % (relative) of its share of the summed rates."""
+    n, T = 32768, 1024
     g = torch.Generator(device="cuda").manual_seed(5)
     a = torch.randn(n, n, device="cuda", generator=g)
     b = torch.randn(n, n, device="cuda", generator=g)
@@ -808,26 +787,27 @@ def bench_inhomogeneous(tr, torch, precision, gpu):
     sms = [8, 16, 24, 32]
     specs = [tr.DeviceSpec(i, gpu=gpu, sms=k) for i, k in enumerate(sms)]
     m = tr.Machine(specs, tr.ProximityMatrix.uniform(len(sms)), dtype=np.float32)
-    rates = standalone_rates(tr, torch, sms, gpu, a, b, c, T, precision)
+    rates = tr.standalone_rates(m, T, a[: 8 * T], b, out=c[: 8 * T], precision=precision)
     with tr.Runtime(m, T, precision=precision) as rt:
         rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
-        tasks = np.zeros(len(sms))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _ in range(3):
-            _, st = rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
-            tasks += [st.tasks_by_device[d] for d in range(len(sms))]
+        _, st = rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
         e1.record()
         torch.cuda.synchronize()
-    share = tasks / tasks.sum()
+    work = np.array([st.devices[d].macs for d in range(len(sms))], dtype=np.float64)
+    share = work / work.sum()
     ideal = np.asarray(rates) / sum(rates)
     relerr = np.abs(share - ideal) / ideal
-    return {"workload": "4 green-context devices of 8/16/24/32 SMs on one B200, N=16384 T=2048 (64 tasks) x 3",
+    ms = e0.elapsed_time(e1)
+    return {"workload": "4 green-context devices of 8/16/24/32 SMs on one B200, N=32768 T=1024 (32 x 32 tasks)",
             "standalone_tflops": [round(r / 1e12, 2) for r in rates],
-            "task_share": [round(float(x), 4) for x in share], "rate_share": [round(float(x), 4) for x in ideal],
+            "tasks": [st.tasks_by_device[d] for d in range(len(sms))], "steals": len(st.steal_events),
+            "work_share": [round(float(x), 4) for x in share], "rate_share": [round(float(x), 4) for x in ideal],
             "max_rel_share_error": float(relerr.max()), "criterion": "<= 0.10 relative (test_acceptance.py:137-141)",
-            "ms_per_product": e0.elapsed_time(e1) / 3, "tflops": 2.0 * n ** 3 / (e0.elapsed_time(e1) / 3e3) / 1e12}
+            "ms_per_product": ms, "tflops": 2.0 * n ** 3 / (ms / 1e3) / 1e12,
+            "sum_of_standalone_tflops": sum(rates) / 1e12}
 
 
 def bench_ooc(args, tr, torch, peaks, links, gpu):

@@ -178,6 +178,7 @@ typedef struct {
 typedef struct {
   int64_t tasks_completed, steals_performed, steals_suffered; /* scheduler.py:261-267 */
   int64_t peer_copies_served; /* B200 addition: L2 fills this device sourced over NVLink / D2D */
+  int64_t macs;               /* B200 addition: sum over completed tasks of rows x cols x K (work share) */
 } tr_device_stats;
 
 typedef struct {
@@ -259,6 +260,11 @@ int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
  * measured with CUDA events on the launching streams (sum over launches). */
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms /* n_devices */);
+/* The directory lock's accounting since the last reset: out[0] ns held, out[1] ns
+ * callers waited to acquire it, out[2] acquisitions, out[3] longest hold (ns).
+ * reset != 0 zeroes it after reading.  B200 addition (coherence.py:202-209 makes
+ * every directory operation one critical section; this measures its cost). */
+int tr_session_lock_stats(tr_session* s, int32_t reset, int64_t* out /* 4 */);
 /* Timeline of the last tr_gemm (sessions created with TR_FLAG_TRACE): one entry
  * per H2D tile copy, split/convert, peer copy, GEMM launch and D2H writeback,
  * with CUDA-event times in ms relative to the product's start on that device. */

@@ -64,7 +64,7 @@ class MatrixC(C.Structure):
 
 class DeviceStatsC(C.Structure):
     _fields_ = [("tasks_completed", i64), ("steals_performed", i64), ("steals_suffered", i64),
-                ("peer_copies_served", i64)]
+                ("peer_copies_served", i64), ("macs", i64)]
 
 
 class StealEventC(C.Structure):
@@ -136,6 +136,7 @@ _PROTOS = {
                       P(GemmReportC)],
     "tr_gemm_batch": [vp, i32, P(ProductC), P(GemmReportC)],
     "tr_session_kernel_ms": [vp, P(f64)],
+    "tr_session_lock_stats": [vp, i32, P(i64)],
     "tr_session_span_ms": [vp, P(f64)],
     "tr_session_trace": [vp, vp, i64, P(i64)],
     "tr_session_set_inflight": [vp, i32],

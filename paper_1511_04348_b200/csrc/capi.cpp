@@ -341,6 +341,13 @@ int tr_gemm(tr_session* s, const tr_matrix* a, uint64_t a_uid, int32_t ta, const
             int32_t tb, const tr_matrix* c, uint64_t c_uid, tr_gemm_report* report) {
   return tr_gemm_shard(s, a, a_uid, ta, b, b_uid, tb, c, c_uid, 0, 1, report);
 }
+int tr_session_lock_stats(tr_session* s, int32_t reset, int64_t* out) {
+  return guarded([&] {
+    if (!out) tr::fail(TR_ERR_VALUE, "null output");
+    s->s->directory().mu.stats(&out[0], &out[1], &out[2], &out[3]);
+    if (reset) s->s->directory().mu.reset();
+  });
+}
 int tr_session_kernel_ms(tr_session* s, double* per_device_ms) {
   return guarded([&] { s->s->kernel_ms(per_device_ms); });
 }
@@ -459,7 +466,7 @@ int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
 }
 int tr_session_forget(tr_session* s, uint64_t uid, int64_t* dropped) {
   return guarded([&] {
-    std::lock_guard<std::mutex> g(s->s->directory().mu);
+    tr::DirLock g(s->s->directory().mu);
     const int64_t n = s->s->directory().forget_locked(uid);
     if (dropped) *dropped = n;
   });

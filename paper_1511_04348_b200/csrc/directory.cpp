@@ -419,65 +419,65 @@ void Directory::check_invariants_locked() {
 
 // ---- self-locking wrappers
 HitLevel Directory::lookup(int requester, const TileKey& key, int32_t* owner) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return lookup_locked(requester, key, owner);
 }
 std::vector<TileKey> Directory::admit(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return admit_locked(device, key, false, nullptr);
 }
 void Directory::pin(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   if (!dev_[device].entries.count(key))
     fail(TR_ERR_VALUE, "cannot pin tile (%llu,%lld,%lld): not resident on device %d", (unsigned long long)key.matrix,
          (long long)key.row, (long long)key.col, device);
   dev_[device].pins[key] += 1;
 }
 void Directory::unpin(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   unpin_locked(device, key);
 }
 bool Directory::is_pinned(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   auto it = dev_[device].pins.find(key);
   return it != dev_[device].pins.end() && it->second > 0;
 }
 std::vector<TileKey> Directory::residents(int device) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return std::vector<TileKey>(dev_[device].order.begin(), dev_[device].order.end());
 }
 int64_t Directory::used_tiles(int device) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return static_cast<int64_t>(dev_[device].order.size());
 }
 Acquired Directory::acquire_input(int requester, const TileKey& key, int64_t nbytes) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return acquire_input_locked(requester, key, nbytes);
 }
 void Directory::release_input(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   release_input_locked(device, key);
 }
 std::vector<TileKey> Directory::admit_output(int device, const TileKey& key) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return admit_output_locked(device, key);
 }
 void Directory::release_output(int device, const TileKey& key, int64_t nbytes) {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   release_output_locked(device, key, nbytes);
 }
 tr_cache_stats Directory::stats() {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   return stats_;
 }
 std::vector<tr_cache_stats> Directory::stats_per_device() {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   std::vector<tr_cache_stats> out;
   for (const Dev& d : dev_) out.push_back(d.stats);
   return out;
 }
 void Directory::check_invariants() {
-  std::lock_guard<std::mutex> g(mu);
+  DirLock g(mu);
   check_invariants_locked();
 }
 

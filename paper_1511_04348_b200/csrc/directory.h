@@ -13,6 +13,7 @@
 // the same LRU/pin rules the counters follow.
 #pragma once
 
+#include <chrono>
 #include <cstdint>
 #include <list>
 #include <mutex>
@@ -22,6 +23,45 @@
 #include "../../include/tilerun_b200.h"
 
 namespace tr {
+
+// The directory lock, instrumented: total time held, time callers waited for it,
+// acquisitions and the longest hold (tr_session_lock_stats).  Two steady_clock
+// reads per acquisition.
+class DirMutex {
+ public:
+  void lock() {
+    const auto t0 = std::chrono::steady_clock::now();
+    m_.lock();
+    t_lock_ = std::chrono::steady_clock::now();
+    wait_ns_ += std::chrono::duration_cast<std::chrono::nanoseconds>(t_lock_ - t0).count();
+    count_ += 1;
+  }
+  void unlock() {
+    const int64_t held =
+        std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t_lock_).count();
+    hold_ns_ += held;
+    if (held > max_hold_ns_) max_hold_ns_ = held;
+    m_.unlock();
+  }
+  // snapshot / reset (caller does not hold the lock)
+  void stats(int64_t* hold_ns, int64_t* wait_ns, int64_t* count, int64_t* max_hold_ns) {
+    std::lock_guard<std::mutex> g(m_);
+    *hold_ns = hold_ns_;
+    *wait_ns = wait_ns_;
+    *count = count_;
+    *max_hold_ns = max_hold_ns_;
+  }
+  void reset() {
+    std::lock_guard<std::mutex> g(m_);
+    hold_ns_ = wait_ns_ = count_ = max_hold_ns_ = 0;
+  }
+
+ private:
+  std::mutex m_;
+  std::chrono::steady_clock::time_point t_lock_;
+  int64_t hold_ns_ = 0, wait_ns_ = 0, count_ = 0, max_hold_ns_ = 0;  // written under m_
+};
+using DirLock = std::lock_guard<DirMutex>;
 
 struct TileKey {
   uint64_t matrix;
@@ -78,7 +118,7 @@ class Directory {
   void check_invariants();
 
   // ---- for the session: caller holds `mu`
-  std::mutex mu;
+  DirMutex mu;
   HitLevel lookup_locked(int requester, const TileKey& key, int32_t* owner);
   std::vector<TileKey> admit_locked(int device, const TileKey& key, bool input, int32_t* slot_out);
   Acquired acquire_input_locked(int requester, const TileKey& key, int64_t nbytes);

@@ -350,7 +350,7 @@ void Session::ensure_slab(int d, int64_t needed) {
   dc.slab_slots = static_cast<int32_t>(grow);
   dc.slots.resize(static_cast<size_t>(grow + scratch));
   {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     dir_->attach_slots(d, dc.slab_slots);
   }
   build_tmaps(d);
@@ -465,7 +465,7 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
   const int64_t nbytes = std::min(T, src.rows - r * T) * std::min(T, src.cols - c * T) * element_bytes_;
   const TileKey key{uid, r, c};
   const int32_t gs = gs_of(d, s);
-  std::lock_guard<std::mutex> g(dir_->mu);
+  DirLock g(dir_->mu);
   Acquired a = dir_->acquire_input_locked(d, key, nbytes);
   if (dryrun_) return a.slot;
   if (!coherence_) {
@@ -581,7 +581,7 @@ bool Session::prefetch_task(int d, Job& job, int64_t gtid, bool host_only, int64
       const int64_t r = which == 0 ? (t ? k : i) : (t ? j : k);
       const int64_t c = which == 0 ? (t ? i : k) : (t ? k : j);
       const TileKey key{uid, r, c};
-      std::lock_guard<std::mutex> g(dir_->mu);
+      DirLock g(dir_->mu);
       int32_t slot = -1, source = TR_SOURCE_HOST;
       if (!dir_->prefetch_locked(d, key, &slot, &source, host_only)) continue;
       load_slot(d, s, phys_of(d, slot), source >= 0 ? HIT_L2 : HIT_MISS, source, key, m, r, c, job);
@@ -847,7 +847,7 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     const int64_t i = tid / p.grid_cols, j = tid % p.grid_cols;
     const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
     {
-      std::lock_guard<std::mutex> g(dir_->mu);
+      DirLock g(dir_->mu);
       dir_->admit_output_locked(d, TileKey{p.c_uid, i, j});
     }
     GemmArgs& args = grp.task[q];
@@ -950,7 +950,7 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   job.launches.fetch_add(1);
   EvRef kernel_done;
   {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     const EvRef ev = record(d, s);
     kernel_done = ev;
     for (int32_t ph : used_phys) note_use(dc.slots[ph], ev);
@@ -986,13 +986,14 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
                                 cudaMemcpyDeviceToHost, dc.streams[wb].stream));
       trace_end(d, wb, tw, TR_TRACE_D2H, gtids[q], p.c_uid, i, j);
     }
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     sc.gout_free = record(d, wb);
   }
   if (job.async) {
     for (int64_t gt : gtids) {
       job.mark(gt);
       dc.stats.tasks_completed += 1;
+      dc.stats.macs += job.task_macs(gt, tile_);
     }
     return;
   }
@@ -1013,7 +1014,7 @@ int32_t Session::write_through(int d, int s, const Product& p, int64_t i, int64_
   const int64_t T = tile_;
   if (T % 256 != 0 || std::min(T, p.M - i * T) != T || std::min(T, p.N - j * T) != T) return -1;
   if ((args.ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(args.c) & 15) != 0) return -1;
-  std::lock_guard<std::mutex> g(dir_->mu);
+  DirLock g(dir_->mu);
   int32_t slot = -1, source = TR_SOURCE_HOST;
   if (!dir_->prefetch_locked(d, TileKey{p.cache_as, i, j}, &slot, &source, false)) return -1;
   const int32_t phys = phys_of(d, slot);
@@ -1042,7 +1043,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
   else if (dc.capacity >= 0 && dc.capacity < 2 * ks + 1) chunk = std::max<int64_t>(1, (dc.capacity - 1) / 2);
   chunk = std::min<int64_t>(chunk, kMaxKSteps);
   {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     dir_->admit_output_locked(d, c_key);  // pinned for the whole task (scheduler.py:390)
   }
   StreamCtx* scp = dryrun_ ? nullptr : &dc.streams[s];
@@ -1146,7 +1147,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
       job.launches.fetch_add(1);
     }
     {
-      std::lock_guard<std::mutex> g(dir_->mu);
+      DirLock g(dir_->mu);
       if (!dryrun_ && coherence_) {
         const EvRef ev = record(d, s);
         for (int32_t p : used_phys) note_use(dc.slots[p], ev);
@@ -1168,12 +1169,13 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     trace_end(d, s, tw, TR_TRACE_D2H, gtid, p.c_uid, i, j);
   }
   {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     dir_->release_output_locked(d, c_key, wb_bytes);  // coherence.py:263-280
   }
   if (dryrun_ || job.async) {  // async: the task completes in stream order
     job.mark(gtid);
     dc.stats.tasks_completed += 1;
+    dc.stats.macs += job.task_macs(gtid, tile_);
     return;
   }
   TR_CUDA(cudaEventRecord(scp->done, scp->stream));
@@ -1197,9 +1199,11 @@ void Session::reap(int d, Job& job, bool block_oldest) {
     TR_CUDA(e);
     job.mark(sc.task);
     dc.stats.tasks_completed += 1;
+    dc.stats.macs += job.task_macs(sc.task, tile_);
     for (int64_t gt : sc.group_rest) {
       job.mark(gt);
       dc.stats.tasks_completed += 1;
+      dc.stats.macs += job.task_macs(gt, tile_);
     }
     sc.group_rest.clear();
     sc.task = -1;
@@ -1225,7 +1229,7 @@ void Session::run_job(int d, Job& job) {
   // tensor cores per 11.6 s product persistent, 0.13 s non-persistent).
   dc.host_fills = false;
   if (!dryrun_) {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     for (const Product& p : job.prods) {
       for (int which = 0; which < 2 && !dc.host_fills; ++which) {
         const Mat& m = which == 0 ? p.a : p.b;
@@ -1270,7 +1274,7 @@ void Session::run_job(int d, Job& job) {
         const Product& p = job.prod_of(static_cast<int64_t>(t), &lt);
         const int64_t i = lt / p.grid_cols, j = lt % p.grid_cols;
         int score = 0;
-        std::lock_guard<std::mutex> g(dir_->mu);
+        DirLock g(dir_->mu);
         for (int64_t k = 0; k < p.k_steps; ++k) {
           const uint64_t oa = dir_->owners_locked(TileKey{p.a_uid, p.ta ? k : i, p.ta ? i : k});
           const uint64_t ob = dir_->owners_locked(TileKey{p.b_uid, p.tb ? j : k, p.tb ? k : j});
@@ -1570,7 +1574,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     for (int d = 0; d < n_devices(); ++d) {
       int64_t missing = 0;
       {
-        std::lock_guard<std::mutex> g(dir_->mu);
+        DirLock g(dir_->mu);
         for (const Product& p : job.prods)
           for (int which = 0; which < 2; ++which) {
             const Mat& m = which == 0 ? p.a : p.b;
@@ -1594,7 +1598,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     bool on;
     ~FutureGuard() {
       if (!on) return;
-      std::lock_guard<std::mutex> g(dir->mu);
+      DirLock g(dir->mu);
       dir->clear_future_locked();
     }
   } future_guard{dir_.get(), job.out_of_core};
@@ -1609,7 +1613,7 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
         future[TileKey{p.b_uid, p.tb ? j : k, p.tb ? k : j}] += 1;
       }
     }
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     dir_->set_future_locked(std::move(future));
   }
   const tr_cache_stats before = dir_->stats();

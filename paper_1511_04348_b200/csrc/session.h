@@ -98,6 +98,15 @@ struct Job {
     return prods[lo];
   }
   void mark(int64_t tid);  // scheduler.py:78-83
+  // rows x cols x K of global task g (its share of the work)
+  int64_t task_macs(int64_t g, int64_t tile) const {
+    int64_t t = 0;
+    const Product& p = prod_of(g, &t);
+    const int64_t i = t / p.grid_cols, j = t % p.grid_cols;
+    const int64_t mt = p.M - i * tile < tile ? p.M - i * tile : tile;
+    const int64_t nt = p.N - j * tile < tile ? p.N - j * tile : tile;
+    return mt * nt * p.K;
+  }
   bool all_done() const { return done_count.load() == n_tasks; }
   void set_error(int status, const std::string& msg);
 };

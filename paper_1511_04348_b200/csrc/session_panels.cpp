@@ -147,7 +147,7 @@ bool Session::run_panels(Job& job) {
           const auto rc = which == 0 ? a_key(ti[u.q], k) : b_key(k, tj[u.q]);
           const Mat& m = which == 0 ? p.a : p.b;
           const uint64_t uid = which == 0 ? p.a_uid : p.b_uid;
-          std::lock_guard<std::mutex> g(dir_->mu);
+          DirLock g(dir_->mu);
           int32_t slot = -1, source = TR_SOURCE_HOST;
           const TileKey key{uid, rc.first, rc.second};
           if (!dir_->prefetch_locked(d, key, &slot, &source, false)) continue;
@@ -173,7 +173,7 @@ bool Session::run_panels(Job& job) {
         const int64_t i = ti[u.q], j = tj[u.q];
         const int64_t mt = std::min(T, p.M - i * T), nt = std::min(T, p.N - j * T);
         if (u.k0 == 0) {
-          std::lock_guard<std::mutex> lk(dir_->mu);
+          DirLock lk(dir_->mu);
           dir_->admit_output_locked(d, TileKey{p.c_uid, i, j});  // scheduler.py:390
           wait_on(d, s, cbuf_free[cq]);
         }
@@ -221,7 +221,7 @@ bool Session::run_panels(Job& job) {
         }
       job.launches.fetch_add(1);
       {
-        std::lock_guard<std::mutex> lk(dir_->mu);
+        DirLock lk(dir_->mu);
         const EvRef ev = record(d, s);
         for (int32_t ph : used_phys) note_use(dc.slots[ph], ev);
         for (const TileKey& key : used) dir_->release_input_locked(d, key);
@@ -242,7 +242,7 @@ bool Session::run_panels(Job& job) {
         TR_CUDA(cudaMemcpy2DAsync(dst, p.c.ld * ces, static_cast<char*>(guard.p) + (q - blk.first) * ctile, nt * ces,
                                   nt * ces, mt, cudaMemcpyDeviceToHost, dc.streams[wb].stream));
         trace_end(d, wb, tw, TR_TRACE_D2H, order[q], p.c_uid, i, j);
-        std::lock_guard<std::mutex> lk(dir_->mu);
+        DirLock lk(dir_->mu);
         cbuf_free[q - blk.first] = record(d, wb);
         dir_->release_output_locked(d, TileKey{p.c_uid, i, j}, mt * nt * element_bytes_);  // coherence.py:263-280
       }
@@ -254,6 +254,7 @@ bool Session::run_panels(Job& job) {
   for (int64_t gt : order) {
     job.mark(gt);
     dc.stats.tasks_completed += 1;
+    dc.stats.macs += job.task_macs(gt, tile_);
   }
   return true;
 }

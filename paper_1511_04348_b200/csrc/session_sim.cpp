@@ -49,7 +49,7 @@ void Session::sim_task(int d, Job& job, int64_t gtid, double t) {
   std::vector<std::pair<double, double>> steps;
   steps.reserve(static_cast<size_t>(p.k_steps));
   {
-    std::lock_guard<std::mutex> g(dir_->mu);
+    DirLock g(dir_->mu);
     dir_->admit_output_locked(d, c_key);  // scheduler.py:390
     for (int64_t k = 0; k < p.k_steps; ++k) {
       const int64_t ar = p.ta ? k : i, ac = p.ta ? i : k;
@@ -82,6 +82,7 @@ void Session::sim_task(int d, Job& job, int64_t gtid, double t) {
   }
   job.mark(gtid);
   devs_[d].stats.tasks_completed += 1;
+  devs_[d].stats.macs += job.task_macs(gtid, tile_);
 }
 
 void Session::run_sim(Job& job) {

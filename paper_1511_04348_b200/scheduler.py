@@ -275,6 +275,7 @@ class DeviceStats:
     steals_performed: int = 0
     steals_suffered: int = 0
     peer_copies_served: int = 0  # B200: L2 fills sourced from this device (not in report schema v1)
+    macs: int = 0  # B200: rows x cols x K summed over its tasks (work share of unequal tasks)
 
 
 @dataclass
@@ -453,6 +454,14 @@ class Runtime:
         N.call("tr_session_set_external_stream", self._h, h or None, int(h is not None))
         N.call("tr_session_set_async", self._h, int(bool(ordered) and h is not None))
 
+    def lock_stats(self, reset: bool = True) -> dict:
+        """The directory lock's cost since the last reset: seconds held, seconds
+        callers waited for it, acquisitions, longest hold (tr_session_lock_stats)."""
+        out = (N.i64 * 4)()
+        N.call("tr_session_lock_stats", self._h, int(reset), out)
+        return {"held_s": out[0] / 1e9, "waited_s": out[1] / 1e9, "acquisitions": int(out[2]),
+                "max_hold_us": out[3] / 1e3}
+
     def forget(self, uid) -> int:
         """Drop every cached tile of matrix ``uid`` (its content is dead); returns the count."""
         n = N.i64()
@@ -619,7 +628,7 @@ class Runtime:
             coherence_enabled=self.coherence, seed=self.seed,
             devices={d: DeviceStats(d, self.machine.devices[d].kind, int(per_dev[d].tasks_completed),
                                     int(per_dev[d].steals_performed), int(per_dev[d].steals_suffered),
-                                    int(per_dev[d].peer_copies_served))
+                                    int(per_dev[d].peer_copies_served), int(per_dev[d].macs))
                      for d in range(n)},
             cache=CacheStats.from_c(rep.cache),
             cache_per_device={d: CacheStats.from_c(per_cache[d]) for d in range(n)},
@@ -673,6 +682,33 @@ def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool =
         return rt.multiply(a, b, a_uid="A", b_uid="B", c_uid="C")
     finally:
         rt.close()
+
+
+def standalone_rates(machine: Machine, tile_size: int, a, b, *, out=None, precision: str = "fp32acc",
+                     reps: int = 2) -> list[float]:
+    """Throughput (flop/s) of every logical device of ``machine`` running the
+    product ``a @ b`` ALONE: a one-device machine with the device's GPU, green-
+    context SM count and slots, warm (the operands' tiles already cached), best
+    device-side span of ``reps`` products.  Devices with the same (gpu, sms,
+    slots) are measured once.  This is the yardstick work shares are judged
+    against on inhomogeneous machines -- the reference's acceptance test compares
+    each device's share with its throughput share (test_acceptance.py:130-141)."""
+    from .devices import DeviceSpec, ProximityMatrix
+
+    flops = 2.0 * np.shape(a)[0] * np.shape(a)[1] * np.shape(b)[1]
+    cache: dict = {}
+    rates = []
+    for spec in machine.devices:
+        key = (spec.gpu, spec.sms, spec.slots)
+        if key not in cache:
+            one = Machine([DeviceSpec(0, gpu=spec.gpu, sms=spec.sms, slots=spec.slots)], ProximityMatrix.uniform(1),
+                          dtype=machine.dtype)
+            with Runtime(one, tile_size, precision=precision) as rt:
+                rt.multiply(a, b, a_uid="A", b_uid="B", out=out)
+                best = min(rt.multiply(a, b, a_uid="A", b_uid="B", out=out)[1].span_ms[0] for _ in range(reps))
+            cache[key] = flops / (best / 1e3)
+        rates.append(cache[key])
+    return rates
 
 
 def release_cached_memory() -> None:
