@@ -66,7 +66,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "out-of-core GEMM TFLOPS & MLP train samples/s at 1/2/4/8 B200 vs CPU ref"
 UNIT = "TFLOP/s"
 TOL = {"fp32acc": 1e-5, "bf16": 1e-2}
-LEGS = ("cfg4", "cfg2", "cfg1", "mlp", "mlp_parity", "wide", "inhomogeneous", "ooc", "cpu")
+LEGS = ("cfg4", "cfg2", "cfg1", "mlp", "mlp_parity", "wide", "wide_hetero", "inhomogeneous", "ooc", "cpu")
 
 
 def parse(argv=None):
@@ -92,6 +92,7 @@ def parse(argv=None):
     p.add_argument("--wide-sizes", default="784,65536,65536,65536")
     p.add_argument("--wide-steps", type=int, default=2)
     p.add_argument("--wide-cache-gib", type=float, default=24.0)
+    p.add_argument("--hetero-steps", type=int, default=3, help="timed steps of the cfg5 8-device leg")
     a = p.parse_args(argv)
     a.legs = [x for x in a.legs.split(",") if x]
     bad = set(a.legs) - set(LEGS)
@@ -771,6 +772,93 @@ def bench_mlp_wide(args, tr, torch, gpus):
             "h2d_bytes_per_step": int(xh.nbytes + th.nbytes), "d2h_bytes_per_step": 8}
 
 
+def hetero_machine(tr, gpus):
+    """BASELINE cfg5's machine: 8 devices with 2 of them SM-throttled by green
+    contexts.  On 8 GPUs: one logical device per GPU, the last two on green
+    contexts of half their SMs (72).  On fewer GPUs: 8 green-context devices
+    spread over them, 6 of 16 SMs and 2 throttled to 8 SMs (a GPU's SMs split in
+    groups of 8, 15 usable groups per B200)."""
+    ng = len(gpus)
+    if ng >= 8:
+        sms = [None] * (ng - 2) + [72, 72]
+        specs = [tr.DeviceSpec(i, gpu=gpus[i], sms=sms[i]) for i in range(ng)]
+    else:
+        sms = [16] * 6 + [8] * 2
+        specs = [tr.DeviceSpec(i, gpu=gpus[i % ng], sms=sms[i]) for i in range(8)]
+    return tr.Machine(specs, tr.ProximityMatrix.uniform(len(specs)), dtype=np.float32), sms
+
+
+def bench_wide_hetero(args, tr, torch, gpus):
+    """cfg5 as specified: the 65536-wide MLP (784-65536-65536-65536, batch 8192)
+    trained tile-parallel -- every product's tasks shared by all 8 devices of one
+    runtime through the global queue and work stealing (the reference's
+    TiledBackend semantics, ann.py:78-104), not data parallel -- on a machine
+    with 2 SM-throttled devices (hetero_machine).  Reports samples/s and each
+    device's share of the work (rows x cols x K of the tasks it ran) against its
+    share of the devices' standalone throughputs (tr.standalone_rates on a
+    slice of the layer-1 forward product), criterion 10 % relative
+    (test_acceptance.py:130-141)."""
+    sizes = [int(v) for v in args.wide_sizes.split(",")]
+    batch, T = args.mlp_batch, args.tile
+    machine, sms = hetero_machine(tr, gpus)
+    torch.cuda.set_device(gpus[0])
+    g = torch.Generator(device="cuda").manual_seed(1)
+    # standalone rates on a layer-shaped product: (batch x 65536) . (65536 x 8192)
+    probe_a = torch.rand((batch, sizes[1]), device="cuda", generator=g)
+    probe_b = torch.rand((sizes[1], 2 * T), device="cuda", generator=g)
+    probe_c = torch.empty((batch, 2 * T), device="cuda")
+    rates = tr.standalone_rates(machine, T, probe_a, probe_b, out=probe_c, precision=args.precision)
+    del probe_a, probe_b, probe_c
+    tr.release_cached_memory()
+    torch.cuda.empty_cache()
+    # weights first, then the session (its tile-cache budget is taken from the HBM left)
+    mlp = tr.GpuMLP.random(sizes, seed=0, device=gpus[0], machine=machine, tile_size=T, precision=args.precision)
+    xh = tr.matrix.pinned_empty((batch, sizes[0]), np.float32)
+    th = tr.matrix.pinned_empty((batch, sizes[-1]), np.float32)
+    xh[...] = (torch.rand(xh.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
+    th[...] = (torch.rand(th.shape, device="cuda", generator=g) * 2 - 1).cpu().numpy()
+    xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
+    rows = slice(0, 256)
+    h = xs[rows].cuda().double()
+    for L in mlp.layers:
+        h = torch.sigmoid(h @ L.w.double() + L.b.double())
+    losses = train_steps(torch, mlp, xs, ts, 1)  # warm-up
+    pred = mlp._bufs[f"a{len(mlp.layers) - 1}"][rows].double()
+    pred_err = float(torch.linalg.norm(pred - h) / torch.linalg.norm(h))
+    del h, pred
+    macs0 = list(mlp.device_macs)
+    tasks0 = list(mlp.device_tasks)
+    for gg in gpus:
+        torch.cuda.synchronize(gg)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    losses += train_steps(torch, mlp, xs, ts, args.hetero_steps)
+    e1.record()
+    for gg in gpus:
+        torch.cuda.synchronize(gg)
+    dt = e0.elapsed_time(e1) / 1e3 / args.hetero_steps
+    work = np.array([m - m0 for m, m0 in zip(mlp.device_macs, macs0)], dtype=np.float64)
+    tasks = [t - t0 for t, t0 in zip(mlp.device_tasks, tasks0)]
+    mlp.close()
+    share = work / work.sum()
+    ideal = np.asarray(rates) / sum(rates)
+    relerr = np.abs(share - ideal) / ideal
+    flops = mlp_flops(sizes, batch)
+    return {"workload": f"cfg5 MLP {'-'.join(map(str, sizes))} batch {batch}, sigmoid, MSE, SGD lr 0.1, tile-parallel "
+                        f"over {machine.n_devices} devices (green-context SMs {sms}; None = whole GPU) on "
+                        f"{len(gpus)} GPU(s)",
+            "precision": args.precision, "samples_per_s": batch / dt, "ms_per_step": dt * 1e3,
+            "tflops": flops / dt / 1e12, "steps": args.hetero_steps, "loss": losses,
+            "standalone_tflops": [round(r / 1e12, 2) for r in rates],
+            "sum_of_standalone_tflops": sum(rates) / 1e12,
+            "tasks_per_step": [t // args.hetero_steps for t in tasks],
+            "work_share": [round(float(x), 4) for x in share], "rate_share": [round(float(x), 4) for x in ideal],
+            "max_rel_share_error": float(relerr.max()), "criterion": "<= 0.10 relative (test_acceptance.py:137-141)",
+            "parity": parity_entry(pred_err, args.precision, "first step's predictions, batch rows 0..255, vs a "
+                                                             "float64 torch forward of the same weights"),
+            "h2d_bytes_per_step": int(xh.nbytes + th.nbytes), "d2h_bytes_per_step": 8}
+
+
 def bench_inhomogeneous(tr, torch, precision, gpu):
     """BASELINE cfg5's inhomogeneous devices on one GPU: four logical devices on
     green contexts of 8 / 16 / 24 / 32 SMs share a 32 x 32 task grid (N=32768,
@@ -1028,6 +1116,9 @@ def run_ours(args, ng) -> dict:
     if "wide" in legs and ng == 1:
         res["mlp_wide"] = bench_mlp_wide(args, tr, torch, gpus)
         free_hbm()
+    if "wide_hetero" in legs:
+        res["mlp_wide_hetero"] = bench_wide_hetero(args, tr, torch, gpus)
+        free_hbm()
     if "inhomogeneous" in legs and ng == 1:
         res["inhomogeneous"] = bench_inhomogeneous(tr, torch, args.precision, gpus[0])
         free_hbm()
@@ -1057,6 +1148,8 @@ def run_ours(args, ng) -> dict:
         parity["ooc"] = res["ooc"]["parity"]
     if "mlp_wide" in res:
         parity["cfg5"] = res["mlp_wide"]["parity"]
+    if "mlp_wide_hetero" in res:
+        parity["cfg5_hetero"] = res["mlp_wide_hetero"]["parity"]
 
     def all_ok(d):
         if isinstance(d, dict):
@@ -1113,6 +1206,9 @@ def summarize(line):
             s["cfg3_bf16_samples_per_s"] = round(line["mlp"]["bf16_mode"]["samples_per_s"])
     if "mlp_wide" in line:
         s["cfg5_samples_per_s"] = round(line["mlp_wide"]["samples_per_s"], 1)
+    if "mlp_wide_hetero" in line:
+        s["cfg5_hetero_samples_per_s"] = round(line["mlp_wide_hetero"]["samples_per_s"], 1)
+        s["cfg5_hetero_max_rel_share_err"] = round(line["mlp_wide_hetero"]["max_rel_share_error"], 3)
     if "inhomogeneous" in line:
         s["inhomog_max_rel_share_err"] = round(line["inhomogeneous"]["max_rel_share_error"], 3)
     if "ooc" in line:

@@ -161,7 +161,9 @@ std::vector<TileKey> Directory::admit_locked(int device, const TileKey& key, boo
       // dead tile if the job's future is known, else the LRU unpinned one.
       TileKey victim{};
       const bool found = physical_victim_locked(device, &victim, false);
-      if (!found) fail(TR_ERR_CAPACITY, "device %d: HBM slab exhausted and all resident tiles pinned", device);
+      if (!found)
+        fail(TR_ERR_CAPACITY, "device %d: HBM slab exhausted (%lld slots, %zu resident) and all resident tiles pinned",
+             device, (long long)slot_total_[device], d.order.size());
       drop_locked(device, victim);
       evicted.push_back(victim);
       stats_.evictions += 1;

@@ -208,7 +208,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       budget /= per_gpu[dc.gpu];
       const int64_t tile_bytes = static_cast<int64_t>(tile) * tile * 8;
       const int64_t slot_bytes = slot_elems_ * 2;
-      int64_t avail = budget - (static_cast<int64_t>(dc.width + 2) * 2 + kStage) * tile_bytes;
+      int64_t avail = budget - static_cast<int64_t>(kStage + 2) * tile_bytes;  // stage ring + lazy tiles
       int64_t slots = avail / slot_bytes - 2 * dc.width;
       slots = std::min<int64_t>(slots, int64_t(1) << 22);
       if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
@@ -235,12 +235,12 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
           TR_CUDA(cudaStreamCreateWithPriority(&sc.stream, cudaStreamNonBlocking, prio));
         }
         TR_CUDA(cudaEventCreateWithFlags(&sc.done, cudaEventDisableTiming));
-        if (static_cast<int>(si) > dc.width + 1) continue;  // the writeback stream only copies
-        TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.staging, &sc.staging_cap));
-        TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &sc.outbuf, &sc.outbuf_cap));
+        // per-stream staging / output tiles are allocated on first use (lazy_tile):
+        // bypass-mode fills and host outputs of single-task launches only
       }
-      for (int k = 0; k < kStage; ++k) TR_CUDA(DevPool::get().alloc(dc.gpu, tile_bytes, &dc.stage[k], &dc.stage_cap[k]));
-      if (tdebug) fprintf(stderr, "[tr] session dev %d: meminfo %.2f ms, streams+buffers %.2f ms\n", d, tms(q0, q1), tms(q1, tnow()));
+      if (tdebug)
+        fprintf(stderr, "[tr] session dev %d: meminfo %.2f ms, streams+buffers %.2f ms, budget %.2f GB, max slots %d\n", d,
+                tms(q0, q1), tms(q1, tnow()), budget / 1e9, dc.max_slots);
     }
     // Peer access between every pair of distinct GPUs in use (NVLink / NVSwitch).
     for (int d = 0; d < n; ++d) {
@@ -300,6 +300,12 @@ Session::~Session() {
   if (ext_ready_) cudaEventDestroy(ext_ready_);
 }
 
+// A tile-sized device buffer (T x T doubles), allocated on first use.
+void* Session::lazy_tile(int d, void** p, size_t* cap) {
+  if (!*p) TR_CUDA(DevPool::get().alloc(devs_[d].gpu, static_cast<size_t>(tile_) * tile_ * 8, p, cap));
+  return *p;
+}
+
 // ---------------------------------------------------------------- HBM slab
 void Session::build_tmaps(int d) {
   DeviceCtx& dc = devs_[d];
@@ -333,10 +339,22 @@ void Session::ensure_slab(int d, int64_t needed) {
     e = DevPool::get().alloc(dc.gpu, static_cast<size_t>((grow + scratch) * slot_elems_ * 2),
                              reinterpret_cast<void**>(&nb), &cap);
   }
+  // HBM taken since the budget was set (other logical devices of this GPU, the
+  // caller's tensors): settle for the largest growth that still fits
+  for (int64_t lo = dc.slab_slots; e != cudaSuccess && grow - lo > 8;) {
+    grow = lo + (grow - lo) / 2;
+    e = DevPool::get().alloc(dc.gpu, static_cast<size_t>((grow + scratch) * slot_elems_ * 2),
+                             reinterpret_cast<void**>(&nb), &cap);
+  }
   if (e != cudaSuccess) {
     cudaGetLastError();
     // a slab that cannot grow still serves the job: the directory evicts into it
-    if (dc.slab_slots >= 3) return;
+    if (dc.slab_slots >= 3) {
+      if (getenv("TR_TIMING"))
+        fprintf(stderr, "[tr] device %d: slab stays at %d slots (growth to %lld failed: %s)\n", d, dc.slab_slots,
+                (long long)grow, cudaGetErrorString(e));
+      return;
+    }
     fail(TR_ERR_CAPACITY, "device %d: cannot allocate a %lld-slot tile slab (%s)", d, (long long)grow,
          cudaGetErrorString(e));
   }
@@ -447,6 +465,7 @@ void Session::fill_slot(int d, int s, int32_t phys, const Mat& src, int64_t r, i
   const void* conv_src = base;
   int64_t conv_ld = src.ld;
   if (src.location == TR_LOC_HOST) {
+    lazy_tile(d, &sc.staging, &sc.staging_cap);
     TR_CUDA(cudaMemcpy2DAsync(sc.staging, tc * es, base, src.ld * es, tc * es, tr_, cudaMemcpyHostToDevice, sc.stream));
     conv_src = sc.staging;
     conv_ld = tc;
@@ -539,6 +558,7 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     // convert follows on the fill stream.  The DMA engine runs up to kStage
     // tiles ahead of the converts (which may wait for SMs busy with GEMMs).
     const int k = static_cast<int>(dc.stage_next++ % kStage);
+    lazy_tile(d, &dc.stage[k], &dc.stage_cap[k]);
     cudaStream_t xs = dc.streams[X].stream;
     wait_on(d, X, dc.stage_free[k]);
     TimedLaunch tc1{}, tc2{};
@@ -608,7 +628,9 @@ void Session::fetch_ahead(int d, Job& job, std::vector<uint8_t>& seen, std::vect
   // shell's first task brings a whole row panel (k tiles) before it can run.
   int64_t max_ks = 0;
   for (const Product& p : job.prods) max_ks = std::max<int64_t>(max_ks, p.k_steps);
-  const int64_t kBudget = std::max<int64_t>(job.out_of_core ? 96 : 32, 4 * max_ks);
+  // never more than a third of the device's slab: unclaimed tiles cannot be evicted
+  const int64_t kBudget = std::min<int64_t>(std::max<int64_t>(job.out_of_core ? 96 : 32, 4 * max_ks),
+                                            std::max<int64_t>(1, dc.slab_slots / 3));
   const int64_t kLookahead = job.out_of_core ? 48 : 16;
   for (uint64_t tid : dc.station->peek()) {
     if (seen[tid]) continue;
@@ -816,6 +838,7 @@ void set_task_group_max(int n) { g_task_group.store(std::max(1, std::min(kMaxGro
 // stream's group buffer and are written back on the writeback stream.
 bool Session::groupable(int d, Job& job, int64_t gtid) {
   if (dryrun_ || !coherence_ || devs_[d].capacity >= 0 || max_group_ < 2) return false;
+  if (devs_[d].green && devs_[d].sms < 64) return false;  // a slice of a GPU: single tasks stay stealable
   int64_t tid = 0;
   const Product& p = job.prod_of(gtid, &tid);
   if (p.k_steps > kMaxKSteps) return false;
@@ -995,6 +1018,10 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
       dc.stats.tasks_completed += 1;
       dc.stats.macs += job.task_macs(gt, tile_);
     }
+    if (n_devices() > 1) {  // throttled: the launch occupies the stream until it completes
+      TR_CUDA(cudaEventRecord(sc.done, sc.stream));
+      sc.task = kTaskMarked;
+    }
     return;
   }
   TR_CUDA(cudaEventRecord(sc.done, sc.stream));
@@ -1052,7 +1079,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
   int64_t ldc = 0;
   if (!dryrun_) {
     if (p.c.location == TR_LOC_HOST) {
-      cptr = scp->outbuf;
+      cptr = lazy_tile(d, &scp->outbuf, &scp->outbuf_cap);
       ldc = nt;
     } else {
       cptr = const_cast<char*>(static_cast<const char*>(p.c.ptr)) + (i * T * p.c.ld + j * T) * ces;
@@ -1176,6 +1203,10 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     job.mark(gtid);
     dc.stats.tasks_completed += 1;
     dc.stats.macs += job.task_macs(gtid, tile_);
+    if (!dryrun_ && n_devices() > 1) {  // throttled: see run_job
+      TR_CUDA(cudaEventRecord(scp->done, scp->stream));
+      scp->task = kTaskMarked;
+    }
     return;
   }
   TR_CUDA(cudaEventRecord(scp->done, scp->stream));
@@ -1187,16 +1218,20 @@ void Session::reap(int d, Job& job, bool block_oldest) {
   int oldest = -1;
   for (int s = 0; s < dc.width; ++s) {
     StreamCtx& sc = dc.streams[s];
-    if (sc.task < 0) continue;
+    if (sc.task == kTaskNone) continue;
     if (oldest < 0 || sc.seq < dc.streams[oldest].seq) oldest = s;
   }
   if (block_oldest && oldest >= 0) TR_CUDA(cudaEventSynchronize(dc.streams[oldest].done));
   for (int s = 0; s < dc.width; ++s) {
     StreamCtx& sc = dc.streams[s];
-    if (sc.task < 0) continue;
+    if (sc.task == kTaskNone) continue;
     cudaError_t e = cudaEventQuery(sc.done);
     if (e == cudaErrorNotReady) continue;
     TR_CUDA(e);
+    if (sc.task == kTaskMarked) {  // stream-ordered task, counted when it was enqueued
+      sc.task = kTaskNone;
+      continue;
+    }
     job.mark(sc.task);
     dc.stats.tasks_completed += 1;
     dc.stats.macs += job.task_macs(sc.task, tile_);
@@ -1248,13 +1283,23 @@ void Session::run_job(int d, Job& job) {
   std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.total) : 0, 0);
   std::vector<uint8_t> seen_global(seen.size(), 0);
   dc.pending_prefetch = 0;
+  // A green-context device is a slice of a GPU.  When one task's CTAs fill it
+  // twice over, a second concurrent task adds nothing but a task the others can
+  // no longer steal (a running task is not stealable): one at a time, like the
+  // reference's workers, so a throttled device never sits on work the faster
+  // devices could finish first.
+  int max_inflight = dc.max_inflight;
+  if (dc.green && !job.prods.empty()) {
+    const int64_t t = std::min<int64_t>(tile_, std::max(job.prods[0].M, job.prods[0].N));
+    if (ceil_div(t, 128) * ceil_div(t, 256) >= 2 * static_cast<int64_t>(dc.sms)) max_inflight = 1;
+  }
   while (!job.abort.load()) {
     int active = 0;
     if (!dryrun_) {
       reap(d, job, false);
-      for (auto& sc : dc.streams) active += sc.task >= 0;
+      for (auto& sc : dc.streams) active += sc.task != kTaskNone;
     }
-    if (active >= dc.max_inflight) {
+    if (active >= max_inflight) {
       reap(d, job, true);
       continue;
     }
@@ -1290,7 +1335,7 @@ void Session::run_job(int d, Job& job) {
       bool got = false;
       if (steal_) got = steal_task(d, station_ptrs_.data(), static_cast<int>(station_ptrs_.size()), &tid, &victim);
       if (!got) {
-        if (active == 0) {
+        if (active == 0 || (job.async && job.all_done())) {  // stream-ordered launches may still run
           if (job.all_done()) return;
           std::this_thread::sleep_for(std::chrono::microseconds(50));
         } else {
@@ -1305,11 +1350,17 @@ void Session::run_job(int d, Job& job) {
       dc.stats.steals_performed += 1;
       devs_[victim].stats.steals_suffered += 1;
     }
+    // Stream-ordered products (job.async) are enqueued without waiting for the
+    // GPU.  One device: round-robin over its streams, nothing to reap.  Several
+    // devices: each keeps at most max_inflight launches in flight (their events
+    // reaped like synchronous tasks), so a device pulls tasks from the shared
+    // queue at the rate its GPU (or green context) retires them -- enqueue speed
+    // would otherwise decide the shares (BASELINE cfg5's throttled devices).
     int s = 0;
-    if (job.async) {
-      s = static_cast<int>(seq++ % static_cast<uint64_t>(dc.max_inflight));  // round-robin, nothing to reap
+    if (job.async && n_devices() == 1) {
+      s = static_cast<int>(seq++ % static_cast<uint64_t>(max_inflight));
     } else if (!dryrun_) {
-      while (dc.streams[s].task >= 0) ++s;
+      while (dc.streams[s].task != kTaskNone) ++s;
       dc.streams[s].seq = ++seq;
     }
     // Group only while the queue still holds a round of groups for every device:
@@ -1337,7 +1388,7 @@ void Session::run_job(int d, Job& job) {
         if (!job.async)  // one grouped launch in flight per device: pairs lose SM pairs to a concurrent kernel
           while (true) {
             int busy = 0;
-            for (int q = 0; q < dc.width; ++q) busy += dc.streams[q].task >= 0 && q != s;
+            for (int q = 0; q < dc.width; ++q) busy += dc.streams[q].task != kTaskNone && q != s;
             if (!busy) break;
             reap(d, job, true);
           }

@@ -37,6 +37,10 @@
 
 namespace tr {
 
+constexpr int64_t kTaskNone = -1;    // StreamCtx::task: idle
+constexpr int64_t kTaskMarked = -2;  // StreamCtx::task: a stream-ordered launch in flight, counted at enqueue
+
+
 struct Mat {
   const void* ptr = nullptr;
   int64_t rows = 0, cols = 0, ld = 0;
@@ -162,7 +166,7 @@ class Session {
     std::vector<uint64_t> gen;
     std::deque<int32_t> fifo;
     cudaEvent_t done = nullptr;
-    int64_t task = -1;      // in-flight task id, -1 idle
+    int64_t task = -1;      // in-flight task id; kTaskNone idle, kTaskMarked stream-ordered (already counted)
     std::vector<int64_t> group_rest;  // further tasks of an in-flight grouped launch
     uint64_t seq = 0;       // issue order
     void* staging = nullptr;  // host-tile landing zone (T*T*8 bytes)
@@ -259,6 +263,7 @@ class Session {
   // session-side
   void ensure_slab(int d, int64_t needed);
   void build_tmaps(int d);
+  void* lazy_tile(int d, void** p, size_t* cap);
   uint16_t* slot_ptr(int d, int32_t phys) const {
     return devs_[d].slab + static_cast<int64_t>(phys) * slot_elems_;
   }

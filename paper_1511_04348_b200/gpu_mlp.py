@@ -110,6 +110,10 @@ class GpuMLP:
         # tile-cache counters summed over every product (directory bookkeeping, exact
         # at enqueue even when the products run stream-ordered)
         self.cache_counts = dict.fromkeys(("l1_hits", "host_fetches", "evictions", "writebacks"), 0)
+        # per logical device: tasks and rows x cols x K of the products it ran (work shares)
+        n_dev = self.rt.machine.n_devices
+        self.device_tasks = [0] * n_dev
+        self.device_macs = [0] * n_dev
 
     @classmethod
     def random(cls, sizes, activation: str = "sigmoid", seed: int = 0, device: int = 0, **kw) -> "GpuMLP":
@@ -149,9 +153,12 @@ class GpuMLP:
         """
         self.rt.set_stream(self._stream(), ordered=self.stream_ordered)
         try:
-            cs = self.rt.multiply_batch(prods).cache
+            st = self.rt.multiply_batch(prods)
             for k in self.cache_counts:
-                self.cache_counts[k] += getattr(cs, k)
+                self.cache_counts[k] += getattr(st.cache, k)
+            for d, ds in st.devices.items():
+                self.device_tasks[d] += ds.tasks_completed
+                self.device_macs[d] += ds.macs
         finally:
             self.rt.set_stream(self._stream(), ordered=False)
         self.products += len(prods)
