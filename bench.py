@@ -66,7 +66,8 @@ sys.path.insert(0, str(ROOT))
 METRIC = "out-of-core GEMM TFLOPS & MLP train samples/s at 1/2/4/8 B200 vs CPU ref"
 UNIT = "TFLOP/s"
 TOL = {"fp32acc": 1e-5, "bf16": 1e-2}
-LEGS = ("cfg4", "cfg2", "cfg1", "mlp", "mlp_parity", "wide", "wide_hetero", "inhomogeneous", "ooc", "cpu")
+LEGS = ("cfg4", "cfg2", "cfg1", "mlp", "mlp_parity", "wide", "wide_hetero", "inhomogeneous", "coherence", "ooc",
+        "cpu")
 
 
 def parse(argv=None):
@@ -889,13 +890,71 @@ def bench_inhomogeneous(tr, torch, precision, gpu):
     ideal = np.asarray(rates) / sum(rates)
     relerr = np.abs(share - ideal) / ideal
     ms = e0.elapsed_time(e1)
+    # the reference's sim engine (scheduler.py:432-464) fed the measured standalone
+    # rates: predicted makespan and task counts of the same warm product
+    sim_specs = [tr.DeviceSpec(i, flops_per_unit=r, host_bandwidth=1e18) for i, r in enumerate(rates)]
+    sim_m = tr.Machine(sim_specs, tr.ProximityMatrix.uniform(len(sms), bandwidth=1e18), dtype=np.float32)
+    with tr.Runtime(sim_m, T, mode="sim", compute=False) as srt:
+        shape = tr.ShapeOnly(n, n, np.float32)
+        srt.multiply(shape, shape, a_uid="A", b_uid="B")  # cold: fills the simulated caches
+        _, ss = srt.multiply(shape, shape, a_uid="A", b_uid="B")
     return {"workload": "4 green-context devices of 8/16/24/32 SMs on one B200, N=32768 T=1024 (32 x 32 tasks)",
             "standalone_tflops": [round(r / 1e12, 2) for r in rates],
             "tasks": [st.tasks_by_device[d] for d in range(len(sms))], "steals": len(st.steal_events),
             "work_share": [round(float(x), 4) for x in share], "rate_share": [round(float(x), 4) for x in ideal],
             "max_rel_share_error": float(relerr.max()), "criterion": "<= 0.10 relative (test_acceptance.py:137-141)",
             "ms_per_product": ms, "tflops": 2.0 * n ** 3 / (ms / 1e3) / 1e12,
-            "sum_of_standalone_tflops": sum(rates) / 1e12}
+            "sum_of_standalone_tflops": sum(rates) / 1e12,
+            "sim_validation": {"predicted_ms": ss.makespan * 1e3, "measured_ms": ms,
+                               "predicted_tasks": [ss.tasks_by_device[d] for d in range(len(sms))],
+                               "measured_tasks": [st.tasks_by_device[d] for d in range(len(sms))],
+                               "note": "sim engine with each device's measured standalone rate; the shared run "
+                                       "is slower than the rates' sum (power cap, shared HBM/L2)"}}
+
+
+def bench_coherence(args, tr, torch, gpu):
+    """SURVEY §8f row 4 at hardware scale: the reference's acceptance criterion C2
+    (test_acceptance.py:95-113) with real copies -- g = 16 (N =
+    16384, T = 1024), integer-valued fp32 from pinned host, one cold run() with
+    the tile cache (2 g^2 = 512 host fetches) and one with --no-coherence bypass
+    (2 g^3 = 8192), timed; and the FIFO vs LRU policies on a bounded cache."""
+    g, T = 16, 1024
+    n = g * T
+    a = tr.matrix.pinned_empty((n, n), np.float32)
+    b = tr.matrix.pinned_empty((n, n), np.float32)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    for m in (a, b):
+        torch.from_numpy(m).copy_(torch.randint(-4, 5, (n, n), device="cuda", generator=gen, dtype=torch.float32))
+    rows = np.arange(0, n, 1021)
+    ref = a[rows].astype(np.float64) @ b.astype(np.float64)
+    machine = tr.homogeneous_machine(1, dtype=np.float32, gpus=[gpu])
+    out = {"workload": f"C2 at g={g}: N={n} T={T} integer-valued fp32 from pinned host, one device"}
+    for coh in (True, False):
+        tr.run(machine, a, b, T, coherence=coh)  # warm-up: pools
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        c, s = tr.run(machine, a, b, T, coherence=coh)
+        dt = time.perf_counter() - t0
+        out["coherent" if coh else "bypass"] = {
+            "ms": dt * 1e3, "host_fetches": s.cache.host_fetches, "bytes_host": s.cache.bytes_host,
+            "h2d_gbs": s.cache.bytes_host / dt / 1e9, "exact_on_sampled_rows": bool(np.array_equal(c[rows], ref))}
+        del c
+    out["host_fetch_ratio"] = out["bypass"]["host_fetches"] / out["coherent"]["host_fetches"]
+    # FIFO vs LRU on a bounded cache (capacity 64 tiles of a g=8 grid, T=1024, device operands)
+    A = torch.from_numpy(a[: 8 * T, : 8 * T]).cuda()
+    B = torch.from_numpy(b[: 8 * T, : 8 * T]).cuda()
+    for policy in ("lru", "fifo"):
+        mach = tr.homogeneous_machine(1, capacity_tiles=64, dtype=np.float32, gpus=[gpu])
+        with tr.Runtime(mach, T, policy=policy) as rt:
+            rt.multiply(A, B, a_uid="A", b_uid="B")
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, s = rt.multiply(A, B, a_uid="A2", b_uid="B2")
+            dt = time.perf_counter() - t0
+        out[policy] = {"ms": dt * 1e3, "capacity_tiles": 64, "cache": s.cache.as_dict()}
+    del A, B, a, b
+    torch._C._host_emptyCache()
+    return out
 
 
 def bench_ooc(args, tr, torch, peaks, links, gpu):
@@ -1121,6 +1180,9 @@ def run_ours(args, ng) -> dict:
         free_hbm()
     if "inhomogeneous" in legs and ng == 1:
         res["inhomogeneous"] = bench_inhomogeneous(tr, torch, args.precision, gpus[0])
+        free_hbm()
+    if "coherence" in legs:
+        res["coherence"] = bench_coherence(args, tr, torch, gpus[0])
         free_hbm()
     if "ooc" in legs and ng == 1:
         res["ooc"] = bench_ooc(args, tr, torch, peaks, links, gpus[0])

@@ -352,10 +352,11 @@ class DirectoryModel:
         return list(self.order[dev])
 
 
-def run_schedule_single_device(m, k, n, tile, capacity=None, element_bytes=8, enabled=True, ta=False, tb=False):
+def run_schedule_single_device(m, k, n, tile, capacity=None, element_bytes=8, enabled=True, ta=False, tb=False,
+                               policy="lru"):
     """Sequential _execute_task loop on ONE device (scheduler.py:371-410) over the
     directory model: the exact counters a one-device run must produce."""
-    d = DirectoryModel([capacity], [[0]], enabled=enabled)
+    d = DirectoryModel([capacity], [[0]], enabled=enabled, policy=policy)
     gr, gc = grid_shape(m, n, tile)
     ks = math.ceil(k / tile)
     for t in plan_tasks(m, k, n, tile):
