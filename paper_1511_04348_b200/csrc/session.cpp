@@ -208,7 +208,11 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       budget /= per_gpu[dc.gpu];
       const int64_t tile_bytes = static_cast<int64_t>(tile) * tile * 8;
       const int64_t slot_bytes = slot_elems_ * 2;
-      int64_t avail = budget - static_cast<int64_t>(kStage + 2) * tile_bytes;  // stage ring + lazy tiles
+      // stage ring + lazy tiles + the grouped launches' host-output buffers (one per
+      // concurrently used compute stream, max_group fp32 tiles each)
+      const int64_t gout_bytes = static_cast<int64_t>(std::min(dc.width, 2)) * std::min(max_group_, kMaxGroup) *
+                                 static_cast<int64_t>(tile) * tile * 4;
+      int64_t avail = budget - static_cast<int64_t>(kStage + 2) * tile_bytes - gout_bytes;
       int64_t slots = avail / slot_bytes - 2 * dc.width;
       slots = std::min<int64_t>(slots, int64_t(1) << 22);
       if (dc.capacity >= 0) slots = std::min<int64_t>(slots, dc.capacity);
@@ -691,8 +695,9 @@ bool Session::plan_narrow(int d, StreamCtx& sc, GemmArgs& args, GemmArgs& t) {
   t.aux = nullptr;
   t.wt = nullptr;
   const int64_t ctas = ceil_div(t.n_valid, 256);  // P has <= 32 rows: one 128-row block
-  int splits = splitk_max() < 2 ? 1 : static_cast<int>(std::max<int64_t>(
-                   1, std::min<int64_t>({ceil_div(2 * devs_[d].sms, ctas), 16, kb / 8})));
+  // narrow tiles split up to 16 ways; a lower TR_SPLITK / set_splitk limit is honoured
+  const int64_t cap = splitk_max() >= 8 ? 16 : splitk_max();
+  int splits = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({ceil_div(2 * devs_[d].sms, ctas), cap, kb / 8})));
   const int64_t ws_ld = (t.n_valid + 255) / 256 * 256;
   const int64_t zstride = static_cast<int64_t>(t.m_valid) * ws_ld;
   float* ws = workspace(d, sc, static_cast<size_t>(splits * zstride) * sizeof(float));
@@ -763,7 +768,10 @@ bool Session::group_outbuf(int d, int s, size_t bytes) {
   if (bytes <= sc.gout_cap) return true;
   DeviceCtx& dc = devs_[d];
   if (sc.gout) {
-    TR_CUDA(cudaDeviceSynchronize());  // earlier launches and writebacks may still use it
+    // earlier launches (this stream) and their writebacks (the writeback stream) may
+    // still use it; other logical devices sharing the GPU are not stalled
+    TR_CUDA(cudaStreamSynchronize(sc.stream));
+    TR_CUDA(cudaStreamSynchronize(dc.streams[dc.width + 2].stream));
     DevPool::get().release(dc.gpu, sc.gout, sc.gout_cap);
     sc.gout = nullptr;
     sc.gout_cap = 0;
@@ -1257,29 +1265,29 @@ void Session::run_job(int d, Job& job) {
   bool prio = !dryrun_ && coherence_ && !job.async && getenv("TR_PRIORITY") == nullptr;
   for (auto& dv : devs_) prio = prio && dv.capacity < 0;
   if (const char* e = getenv("TR_PRIORITY")) prio = !dryrun_ && e[0] == '1';
-  // A job that still has host tiles to fill runs its grouped launches
-  // non-persistent: a persistent grid holds every SM for the whole launch, so the
-  // fill stream's split/convert blocks (top priority) only start between launches
-  // and the next group's tiles arrive late (cfg4 N=131072 cold: 0.75 s of idle
-  // tensor cores per 11.6 s product persistent, 0.13 s non-persistent).
-  dc.host_fills = false;
-  if (!dryrun_) {
+  // While the job still has host tiles to fill on this device, its grouped
+  // launches are non-persistent: a persistent grid holds every SM for the whole
+  // launch, so the fill stream's split/convert blocks (top priority) only start
+  // between launches and the next group's tiles arrive late (cfg4 N=131072 cold:
+  // 0.75 s of idle tensor cores per 11.6 s product persistent, 0.13 s
+  // non-persistent).  Re-evaluated every 16 issues: once every input tile is
+  // resident (the first-touch phase is over) launches go persistent again.
+  auto host_fills_pending = [&]() {
+    if (dryrun_) return false;
     DirLock g(dir_->mu);
-    for (const Product& p : job.prods) {
-      for (int which = 0; which < 2 && !dc.host_fills; ++which) {
+    for (const Product& p : job.prods)
+      for (int which = 0; which < 2; ++which) {
         const Mat& m = which == 0 ? p.a : p.b;
         if (m.location != TR_LOC_HOST) continue;
         const uint64_t uid = which == 0 ? p.a_uid : p.b_uid;
-        for (int64_t r = 0; r < (m.rows + tile_ - 1) / tile_ && !dc.host_fills; ++r)
+        for (int64_t r = 0; r < (m.rows + tile_ - 1) / tile_; ++r)
           for (int64_t c = 0; c < (m.cols + tile_ - 1) / tile_; ++c)
-            if (!(dir_->owners_locked(TileKey{uid, r, c}) >> d & 1)) {
-              dc.host_fills = true;
-              break;
-            }
+            if (!(dir_->owners_locked(TileKey{uid, r, c}) >> d & 1)) return true;
       }
-      if (dc.host_fills) break;
-    }
-  }
+    return false;
+  };
+  dc.host_fills = host_fills_pending();
+  int64_t issues = 0;
   std::vector<uint8_t> seen(ahead ? static_cast<size_t>(job.total) : 0, 0);
   std::vector<uint8_t> seen_global(seen.size(), 0);
   dc.pending_prefetch = 0;
@@ -1356,6 +1364,7 @@ void Session::run_job(int d, Job& job) {
     // reaped like synchronous tasks), so a device pulls tasks from the shared
     // queue at the rate its GPU (or green context) retires them -- enqueue speed
     // would otherwise decide the shares (BASELINE cfg5's throttled devices).
+    if (dc.host_fills && ++issues % 16 == 0) dc.host_fills = host_fills_pending();
     int s = 0;
     if (job.async && n_devices() == 1) {
       s = static_cast<int>(seq++ % static_cast<uint64_t>(max_inflight));

@@ -74,7 +74,7 @@ class GpuMLP:
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
                  device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
                  process_group=None, write_through: bool = True, fused_sgd: bool = True,
-                 write_through_weights: bool | None = None):
+                 write_through_weights: bool | None = None, skip_input_grad: bool = False):
         import torch
 
         self.torch = torch
@@ -96,6 +96,9 @@ class GpuMLP:
         self.fused_sgd = fused_sgd  # one process: dW products accumulate straight into W (no gradient buffer)
         # fused SGD: the update product also writes the new weights' tiles into the cache
         self.write_through_weights = write_through if write_through_weights is None else write_through_weights
+        # ann.py:171-172 computes dX of the first layer too, though nothing reads it;
+        # True skips that product (cfg3: 784-wide output, ~1.5 % of a step's flops)
+        self.skip_input_grad = skip_input_grad
         self.pg = process_group
         if process_group is not None:
             import torch.distributed as dist
@@ -225,15 +228,17 @@ class GpuMLP:
                 if self.write_through:
                     dx["cache_as"] = next_dy  # dY_{l-1} is the next round's operand
             dw = dict(a=xs[li], b=d_y, transpose_a=True, a_uid=uids[li], b_uid=dy_uid)
+            dxs = [] if (li == 0 and self.skip_input_grad) else [dx]
             if lr is None:
                 d_w = dw["out"] = self._buf(f"dw{li}", L.w.shape)
-                self._batch([dw, dx])
+                self._batch([dw] + dxs)
             else:
                 d_w = None
                 dw.update(out=L.w, axpy=-float(lr))
                 if self.write_through_weights:  # the updated weights' tiles enter the cache as the next version
                     dw["cache_as"] = f"{L.tag}.w.v{L.version + 1}"
-                self._batch([dx] + ([update] if update else []))
+                if dxs or update:
+                    self._batch(dxs + ([update] if update else []))
                 update = dw
             d_b = None
             if L.b is not None:

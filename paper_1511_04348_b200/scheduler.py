@@ -59,36 +59,37 @@ class Task:
 
 
 class Completion:
-    """Exactly-once bitmap; a second mark raises (scheduler.py:70-96).
-
-    The native runtime keeps the same bitmap with an atomic exchange per task;
-    its snapshot is copied here after every product.
-    """
+    """Exactly-once task bitmap with the contract of scheduler.py:70-96 (a second
+    mark raises RuntimeError; ``all_done`` gates the result).  Stored as one byte
+    per task -- the layout of the native runtime's bitmap
+    (tr_gemm_report.completion, set by an atomic exchange per task), so
+    ``Completion.of(bits)`` wraps a product's native snapshot without copying."""
 
     def __init__(self, n_tasks: int):
-        self._done = [False] * n_tasks
-        self._count = 0
-        self._lock = threading.Lock()
+        self._bits = np.zeros(max(0, int(n_tasks)), dtype=np.uint8)
+        self._guard = threading.Lock()
+
+    @classmethod
+    def of(cls, bits) -> "Completion":
+        c = cls(0)
+        c._bits = np.asarray(bits, dtype=np.uint8)
+        return c
 
     def mark(self, task_id: int) -> None:
-        with self._lock:
-            if self._done[task_id]:
+        with self._guard:
+            if self._bits[task_id]:
                 raise RuntimeError(f"task {task_id} executed twice")
-            self._done[task_id] = True
-            self._count += 1
+            self._bits[task_id] = 1
 
     def all_done(self) -> bool:
-        with self._lock:
-            return self._count == len(self._done)
+        return bool(self._bits.all())
 
     @property
     def done_count(self) -> int:
-        with self._lock:
-            return self._count
+        return int(np.count_nonzero(self._bits))
 
     def snapshot(self) -> list[bool]:
-        with self._lock:
-            return list(self._done)
+        return self._bits.astype(bool).tolist()
 
 
 @dataclass
@@ -302,6 +303,7 @@ class RunStats:
     kernel_ms: dict[int, float] = field(default_factory=dict)  # sum of tile-GEMM kernel durations
     span_ms: dict[int, float] = field(default_factory=dict)  # device-side span of the product
     trace: list = field(default_factory=list)  # Runtime(trace=True): device timeline of the product
+    completion: Completion | None = None  # the native exactly-once bitmap of the product
 
     @property
     def tasks_by_device(self) -> dict[int, int]:
@@ -618,10 +620,10 @@ class Runtime:
             span = (N.f64 * n)()
             N.call("tr_session_span_ms", self._h, span)
             trace = self._read_trace() if self.tracing else []
-        done = [bool(completion[t]) for t in range(total)]
-        want = [planned(t) for t in range(total)]
-        if done != want:
-            raise RuntimeError(f"run incomplete: {sum(done)}/{sum(want)} tasks")
+        done = Completion.of(np.frombuffer(completion, dtype=np.uint8, count=total).copy())
+        want = np.array([planned(t) for t in range(total)], dtype=bool)
+        if not np.array_equal(done._bits.astype(bool), want):
+            raise RuntimeError(f"run incomplete: {done.done_count}/{int(want.sum())} tasks")
         return RunStats(
             mode=self.mode, tile_size=self.tile_size, grid_rows=int(rep.grid_rows), grid_cols=int(rep.grid_cols),
             k_steps=int(rep.k_steps), total_tasks=int(rep.total_tasks), steal_enabled=self.steal,
@@ -639,7 +641,7 @@ class Runtime:
             precision=self.precision, gpu_launches=int(rep.gpu_launches),
             kernel_ms={d: float(kms[d]) for d in range(n)},
             span_ms={d: float(span[d]) for d in range(n)},
-            trace=trace,
+            trace=trace, completion=done,
         )
 
     def _read_trace(self) -> list[dict]:

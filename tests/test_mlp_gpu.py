@@ -239,3 +239,27 @@ def test_fused_sgd_matches_gradient_buffers():
     assert np.allclose(l0, l1, rtol=1e-6, atol=0)
     for (w0, b0), (w1, b1) in zip(p0, p1):
         assert relerr(w0, w1) <= 1e-6 and np.array_equal(b0, b1)
+
+
+@pytest.mark.parametrize("fused", [True, False])
+def test_skip_input_grad_same_trajectory(fused):
+    """skip_input_grad drops the first layer's dX product (ann.py:171-172 computes
+    it; nothing reads it): same losses and weights, one product fewer per step."""
+    sizes = [300, 256, 200, 10]
+    rng = np.random.default_rng(41)
+    layers = [Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
+                           tag=f"layer{i}") for i in range(3)]
+    x = torch.as_tensor(rng.uniform(-1, 1, (512, sizes[0])), dtype=torch.float32).cuda()
+    t = torch.as_tensor(rng.uniform(-1, 1, (512, sizes[-1])), dtype=torch.float32).cuda()
+    runs = {}
+    for skip in (False, True):
+        mlp = GpuMLP(layers, machine=homogeneous_machine(1, dtype=np.float32), tile_size=128, fused_sgd=fused,
+                     skip_input_grad=skip)
+        losses = [mlp.train_step(x, t, 0.1) for _ in range(4)]
+        runs[skip] = (losses, mlp.to_host(), mlp.products)
+        mlp.close()
+    # the other products are unchanged; only their grouping into launches may differ
+    assert np.allclose(runs[False][0], runs[True][0], rtol=1e-6, atol=0)
+    for (w0, b0), (w1, b1) in zip(runs[False][1], runs[True][1]):
+        assert relerr(w1, w0) <= 1e-6 and relerr(b1, b0) <= 1e-6
+    assert runs[False][2] - runs[True][2] == 4  # one dX product per step

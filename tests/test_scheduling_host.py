@@ -276,3 +276,24 @@ def test_describe_strided_host_views():
         describe(m.T)  # column-major: not readable in place
     with pytest.raises(ValueError):
         describe(m[:, ::2])
+
+
+def test_completion_bitmap_contract_and_native_view():
+    """Completion (scheduler.py:70-96): exactly once, all_done gate; every product's
+    RunStats carries the native runtime's bitmap as one."""
+    import numpy as np
+
+    from paper_1511_04348_b200 import Runtime, homogeneous_machine
+    from paper_1511_04348_b200.scheduler import Completion
+
+    c = Completion(3)
+    c.mark(0)
+    c.mark(2)
+    assert not c.all_done() and c.done_count == 2 and c.snapshot() == [True, False, True]
+    with pytest.raises(RuntimeError, match="executed twice"):
+        c.mark(2)
+    c.mark(1)
+    assert c.all_done()
+    with Runtime(homogeneous_machine(2), 4, mode="dryrun") as rt:
+        _, s = rt.multiply(np.zeros((12, 8)), np.zeros((8, 16)))
+    assert s.completion.all_done() and s.completion.done_count == s.total_tasks == 12
