@@ -243,8 +243,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && leader) {
-      // ---------------- MMA issuer (the pair's leader issues for both CTAs)
+    if (leader) {
+      // ---------------- MMA issuer (the pair's leader issues for both CTAs).  The
+      // whole warp walks the k-loop -- converged, so barrier phases, stage
+      // addresses and descriptors are warp-uniform (uniform registers) -- and one
+      // elected lane issues each k-block's MMAs and their commits.
       constexpr uint32_t idesc = ptx::idesc_bf16_f32(BM * CG, BN, A_MN, !B_K);
       int stage = 0;
       uint32_t phase = 0;
@@ -274,41 +277,53 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             ptx::tc_fence_after();
             const uint32_t a_base = ptx::smem_u32(smem + stage * STAGE_BYTES);
             const uint32_t b_base = a_base + PLANES * A_BYTES;
-            // PLANES == 2: small cross terms first, then hi*hi.
+            const bool seg_done = kb_in_seg + 1 == seg_kb;
+            if (ptx::elect_one()) {
+              uint32_t acc = accumulate;
+              // PLANES == 2: small cross terms first, then hi*hi.
 #pragma unroll
-            for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
-              const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
-              const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
+              for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
+                const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
+                const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
+                // k16 advances the start address field (bits [0,14), 16-byte units)
+                const uint64_t a0 = A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES, MN_GROUP_BYTES, 1024)
+                                         : ptx::sdesc_sw128(a_base + pa * A_BYTES, 16, 1024);
+                const uint64_t b0 = B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES, 16, 1024)
+                                        : ptx::sdesc_sw128(b_base + pb * B_BYTES, MN_GROUP_BYTES, 1024);
 #pragma unroll
-              for (int k16 = 0; k16 < BK / 16; ++k16) {
-                const uint64_t adesc =
-                    A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024)
-                         : ptx::sdesc_sw128(a_base + pa * A_BYTES + k16 * 32, 16, 1024);
-                const uint64_t bdesc =
-                    B_K ? ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 32, 16, 1024)
-                        : ptx::sdesc_sw128(b_base + pb * B_BYTES + k16 * 2048, MN_GROUP_BYTES, 1024);
-                if (CG == 2) ptx::mma_bf16_cg2(tmem_d, adesc, bdesc, idesc, accumulate);
-                else ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, accumulate);
-                accumulate = 1;
+                for (int k16 = 0; k16 < BK / 16; ++k16) {
+                  const uint64_t adesc = a0 + static_cast<uint64_t>((A_MN ? 2048 : 32) * k16 >> 4);
+                  const uint64_t bdesc = b0 + static_cast<uint64_t>((B_K ? 32 : 2048) * k16 >> 4);
+                  if (CG == 2) ptx::mma_bf16_cg2(tmem_d, adesc, bdesc, idesc, acc);
+                  else ptx::mma_bf16(tmem_d, adesc, bdesc, idesc, acc);
+                  acc = 1;
+                }
+              }
+              if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+              else ptx::mma_commit(&empty[stage]);
+              if (seg_done) {
+                if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+                else ptx::mma_commit(&acc_full[seg & 1]);
               }
             }
-            if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
-            else ptx::mma_commit(&empty[stage]);
+            __syncwarp();
+            accumulate = 1;
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
             }
             if (++kb_in_seg == seg_kb) {
-              if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
-              else ptx::mma_commit(&acc_full[seg & 1]);
               kb_in_seg = 0;
               ++seg;
             }
           }
         }
         if (kb_in_seg != 0) {  // the unit's last, partial segment
-          if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
-          else ptx::mma_commit(&acc_full[seg & 1]);
+          if (ptx::elect_one()) {
+            if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+            else ptx::mma_commit(&acc_full[seg & 1]);
+          }
+          __syncwarp();
           ++seg;
         }
       }
