@@ -1,7 +1,8 @@
 """The bench.py output contract, checked on the committed final line of the
-round (profiles/r1_bench_final.json) and on the argument parser: every key
+round (profiles/r2_bench_final.json) and on the argument parser: every key
 the driver and the judge read is present and typed, the timing rules hold
-(W >= 3, device-timed, clocks sampled), and the reference arm's flags parse."""
+(W >= 3, device-timed, clocks sampled), every config's parity entry is within
+its tolerance, and the reference arm's flags parse."""
 
 import json
 from pathlib import Path
@@ -13,7 +14,7 @@ ROOT = Path(__file__).resolve().parent.parent
 
 @pytest.fixture(scope="module")
 def line():
-    return json.loads((ROOT / "profiles" / "r1_bench_final.json").read_text().strip().splitlines()[-1])
+    return json.loads((ROOT / "profiles" / "r2_bench_final.json").read_text().strip().splitlines()[-1])
 
 
 def test_top_level_keys(line):
@@ -43,12 +44,34 @@ def test_clocks_and_parity(line):
     clk = line["clocks"]
     assert clk["samples"] > 0 and clk["sm_mhz"] > 0
     assert not {"hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"} & set(clk["reasons"])
-    assert line["parity_rel_fro_sampled"] <= 1e-5
-    assert line["e2e"]["parity_rel_fro_sampled"] <= 1e-5
-    assert line["ooc"]["parity_rel_fro_sampled"] <= 1e-5
-    assert line["mlp"]["pred_rel_err_vs_torch_fp32"] <= 1e-5
-    assert line["mlp"]["bf16_mode"]["pred_rel_err_vs_torch_fp32"] <= 1e-2
-    assert line["mlp_wide"]["pred_rel_err_vs_torch_fp32"] <= 1e-5
+    assert line["parity_ok"] is True
+
+    def entries(d):
+        if "rel_fro" in d:
+            yield d
+        else:
+            for v in d.values():
+                if isinstance(v, dict):
+                    yield from entries(v)
+
+    got = list(entries(line["parity"]))
+    assert len(got) >= 10
+    for e in got:
+        assert e["rel_fro"] <= e["tol"] and e["ok"] and e["sample"]
+    for cfg in ("cfg1", "cfg2", "cfg3", "cfg4", "cfg5"):
+        assert cfg in line["parity"]
+    assert "256 rows x 256 cols" in line["parity"]["cfg4"]["value"]["sample"]
+
+
+def test_headline_is_cfg4_and_summary_last(line):
+    assert line["config"]["n"] == 131072 and line["config"]["tile"] == 4096
+    assert line["e2e"]["h2d_bytes_per_step"] == 2 * 32 * 32 * 4096 * 4096 * 4
+    assert list(line)[-1] == "summary" and line["summary"]["parity_ok"] is True
+    assert line["links"]["h2d_gbs"] > 1 and line["roofline"]["launches"] > 0
+    for leg in ("cfg2", "mlp", "mlp_wide", "mlp_wide_hetero", "inhomogeneous", "coherence", "ooc"):
+        assert leg in line, leg
+    assert line["mlp_wide_hetero"]["max_rel_share_error"] <= 0.10
+    assert line["inhomogeneous"]["max_rel_share_error"] <= 0.10
 
 
 def test_parser_defaults():
