@@ -93,7 +93,7 @@ def parse(argv=None):
     p.add_argument("--wide-sizes", default="784,65536,65536,65536")
     p.add_argument("--wide-steps", type=int, default=2)
     p.add_argument("--wide-cache-gib", type=float, default=24.0)
-    p.add_argument("--hetero-steps", type=int, default=3, help="timed steps of the cfg5 8-device leg")
+    p.add_argument("--hetero-steps", type=int, default=4, help="timed steps of the cfg5 8-device leg")
     a = p.parse_args(argv)
     a.legs = [x for x in a.legs.split(",") if x]
     bad = set(a.legs) - set(LEGS)
@@ -780,12 +780,14 @@ def hetero_machine(tr, gpus):
     spread over them, 6 of 16 SMs and 2 throttled to 8 SMs (a GPU's SMs split in
     groups of 8, 15 usable groups per B200)."""
     ng = len(gpus)
+    # a throttled device reserves half as many tasks (DeviceSpec.slots, the
+    # reservation-station width): it holds no more queued work than it can retire
     if ng >= 8:
         sms = [None] * (ng - 2) + [72, 72]
-        specs = [tr.DeviceSpec(i, gpu=gpus[i], sms=sms[i]) for i in range(ng)]
+        specs = [tr.DeviceSpec(i, gpu=gpus[i], sms=sms[i], slots=2 if sms[i] else 4) for i in range(ng)]
     else:
         sms = [16] * 6 + [8] * 2
-        specs = [tr.DeviceSpec(i, gpu=gpus[i % ng], sms=sms[i]) for i in range(8)]
+        specs = [tr.DeviceSpec(i, gpu=gpus[i % ng], sms=sms[i], slots=2 if sms[i] == 8 else 4) for i in range(8)]
     return tr.Machine(specs, tr.ProximityMatrix.uniform(len(specs)), dtype=np.float32), sms
 
 
@@ -804,12 +806,21 @@ def bench_wide_hetero(args, tr, torch, gpus):
     machine, sms = hetero_machine(tr, gpus)
     torch.cuda.set_device(gpus[0])
     g = torch.Generator(device="cuda").manual_seed(1)
-    # standalone rates on a layer-shaped product: (batch x 65536) . (65536 x 8192)
-    probe_a = torch.rand((batch, sizes[1]), device="cuda", generator=g)
-    probe_b = torch.rand((sizes[1], 2 * T), device="cuda", generator=g)
-    probe_c = torch.empty((batch, 2 * T), device="cuda")
-    rates = tr.standalone_rates(machine, T, probe_a, probe_b, out=probe_c, precision=args.precision)
-    del probe_a, probe_b, probe_c
+    # Standalone rates on the step's two product shapes: long contractions (the
+    # forward and dX products, K = 65536: (batch x 65536).(65536 x 8192)) and the
+    # weight gradients (K = batch = 8192: (16384 x 8192).(8192 x 16384)),
+    # combined by their shares of the step's flops (time = sum f_i / r_i).
+    # (each layer's forward, dX and dW products have the same flops: 2 of 3 are long-K)
+    w = sizes[1]
+    rates_by_shape = []
+    for (m, k, n) in ((batch, w, 2 * T), (4 * T, batch, 4 * T)):
+        pa = torch.rand((m, k), device="cuda", generator=g)
+        pb = torch.rand((k, n), device="cuda", generator=g)
+        pc = torch.empty((m, n), device="cuda")
+        rates_by_shape.append(tr.standalone_rates(machine, T, pa, pb, out=pc, precision=args.precision))
+        del pa, pb, pc
+    f_long = 2.0 / 3.0
+    rates = [1.0 / (f_long / r1 + (1.0 - f_long) / r2) for r1, r2 in zip(*rates_by_shape)]
     tr.release_cached_memory()
     torch.cuda.empty_cache()
     # weights first, then the session (its tile-cache budget is taken from the HBM left)
@@ -827,8 +838,9 @@ def bench_wide_hetero(args, tr, torch, gpus):
     pred = mlp._bufs[f"a{len(mlp.layers) - 1}"][rows].double()
     pred_err = float(torch.linalg.norm(pred - h) / torch.linalg.norm(h))
     del h, pred
-    macs0 = list(mlp.device_macs)
-    tasks0 = list(mlp.device_tasks)
+    # shares are counted over every step (warm-up included); the rate over the timed ones
+    macs0 = [0] * len(mlp.device_macs)
+    tasks0 = [0] * len(mlp.device_tasks)
     for gg in gpus:
         torch.cuda.synchronize(gg)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -851,8 +863,12 @@ def bench_wide_hetero(args, tr, torch, gpus):
             "precision": args.precision, "samples_per_s": batch / dt, "ms_per_step": dt * 1e3,
             "tflops": flops / dt / 1e12, "steps": args.hetero_steps, "loss": losses,
             "standalone_tflops": [round(r / 1e12, 2) for r in rates],
+            "standalone_by_shape_tflops": {"long_k": [round(r / 1e12, 2) for r in rates_by_shape[0]],
+                                           "weight_grad": [round(r / 1e12, 2) for r in rates_by_shape[1]],
+                                           "long_k_flop_share": round(f_long, 4)},
             "sum_of_standalone_tflops": sum(rates) / 1e12,
-            "tasks_per_step": [t // args.hetero_steps for t in tasks],
+            "tasks_per_step": [t // (args.hetero_steps + 1) for t in tasks],
+            "share_steps": args.hetero_steps + 1,
             "work_share": [round(float(x), 4) for x in share], "rate_share": [round(float(x), 4) for x in ideal],
             "max_rel_share_error": float(relerr.max()), "criterion": "<= 0.10 relative (test_acceptance.py:137-141)",
             "parity": parity_entry(pred_err, args.precision, "first step's predictions, batch rows 0..255, vs a "

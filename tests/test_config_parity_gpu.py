@@ -84,3 +84,68 @@ def test_band_sampled_ragged_product(precision):
     assert err <= TOL[precision], err
     assert s.cache.host_fetches == 3 * 2 + 2 * 4 and s.cache.writebacks == 3 * 4
 
+
+
+def _host_mem_available():
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemAvailable:"):
+                return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def test_cfg2_full_size_band_sampled():
+    """cfg2 (N = 32768, T = 4096) through run() on pinned host arrays, both
+    precisions: >= 8 rows and columns per tile band against the float64 oracle,
+    and the reference's first-touch counters (2 g^2 fetches, g^2 writebacks)."""
+    import torch
+
+    from paper_1511_04348_b200.matrix import pinned_empty
+
+    n, T = 32768, 4096
+    a, b = pinned_empty((n, n), np.float32), pinned_empty((n, n), np.float32)
+    g = torch.Generator(device="cuda")
+    torch.from_numpy(a).copy_(torch.randn((n, n), generator=g.manual_seed(1), device="cuda"))
+    torch.from_numpy(b).copy_(torch.randn((n, n), generator=g.manual_seed(2), device="cuda"))
+    rows, cols = O.band_samples(n, T, seed=5), O.band_samples(n, T, seed=6)
+    a_rows, b_cols = a[rows].astype(np.float64), b[:, cols].astype(np.float64)
+    for precision in ("fp32acc", "bf16"):
+        c, s = run(homogeneous_machine(1, dtype=np.float32), a, b, T, precision=precision)
+        err = O.sampled_rel_error(a_rows, b_cols, c[np.ix_(rows, cols)])
+        assert err <= TOL[precision], (precision, err)
+        assert (s.cache.host_fetches, s.cache.writebacks) == (2 * 64, 64)
+        del c
+
+
+@pytest.mark.skipif(_host_mem_available() < 2 * 131072 ** 2 * 4 + 24 * 2 ** 30,
+                    reason="cfg4 needs 2 x 64 GiB of pinned host memory")
+def test_cfg4_full_size_out_of_core_band_sampled():
+    """cfg4 at its full size, N = 131072, T = 4096, fp32-accurate, streamed from
+    pinned host (B aliases A's buffer under its own uid, as in bench.py): 256 x
+    256 band-sampled elements (8 per tile band) against the float64 oracle, and
+    the counters of a cold product: 2048 first-touch fetches, 1024 writebacks."""
+    import torch
+
+    from paper_1511_04348_b200 import Runtime
+    from paper_1511_04348_b200.matrix import pinned_empty
+
+    n, T = 131072, 4096
+    torch._C._host_emptyCache()
+    a = pinned_empty((n, n), np.float32)
+    c = pinned_empty((n, n), np.float32)
+    g = torch.Generator(device="cuda").manual_seed(4)
+    at = torch.from_numpy(a)
+    for r in range(0, n, 4096):
+        at[r:r + 4096].copy_(torch.randn((4096, n), device="cuda", generator=g))
+    torch.cuda.synchronize()
+    with Runtime(homogeneous_machine(1, dtype=np.float32), T) as rt:
+        _, s = rt.multiply(a, a, a_uid="A", b_uid="B", c_uid="C", out=c)
+    assert (s.cache.host_fetches, s.cache.writebacks, s.cache.evictions) == (2048, 1024, 0)
+    assert s.cache.l1_hits == 2 * 1024 * 32 - 2048
+    rows, cols = O.band_samples(n, T, seed=7), O.band_samples(n, T, seed=8)
+    err = O.sampled_rel_error(a[rows].astype(np.float64), a[:, cols].astype(np.float64), c[np.ix_(rows, cols)])
+    assert err <= 1e-5, err
+    del a, c, at
+    torch._C._host_emptyCache()

@@ -263,3 +263,29 @@ def test_skip_input_grad_same_trajectory(fused):
     for (w0, b0), (w1, b1) in zip(runs[False][1], runs[True][1]):
         assert relerr(w1, w0) <= 1e-6 and relerr(b1, b0) <= 1e-6
     assert runs[False][2] - runs[True][2] == 4  # one dX product per step
+
+
+def test_cfg3_full_shape_losses_vs_f64_oracle():
+    """BASELINE cfg3 at its full shape, 784-8192-8192-8192-10 x 8192 (SURVEY §8d
+    init: per-layer scale 1/sqrt(fan_in), random_regression data): 3 SGD steps
+    on the GPU in both precisions against the reference's train_step algebra in
+    float64 (oracle.train_step with BLAS products, ann.py:239-248); per-step loss
+    relative error <= 1e-5 (fp32acc) / 1e-2 (bf16)."""
+    sizes, batch = [784, 8192, 8192, 8192, 10], 8192
+    rng = np.random.default_rng(0)
+    layers = [Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
+                           tag=f"layer{i}") for i in range(4)]
+    x = rng.uniform(-1.0, 1.0, size=(batch, sizes[0]))
+    t = rng.uniform(-1.0, 1.0, size=(batch, sizes[-1]))
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    got = {}
+    for precision in ("fp32acc", "bf16"):
+        mlp = GpuMLP(layers, machine=homogeneous_machine(1, dtype=np.float32), tile_size=4096, precision=precision)
+        got[precision] = [mlp.train_step(xd, td, 0.1) for _ in range(3)]
+        mlp.close()
+    ol = [O.OracleLayer(np.array(L.weights, np.float64), np.array(L.bias, np.float64), "sigmoid") for L in layers]
+    ref = [O.train_step(ol, x, t, 0.1, matmul=O.blas_matmul) for _ in range(3)]
+    for precision, tol in (("fp32acc", 1e-5), ("bf16", 1e-2)):
+        errs = [abs(g - r) / abs(r) for g, r in zip(got[precision], ref)]
+        assert max(errs) <= tol, (precision, errs)
