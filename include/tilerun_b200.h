@@ -255,6 +255,11 @@ typedef struct {
   int32_t axpy;        /* != 0: C += alpha * A.B (float32 device C, post-op NONE) -- e.g. the fused SGD
                           update W += (-lr) X^T dY of ann.py:247 without a gradient buffer */
   float alpha;
+  float* colsum;       /* != NULL: column sums of the FINAL output (after the post-op) per 32-row
+                          block, colsum[(r / 32) * c.cols + col] = sum of C[r..r+31][col] (rows in
+                          order); finish with tr_mlp_colsum_finish -- the bias gradient
+                          db = colsum(dY) of ann.py:173 without a pass over dY.  ceil(c.rows/32)
+                          x c.cols floats (device); float32 device C; tile size a multiple of 32. */
 } tr_product;
 int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_report* report);
 /* Device-side duration (ms) of the last tr_gemm's GEMM kernels on each device,
@@ -327,6 +332,8 @@ int tr_mlp_mse_grad_global(float* dout, const float* pred, const float* target, 
                            double* loss_sum, void* stream);
 /* out[c] = sum_r m[r, c], fixed summation order (reproducible)   ann.py:173 */
 int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream);
+/* out[c] = sum over b < n_blocks of part[b * cols + c], blocks in order (tr_product.colsum). */
+int tr_mlp_colsum_finish(const float* part, int64_t n_blocks, int64_t cols, float* out, void* stream);
 /* w -= lr * g                                                ann.py:243-247 */
 int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream);
 

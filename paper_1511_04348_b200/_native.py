@@ -75,7 +75,7 @@ class ProductC(C.Structure):
     _fields_ = [("a", MatrixC), ("a_uid", u64), ("transpose_a", i32), ("b", MatrixC), ("b_uid", u64),
                 ("transpose_b", i32), ("c", MatrixC), ("c_uid", u64), ("post", i32), ("act", i32),
                 ("bias", C.c_void_p), ("aux", C.c_void_p), ("ldaux", i64), ("cache_as", u64),
-                ("axpy", i32), ("alpha", C.c_float)]
+                ("axpy", i32), ("alpha", C.c_float), ("colsum", C.c_void_p)]
 
 
 TR_POST_NONE, TR_POST_BIAS_ACT, TR_POST_ACT_GRAD = 0, 1, 2
@@ -153,6 +153,7 @@ _PROTOS = {
     "tr_mlp_mse_grad": [vp, vp, vp, i64, vp, vp],
     "tr_mlp_mse_grad_global": [vp, vp, vp, i64, i64, vp, vp],
     "tr_mlp_colsum": [vp, i64, i64, vp, vp],
+    "tr_mlp_colsum_finish": [vp, i64, i64, vp, vp],
     "tr_mlp_sgd": [vp, vp, i64, C.c_float, vp],
     "tr_session_set_external_stream": [vp, vp, i32],
     "tr_session_set_async": [vp, i32],

@@ -333,6 +333,7 @@ int tr_gemm_batch(tr_session* s, int32_t n, const tr_product* products, tr_gemm_
       p.cache_as = q.cache_as;
       p.axpy = q.axpy != 0;
       p.alpha = q.alpha;
+      p.colsum = q.colsum;
     }
     s->s->run_products(std::move(v), 0, 1, report);
   });
@@ -460,6 +461,11 @@ int tr_mlp_mse_grad_global(float* dout, const float* pred, const float* target, 
 }
 int tr_mlp_colsum(const float* m, int64_t rows, int64_t cols, float* out, void* stream) {
   return guarded([&] { TR_CUDA(tr::mlp_colsum(m, rows, cols, out, static_cast<cudaStream_t>(stream))); });
+}
+int tr_mlp_colsum_finish(const float* part, int64_t n_blocks, int64_t cols, float* out, void* stream) {
+  return guarded([&] {
+    TR_CUDA(tr::mlp_colsum_finish(part, n_blocks, cols, out, static_cast<cudaStream_t>(stream)));
+  });
 }
 int tr_mlp_sgd(float* w, const float* g, int64_t n, float lr, void* stream) {
   return guarded([&] { TR_CUDA(tr::mlp_sgd(w, g, n, lr, static_cast<cudaStream_t>(stream))); });

@@ -117,6 +117,41 @@ __global__ void colsum_finish_kernel(const float* __restrict__ part, int ny, int
   }
 }
 
+// The same sum for many blocks: 32 columns x 8 row lanes per CTA; lane y sums
+// blocks y, y + 8, ... in order, then the 8 lane sums are added in order
+// (a fixed order: bitwise reproducible).
+__global__ void colsum_finish8_kernel(const float* __restrict__ part, int ny, int64_t cols, float* __restrict__ out) {
+  const int64_t c = blockIdx.x * 32 + (threadIdx.x & 31);
+  const int y0 = threadIdx.x >> 5;
+  __shared__ float sh[8][33];
+  float s = 0.f;
+  if (c < cols)
+    for (int y = y0; y < ny; y += 8) s += part[y * cols + c];
+  sh[y0][threadIdx.x & 31] = s;
+  __syncthreads();
+  if (y0 == 0 && c < cols) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += sh[k][threadIdx.x & 31];
+    out[c] = t;
+  }
+}
+
+__global__ void tile_colsum32_kernel(const float* __restrict__ m, int64_t ldm, int64_t rows, int64_t cols,
+                                     float* __restrict__ part, int64_t ld_part) {
+  const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t r0 = static_cast<int64_t>(blockIdx.y) * 32;
+  if (c >= cols) return;
+  const int n = static_cast<int>(min(rows - r0, static_cast<int64_t>(32)));
+  const float* p = m + r0 * ldm + c;
+  float v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) v[r] = r < n ? __ldg(p + r * ldm) : 0.f;  // all 32 loads in flight
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < 32; ++r) s += v[r];
+  part[blockIdx.y * ld_part + c] = s;
+}
+
 __global__ void sgd_kernel(float* __restrict__ w, const float* __restrict__ g, int64_t n, float lr) {
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
@@ -172,6 +207,20 @@ cudaError_t mlp_mse_grad(float* dout, const float* pred, const float* target, in
   if (e != cudaSuccess) return e;
   mse_grad_kernel<<<blocks, kThreads, 0, s>>>(dout, pred, target, n, n_mean, parts);
   sum_partials_kernel<<<1, kThreads, 0, s>>>(parts, blocks, loss_sum);
+  return cudaGetLastError();
+}
+
+cudaError_t mlp_colsum_finish(const float* part, int64_t n_blocks, int64_t cols, float* out, cudaStream_t s) {
+  colsum_finish8_kernel<<<static_cast<unsigned>((cols + 31) / 32), 256, 0, s>>>(part, static_cast<int>(n_blocks),
+                                                                                cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t tile_colsum32(const float* m, int64_t ldm, int64_t rows, int64_t cols, float* part, int64_t ld_part,
+                          cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 grid(static_cast<unsigned>((cols + 255) / 256), static_cast<unsigned>((rows + 31) / 32));
+  tile_colsum32_kernel<<<grid, 256, 0, s>>>(m, ldm, rows, cols, part, ld_part);
   return cudaGetLastError();
 }
 

@@ -13,6 +13,7 @@
 #include <string>
 
 #include "common.h"
+#include "mlp_kernels.h"
 
 namespace tr {
 
@@ -940,11 +941,13 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
       }
     }
   }
+  std::vector<size_t> cs_pass;  // tasks whose column sums need a pass over the finished tile
   for (size_t q = 0; q < gtids.size(); ++q) {  // write-through: unsplit full tiles only
     int64_t tid = 0;
     const Product& p = job.prod_of(gtids[q], &tid);
     const int32_t wt = write_through(d, s, p, tid / p.grid_cols, tid % p.grid_cols, grp.task[q]);
     if (wt >= 0) wt_phys.push_back(wt);
+    if (p.colsum && !fuse_colsum(p, tid / p.grid_cols, tid % p.grid_cols, grp.task[q])) cs_pass.push_back(q);
   }
   const bool host_c = p0->c.location == TR_LOC_HOST;
   if (host_c) wait_on(d, s, sc.gout_free);  // the previous group's writeback has read the buffer
@@ -956,6 +959,11 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
                                    dc.sms));
     if (grp.k_split > 1)
       for (int t = 0; t < grp.n_tasks; ++t) TR_CUDA(launch_splitk_reduce(grp.task[t], sc.stream));
+    for (size_t q : cs_pass) {
+      int64_t tid = 0;
+      const Product& p = job.prod_of(gtids[q], &tid);
+      colsum_pass(p, tid / p.grid_cols, tid % p.grid_cols, sc.stream);
+    }
     job.launches.fetch_add(grp.k_split > 1 ? grp.n_tasks : 0);
   };
   if (job.async) {
@@ -1035,6 +1043,30 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   TR_CUDA(cudaEventRecord(sc.done, sc.stream));
   sc.task = gtids[0];
   sc.group_rest.assign(gtids.begin() + 1, gtids.end());
+}
+
+// ---------------------------------------------------------------- fused column sums
+// Product::colsum (tr_product.colsum): the 32-row block column sums of task
+// (i, j)'s final output.  fuse_colsum points the launch's epilogue at the
+// tile's block of the partial-sum matrix when K1 stores the tile through its
+// coalesced path (unsplit, fp32, 128-column multiples); false means the caller
+// runs colsum_pass on the finished tile instead.
+bool Session::fuse_colsum(const Product& p, int64_t i, int64_t j, GemmArgs& args, bool small) const {
+  args.colsum = nullptr;
+  if (!p.colsum) return true;
+  if (args.k_split > 1 || args.c_f64) return false;
+  if (!small && (args.n_valid % 128 != 0 || (args.ldc & 3) != 0 || (reinterpret_cast<uintptr_t>(args.c) & 15) != 0))
+    return false;  // K1 sums on its coalesced store path only
+  args.colsum = p.colsum + (i * tile_ / 32) * p.N + j * tile_;
+  args.colsum_ld = p.N;
+  return true;
+}
+
+void Session::colsum_pass(const Product& p, int64_t i, int64_t j, cudaStream_t s) {
+  const int64_t T = tile_;
+  const float* c = static_cast<const float*>(p.c.ptr) + i * T * p.c.ld + j * T;
+  TR_CUDA(tile_colsum32(c, p.c.ld, std::min(T, p.M - i * T), std::min(T, p.N - j * T),
+                        p.colsum + (i * T / 32) * p.N + j * T, p.N, s));
 }
 
 // ---------------------------------------------------------------- write-through
@@ -1145,22 +1177,25 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     }
     const int32_t wt = (!dryrun_ && !narrow && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
     const bool reduce = narrow || args.k_split > 1;
+    // column sums of the final output: fused into K1's epilogue when it stores the tile, else a pass over it
+    const bool cs_pass = !dryrun_ && p.colsum && k0 + kc == ks && (narrow || !fuse_colsum(p, i, j, args, small));
     auto launch = [&] {
       if (narrow) {  // A' = Bᵀ, B' = Aᵀ: the layouts swap roles
         BoxKind ba, bb;
         gemm_boxes(!p.tb, !p.ta, targs.m_valid, &ba, &bb);
         TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], targs, !p.tb, !p.ta, scp->stream));
         TR_CUDA(launch_splitk_reduce_t(args, scp->stream));
-        return;
-      }
-      if (small) {
-        TR_CUDA(launch_small_gemm(dc.slab, ld_, plane_elems_, args, p.ta, p.tb, scp->stream));
       } else {
-        BoxKind ba, bb;
-        gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
-        TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+        if (small) {
+          TR_CUDA(launch_small_gemm(dc.slab, ld_, plane_elems_, args, p.ta, p.tb, scp->stream));
+        } else {
+          BoxKind ba, bb;
+          gemm_boxes(p.ta, p.tb, args.m_valid, &ba, &bb);
+          TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], args, p.ta, p.tb, scp->stream));
+        }
+        if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
       }
-      if (args.k_split > 1) TR_CUDA(launch_splitk_reduce(args, scp->stream));
+      if (cs_pass) colsum_pass(p, i, j, scp->stream);
     };
     if (!dryrun_ && job.async) {
       launch();
@@ -1541,6 +1576,8 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     if (p.post != POST_NONE && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
       fail(TR_ERR_VALUE, "fused epilogues need a float32 device output");
     if (p.post == POST_ACT_GRAD && !p.aux) fail(TR_ERR_VALUE, "POST_ACT_GRAD needs the activation (aux) matrix");
+    if (p.colsum && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32 || T % 32 != 0))
+      fail(TR_ERR_VALUE, "fused column sums need a float32 device output and a tile size that is a multiple of 32");
     if (p.axpy && (p.post != POST_NONE || c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
       fail(TR_ERR_VALUE, "axpy products accumulate into a float32 device matrix, without a post-op");
     p.grid_rows = ceil_div(p.M, T);

@@ -67,6 +67,7 @@ struct Product {
   uint64_t cache_as = 0;  // write-through: the output's tiles enter the cache under this uid
   bool axpy = false;      // C += alpha * A.B (every k-chunk accumulates)
   float alpha = 1.f;
+  float* colsum = nullptr;  // 32-row block column sums of the final output (tr_product.colsum)
 };
 
 struct Job {
@@ -264,6 +265,8 @@ class Session {
   void ensure_slab(int d, int64_t needed);
   void build_tmaps(int d);
   void* lazy_tile(int d, void** p, size_t* cap);
+  bool fuse_colsum(const Product& p, int64_t i, int64_t j, GemmArgs& args, bool small = false) const;
+  void colsum_pass(const Product& p, int64_t i, int64_t j, cudaStream_t s);
   uint16_t* slot_ptr(int d, int32_t phys) const {
     return devs_[d].slab + static_cast<int64_t>(phys) * slot_elems_;
   }

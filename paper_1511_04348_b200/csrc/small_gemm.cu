@@ -230,6 +230,10 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
                    (reinterpret_cast<uintptr_t>(base) & 15) == 0 &&
                    (!args.aux || ((args.ldaux & 3) == 0 && (reinterpret_cast<uintptr_t>(args.aux) & 15) == 0)) &&
                    (!args.wt || (args.wt_ld & 3) == 0);
+  // fused column sums (args.colsum): this thread's 4 columns over its 4 rows,
+  // then the 8 threads of each 32-row block are summed in row order below
+  const bool do_cs = !part && !args.c_f64 && args.colsum != nullptr;
+  float csum[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int64_t r = m0 + ty * 4 + i;
@@ -257,6 +261,12 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
         }
       }
       *d4 = v;
+      if (do_cs) {
+        csum[0] += v.x;
+        csum[1] += v.y;
+        csum[2] += v.z;
+        csum[3] += v.w;
+      }
       if (!part && args.wt) split_store4(args.wt + r * args.wt_ld + c0, args.wt_plane, planes, v);
       continue;
     }
@@ -279,7 +289,24 @@ __global__ void __launch_bounds__(NTH) small_gemm_kernel(const uint16_t* __restr
       if (post == POST_BIAS_ACT) v = act_fwd(args.act, v + (args.bias ? args.bias[c] : 0.f));
       else if (post == POST_ACT_GRAD) v *= act_grad_from_out(args.act, args.aux[r * args.ldaux + c]);
       *dst = v;
+      if (do_cs) csum[j] += v;
       if (args.wt) split_store(args.wt + r * args.wt_ld + c, args.wt_plane, planes, v);
+    }
+  }
+  if (do_cs) {  // (block-uniform branch) 32-row blocks = 8 consecutive ty; sum them in order
+    float(*red)[BN] = reinterpret_cast<float(*)[BN]>(&As[0][0]);  // (NTH / TX) x BN floats
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 4; ++j) red[ty][tx * 4 + j] = csum[j];
+    __syncthreads();
+    if (ty % 8 == 0 && m0 + ty * 4 < args.m_valid) {
+      for (int j = 0; j < 4; ++j) {
+        const int64_t c = c0 + j;
+        if (c >= args.n_valid) break;
+        float s = 0.f;
+        for (int y = ty; y < ty + 8; ++y) s += red[y][tx * 4 + j];
+        args.colsum[((m0 + ty * 4) / 32) * args.colsum_ld + c] = s;
+      }
     }
   }
 }

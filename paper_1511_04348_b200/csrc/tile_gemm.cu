@@ -389,6 +389,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (post == POST_BIAS_ACT && args.bias)
           for (int x = 0; x < 4; ++x) bias4[x] = args.bias[gcol0 + c + x];
         const int row0 = un.m0 + q * 32;
+        // fused column sums of the final values over this warp's 32 rows (in row order)
+        const bool do_cs = !part && args.colsum != nullptr;
+        float4 csum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
         for (int rb = 0; rb < 32; rb += C::STAGE_ROWS) {
           if (lane >= rb && lane < rb + C::STAGE_ROWS) {
@@ -448,11 +451,24 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 v.w *= act_grad_from_out(args.act, pre[i].w);
               }
               *d4 = v;
+              if (do_cs) {
+                csum.x += v.x;
+                csum.y += v.y;
+                csum.z += v.z;
+                csum.w += v.w;
+              }
               if (args.wt)  // write-through: the converted planes of this row segment (as K2)
                 split4(args.wt + grow_i * args.wt_ld + gcol0 + c, args.wt_plane, PLANES, v);
             }
           }
           __syncwarp();
+        }
+        if (do_cs && row0 < args.m_valid) {
+          float* cs = args.colsum + static_cast<int64_t>(row0 / 32) * args.colsum_ld + gcol0 + c;
+          cs[0] = csum.x;
+          cs[1] = csum.y;
+          cs[2] = csum.z;
+          cs[3] = csum.w;
         }
       } else if (grow < args.m_valid && gcol0 < args.n_valid) {
         const int ncols = min(128, args.n_valid - gcol0);

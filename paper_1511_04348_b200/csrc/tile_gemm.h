@@ -67,6 +67,12 @@ struct GemmArgs {
   uint16_t* wt;
   int64_t wt_ld;
   int64_t wt_plane;
+  // Fused column sums (non-null colsum): each epilogue warp also sums its 32
+  // rows of final values per column and stores colsum[(row / 32) * colsum_ld +
+  // col] (tile-relative row / col; the caller offsets the pointer to the tile).
+  // Coalesced unsplit path only; the session runs tile_colsum32 otherwise.
+  float* colsum;
+  int64_t colsum_ld;
 };
 
 // Several tasks in ONE launch (a station's worth of ready tasks): CTAs

@@ -74,7 +74,8 @@ class GpuMLP:
     def __init__(self, layers, machine: Machine | None = None, tile_size: int = 4096, precision: str = "fp32acc",
                  device: int = 0, runtime: Runtime | None = None, stream_ordered: bool = True,
                  process_group=None, write_through: bool = True, fused_sgd: bool = True,
-                 write_through_weights: bool | None = None, skip_input_grad: bool = False):
+                 write_through_weights: bool | None = None, skip_input_grad: bool = False,
+                 fused_colsum: bool = True):
         import torch
 
         self.torch = torch
@@ -99,6 +100,8 @@ class GpuMLP:
         # ann.py:171-172 computes dX of the first layer too, though nothing reads it;
         # True skips that product (cfg3: 784-wide output, ~1.5 % of a step's flops)
         self.skip_input_grad = skip_input_grad
+        # db = colsum(dY) from the dX product's epilogue (32-row block sums) instead of a pass over dY
+        self.fused_colsum = fused_colsum
         self.pg = process_group
         if process_group is not None:
             import torch.distributed as dist
@@ -217,6 +220,7 @@ class GpuMLP:
         grads = [None] * len(self.layers)
         dy_uid = self.rt.fresh_uid("dy")
         update = None  # fused SGD: the layer above's W += (-lr) X^T dY, run with this layer's round
+        cs_parts = None  # block column sums of the current dY (fused into the producing product)
         for li in range(last, -1, -1):
             L = self.layers[li]
             self._step_uids.append(dy_uid)
@@ -227,6 +231,9 @@ class GpuMLP:
                 dx["post"] = ("act_grad", xs[li], self.layers[li - 1].activation)
                 if self.write_through:
                     dx["cache_as"] = next_dy  # dY_{l-1} is the next round's operand
+                if self.fused_colsum and self.layers[li - 1].b is not None and self.rt.tile_size % 32 == 0:
+                    # db_{l-1} = colsum(dY_{l-1}): block sums from the producing epilogue
+                    dx["colsum"] = self._buf(f"cs{li - 1}", (-(-d_x.shape[0] // 32), d_x.shape[1]))
             dw = dict(a=xs[li], b=d_y, transpose_a=True, a_uid=uids[li], b_uid=dy_uid)
             dxs = [] if (li == 0 and self.skip_input_grad) else [dx]
             if lr is None:
@@ -243,10 +250,14 @@ class GpuMLP:
             d_b = None
             if L.b is not None:
                 d_b = self._buf(f"db{li}", L.b.shape)
-                N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
+                if cs_parts is not None:  # the block sums came with dY (fused colsum)
+                    N.call("tr_mlp_colsum_finish", _ptr(cs_parts), cs_parts.shape[0], cs_parts.shape[1], _ptr(d_b), s)
+                else:
+                    N.call("tr_mlp_colsum", _ptr(d_y), d_y.shape[0], d_y.shape[1], _ptr(d_b), s)
             self._allreduce(d_w, d_b)  # overlaps the next (lower) layer's backward round
             grads[li] = (d_w, d_b)
             d_y, dy_uid = d_x, next_dy
+            cs_parts = dx.get("colsum")
         if update:
             self._batch([update])
         return pred.numel(), grads

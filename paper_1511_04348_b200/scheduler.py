@@ -561,7 +561,10 @@ class Runtime:
         later product reads as an input under ``uid``: the producing kernel writes
         its converted tiles straight into the tile cache (tr_product.cache_as).
         ``axpy=alpha`` accumulates instead: out += alpha * a.b (tr_product.axpy; the
-        fused SGD update W += (-lr) X^T dY).  Returns the combined RunStats."""
+        fused SGD update W += (-lr) X^T dY).  ``colsum=buf`` (a float32 CUDA tensor of
+        ceil(rows/32) x cols) receives the 32-row block column sums of the final
+        output, summed by ``tr_mlp_colsum_finish`` (the bias gradient without a pass
+        over the output).  Returns the combined RunStats."""
         if self.mode == "sim":
             raise ValueError("multiply_batch runs on the GPU; the simulated engine takes one product per call")
         acts = {"identity": N.TR_ACT_IDENTITY, "sigmoid": N.TR_ACT_SIGMOID, "relu": N.TR_ACT_RELU}
@@ -581,6 +584,9 @@ class Runtime:
                 q.cache_as = self._uids.id(pr["cache_as"])
             if pr.get("axpy") is not None:  # out += alpha * a.b (float32 device out, no post-op)
                 q.axpy, q.alpha = 1, float(pr["axpy"])
+            if pr.get("colsum") is not None:  # 32-row block column sums of the final output (tr_product.colsum)
+                q.colsum = pr["colsum"].data_ptr()
+                keep.append(pr["colsum"])
             post = pr.get("post")
             if post is not None:
                 kind, ref, act = post

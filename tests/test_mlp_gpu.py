@@ -289,3 +289,49 @@ def test_cfg3_full_shape_losses_vs_f64_oracle():
     for precision, tol in (("fp32acc", 1e-5), ("bf16", 1e-2)):
         errs = [abs(g - r) / abs(r) for g, r in zip(got[precision], ref)]
         assert max(errs) <= tol, (precision, errs)
+
+
+@pytest.mark.parametrize("m,k,n,tile", [(8192, 4096, 8192, 4096),   # full tiles: fused into K1's epilogue
+                                        (1000, 4096, 768, 256),     # ragged rows, split-K launches: tile passes
+                                        (512, 10, 640, 256),        # k = 10: CUDA-core tasks
+                                        (4096, 2048, 10, 4096)])    # 10 wide: transposed tensor-core product
+def test_fused_colsum_block_sums(m, k, n, tile):
+    """tr_product.colsum: the 32-row block column sums of the FINAL output (after
+    the act_grad post-op), whichever kernel path each task takes; summed by
+    tr_mlp_colsum_finish they are db = colsum(dY) (ann.py:173)."""
+    from paper_1511_04348_b200 import _native as N
+
+    g = torch.Generator(device="cuda").manual_seed(m + n)
+    a = torch.randn(m, k, device="cuda", generator=g)
+    b = torch.randn(k, n, device="cuda", generator=g)
+    act = torch.rand(m, n, device="cuda", generator=g)
+    out = torch.empty(m, n, device="cuda")
+    parts = torch.full((-(-m // 32), n), float("nan"), device="cuda")
+    with Runtime(homogeneous_machine(1, dtype=np.float32), tile) as rt:
+        rt.multiply_batch([dict(a=a, b=b, out=out, post=("act_grad", act, "sigmoid"), colsum=parts)])
+    torch.cuda.synchronize()
+    ref = torch.nn.functional.pad(out.double(), (0, 0, 0, parts.shape[0] * 32 - m)).view(-1, 32, n).sum(1)
+    assert not torch.isnan(parts).any()
+    assert float(torch.linalg.norm(parts.double() - ref) / torch.linalg.norm(ref)) <= 1e-6
+    db = torch.empty(n, device="cuda")
+    N.call("tr_mlp_colsum_finish", parts.data_ptr(), parts.shape[0], n, db.data_ptr(), None)
+    torch.cuda.synchronize()
+    want = out.double().sum(0)
+    assert float(torch.linalg.norm(db.double() - want) / torch.linalg.norm(want)) <= 1e-6
+
+
+def test_fused_colsum_same_trajectory_as_colsum_pass():
+    sizes = [300, 512, 256, 10]
+    rng = np.random.default_rng(43)
+    layers = [Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
+                           tag=f"layer{i}") for i in range(3)]
+    x = torch.as_tensor(rng.uniform(-1, 1, (1024, sizes[0])), dtype=torch.float32).cuda()
+    t = torch.as_tensor(rng.uniform(-1, 1, (1024, sizes[-1])), dtype=torch.float32).cuda()
+    runs = {}
+    for fused in (False, True):
+        mlp = GpuMLP(layers, machine=homogeneous_machine(1, dtype=np.float32), tile_size=256, fused_colsum=fused)
+        runs[fused] = ([mlp.train_step(x, t, 0.1) for _ in range(4)], mlp.to_host())
+        mlp.close()
+    assert np.allclose(runs[False][0], runs[True][0], rtol=1e-6, atol=0)
+    for (w0, b0), (w1, b1) in zip(runs[False][1], runs[True][1]):
+        assert relerr(w1, w0) <= 1e-6 and relerr(b1, b0) <= 1e-6
