@@ -5,6 +5,8 @@
 #include <sched.h>
 
 #include <algorithm>
+#include <cctype>
+#include <cstdio>
 #include <cstdlib>
 #include <chrono>
 #include <cstring>
@@ -21,16 +23,54 @@ namespace {
 
 int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
-void pin_thread_to_core(int index) {
+// CPUs of the NUMA node the GPU's PCIe root hangs off (sysfs), empty when
+// unknown (numa_node -1: one node, or a VM that hides it).
+std::vector<int> gpu_local_cpus(int gpu) {
+  std::vector<int> out;
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), gpu) != cudaSuccess) {
+    cudaGetLastError();
+    return out;
+  }
+  for (char* p = bus; *p; ++p) *p = static_cast<char>(tolower(*p));
+  int node = -1;
+  if (FILE* f = fopen((std::string("/sys/bus/pci/devices/") + bus + "/numa_node").c_str(), "r")) {
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+  }
+  if (node < 0) return out;
+  char list[4096] = {0};
+  if (FILE* f = fopen(("/sys/devices/system/node/node" + std::to_string(node) + "/cpulist").c_str(), "r")) {
+    if (!fgets(list, sizeof(list), f)) list[0] = 0;
+    fclose(f);
+  }
+  for (char* tok = strtok(list, ",\n"); tok; tok = strtok(nullptr, ",\n")) {  // "0-15,32-47"
+    int a = -1, b = -1;
+    if (sscanf(tok, "%d-%d", &a, &b) == 2)
+      for (int c = a; c <= b; ++c) out.push_back(c);
+    else if (sscanf(tok, "%d", &a) == 1)
+      out.push_back(a);
+  }
+  return out;
+}
+
+// Pin device `index`'s worker to one core: of the GPU's NUMA node when sysfs
+// names one (its host copies stay on the local memory controller), else of the
+// whole allowed set; core 0 of the set stays with the calling (Python) thread.
+void pin_thread_to_core(int index, int gpu) {
   cpu_set_t allowed;
   CPU_ZERO(&allowed);
   if (sched_getaffinity(0, sizeof(allowed), &allowed) != 0) return;
-  std::vector<int> cores;
+  std::vector<int> cores, local;
   for (int c = 0; c < CPU_SETSIZE; ++c)
     if (CPU_ISSET(c, &allowed)) cores.push_back(c);
-  if (cores.size() < 2) return;
-  // core 0 of the allowed set stays with the calling (Python) thread
-  const int core = cores[1 + index % static_cast<int>(cores.size() - 1)];
+  if (gpu >= 0)
+    for (int c : gpu_local_cpus(gpu))
+      if (c < CPU_SETSIZE && CPU_ISSET(c, &allowed) && c != cores.front()) local.push_back(c);
+  int core = -1;
+  if (!local.empty()) core = local[static_cast<size_t>(index) % local.size()];
+  else if (cores.size() >= 2) core = cores[1 + index % static_cast<int>(cores.size() - 1)];
+  if (core < 0) return;
   cpu_set_t one;
   CPU_ZERO(&one);
   CPU_SET(core, &one);
@@ -1445,7 +1485,7 @@ void Session::run_job(int d, Job& job) {
 }
 
 void Session::worker_main(int d) {
-  pin_thread_to_core(d);
+  pin_thread_to_core(d, dryrun_ ? -1 : devs_[d].gpu);
   if (!dryrun_) cudaSetDevice(devs_[d].gpu);
   uint64_t seen = 0;
   for (;;) {
