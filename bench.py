@@ -385,7 +385,8 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
     last = stats[-1]
     cs = last.cache
     wb_bw = links["d2h_gbs"] * 1e9 * ng
-    t_roof_value = max(flops / (ng * mode_burst), cs.bytes_writeback / wb_bw)
+    t_roof_value = max(flops / (ng * mode_sust), cs.bytes_writeback / wb_bw)
+    t_roof_value_b = max(flops / (ng * mode_burst), cs.bytes_writeback / wb_bw)
     err_value, nr, nc = band_parity(a, a, c, T, seed=40)
     out["value"] = {"tflops": flops / t_step / 1e12, "ms_per_step": t_step * 1e3, "steps": args.steps,
                     "warmup": warm, "gpu_launches": launches,
@@ -393,13 +394,16 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
                     "tasks_by_device": last.tasks_by_device,
                     "first_warmup_cache": first.cache.as_dict() if first else None,
                     "roofline_time_ms": t_roof_value * 1e3, "frac_of_roofline": t_roof_value / t_step,
-                    "roofline_def": "max(2N^3 / (n_gpus * bf16 burst peak / 3), bytes_writeback / (n_gpus * D2H GB/s "
-                                    "measured in this run))"}
-    out["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": peaks["burst"], "unit": UNIT,
-                       "frac": achieved / peaks["burst"], "traffic": profile_traffic("cfg4"),
-                       "peak_source": peaks["source"], "mode_peak": peaks["burst"] / passes,
-                       "frac_of_mode_peak": achieved / (peaks["burst"] / passes),
-                       "frac_of_mode_peak_sustained": achieved / (peaks["sustained"] / passes),
+                    "frac_of_roofline_burst_peak": t_roof_value_b / t_step,
+                    "roofline_def": "max(2N^3 / (n_gpus * sustained bf16 peak / 3), bytes_writeback / (n_gpus * D2H "
+                                    "GB/s measured in this run))"}
+    # the kernel is timed inside long steps (11 s products back to back): the
+    # sustained bf16 figure is its denominator (the burst one is kept beside it)
+    out["roofline"] = {"bound": "tensor", "achieved": achieved, "peak": peaks["sustained"], "unit": UNIT,
+                       "frac": achieved / peaks["sustained"], "traffic": profile_traffic("cfg4"),
+                       "peak_source": peaks["source_sustained"], "mode_peak": peaks["sustained"] / passes,
+                       "frac_of_mode_peak": achieved / (peaks["sustained"] / passes),
+                       "frac_of_mode_peak_burst": achieved / (peaks["burst"] / passes),
                        "kernel": "tile_gemm_kernel (tcgen05 2-CTA 256x256, split-bf16 x3)" if passes == 3
                        else "tile_gemm_kernel (tcgen05 2-CTA 256x256, bf16)",
                        "per_launch": f"{per_launch / (2.0 * T * T * n):g} task(s) of 2*{T}*{T}*{n} flops",
@@ -441,9 +445,9 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
                   "warmup": 1, "call": f"paper_1511_04348_b200.run(machine, A_host_pinned, B_host_pinned, {T})",
                   "steps_ms_event_wall": detail, "cache": ce.as_dict(), "tasks_by_device": stats_e2e.tasks_by_device,
                   "steals": len(stats_e2e.steal_events),
-                  "roofline_time_ms": t_roof * 1e3, "frac_of_roofline": t_roof / t_e2e,
-                  "frac_of_roofline_sustained_peak": t_roof_s / t_e2e,
-                  "roofline_def": "max(2N^3 / (n_gpus * bf16 peak / 3), bytes_host / aggregate H2D GB/s, "
+                  "roofline_time_ms": t_roof_s * 1e3, "frac_of_roofline": t_roof_s / t_e2e,
+                  "frac_of_roofline_burst_peak": t_roof / t_e2e,
+                  "roofline_def": "max(2N^3 / (n_gpus * sustained bf16 peak / 3), bytes_host / aggregate H2D GB/s, "
                                   "bytes_writeback / aggregate D2H GB/s), link rates measured in this run",
                   "sim_reference_schedule_ms": {str(w): sim_prediction_ms(tr, n, T, w, args.precision, links)
                                                 for w in sorted({1, 2, 4, 8, ng})}}
@@ -1158,9 +1162,11 @@ def run_ours(args, ng) -> dict:
     torch.cuda.set_device(gpus[0])
     machine = tr.homogeneous_machine(ng, dtype=np.float32, gpus=gpus)
     mp = measured_peaks()
-    peaks = {"burst": mp.get("bf16_tflops", 1590.0), "sustained": mp.get("bf16_tflops_sustained", 1590.0),
-             "source": "MEASURED_PEAKS.json bf16_tflops (burst) / bf16_tflops_sustained" if mp else
-             "fallback 1.59 PFLOP/s (B200_PROFILING.md)"}
+    peaks = {"burst": mp.get("bf16_tflops", 1590.0), "sustained": mp.get("bf16_tflops_sustained", 1400.0),
+             "source": "MEASURED_PEAKS.json bf16_tflops (burst, kernel timed alone)" if mp else
+             "fallback 1.59 PFLOP/s burst (B200_PROFILING.md)",
+             "source_sustained": "MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside long steps)" if mp
+             else "fallback ~1.4 PFLOP/s sustained (B200_PROFILING.md)"}
 
     def free_hbm():
         tr.release_cached_memory()
