@@ -9,7 +9,8 @@ Same algebra and the same 3·L products per step as the reference's
               dW_l = X_l^T dY_l        (product, transposed A: layout, no copy)
               dX_l = dY_l W_l^T        (product, transposed B; also for l = 0,
                                         as the reference does)
-              db_l = colsum dY_l                                           (K5)
+              db_l = colsum dY_l   (K5; for l < L-1 summed from the 32-row block
+                                    sums the dX product's epilogue emits with dY_l)
     update    W_l -= lr dW_l ; b_l -= lr db_l ; version += 1               (K6)
 
 Every product is ``Runtime.multiply`` on device-resident operands: tiles are
