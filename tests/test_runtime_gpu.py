@@ -534,3 +534,18 @@ def test_green_context_devices_1234():
     ref = a[rows].double() @ b.double()
     assert rel(c[rows].double().cpu().numpy(), ref.cpu().numpy()) <= 1e-5
     rt.close()
+
+
+def test_standalone_rates_follow_sm_counts():
+    """standalone_rates: each device's throughput alone; identical specs are
+    measured once, and an 8-SM green context runs at about half a 16-SM one."""
+    from paper_1511_04348_b200 import standalone_rates
+
+    T = 1024
+    a = torch.randn(4 * T, 4 * T, device="cuda")
+    b = torch.randn(4 * T, 4 * T, device="cuda")
+    c = torch.empty(4 * T, 4 * T, device="cuda")
+    m = Machine([DeviceSpec(0, gpu=0, sms=16), DeviceSpec(1, gpu=0, sms=8), DeviceSpec(2, gpu=0, sms=16)],
+                ProximityMatrix.uniform(3), dtype=np.float32)
+    r = standalone_rates(m, T, a, b, out=c)
+    assert r[0] == r[2] and 0.35 <= r[1] / r[0] <= 0.65, r

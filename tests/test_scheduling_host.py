@@ -297,3 +297,19 @@ def test_completion_bitmap_contract_and_native_view():
     with Runtime(homogeneous_machine(2), 4, mode="dryrun") as rt:
         _, s = rt.multiply(np.zeros((12, 8)), np.zeros((8, 16)))
     assert s.completion.all_done() and s.completion.done_count == s.total_tasks == 12
+
+
+def test_directory_lock_stats_dryrun():
+    """Runtime.lock_stats (tr_session_lock_stats): every directory operation is one
+    acquisition of the instrumented lock; reset=True zeroes the counters."""
+    import numpy as np
+
+    from paper_1511_04348_b200 import Runtime, homogeneous_machine
+
+    with Runtime(homogeneous_machine(3), 4, mode="dryrun") as rt:
+        rt.lock_stats(reset=True)
+        rt.multiply(np.zeros((16, 12)), np.zeros((12, 20)))
+        st = rt.lock_stats(reset=True)
+        assert st["acquisitions"] >= 2 * 4 * 5 * 3  # >= one per input request (20 tasks x 3 k-steps x A, B)
+        assert st["held_s"] >= 0 and st["waited_s"] >= 0 and st["max_hold_us"] >= 0
+        assert rt.lock_stats()["acquisitions"] < st["acquisitions"]
