@@ -335,3 +335,28 @@ def test_fused_colsum_same_trajectory_as_colsum_pass():
     assert np.allclose(runs[False][0], runs[True][0], rtol=1e-6, atol=0)
     for (w0, b0), (w1, b1) in zip(runs[False][1], runs[True][1]):
         assert relerr(w1, w0) <= 1e-6 and relerr(b1, b0) <= 1e-6
+
+
+def test_tile_parallel_mlp_on_green_context_devices():
+    """cfg5's machine in miniature: the MLP's products shared tile by tile (the
+    reference's TiledBackend semantics, ann.py:78-104) by three green-context
+    devices, one throttled; 5 SGD steps against the float64 oracle, and every
+    device did part of the work."""
+    from paper_1511_04348_b200 import DeviceSpec, Machine, ProximityMatrix
+
+    sizes = [256, 1024, 768, 10]
+    rng = np.random.default_rng(47)
+    layers = [Layer.random(sizes[i], sizes[i + 1], rng, activation="sigmoid", scale=1.0 / np.sqrt(sizes[i]),
+                           tag=f"layer{i}") for i in range(3)]
+    x, t = O.random_regression(rng, 512, sizes[0], sizes[-1])
+    m = Machine([DeviceSpec(0, gpu=0, sms=16), DeviceSpec(1, gpu=0, sms=16), DeviceSpec(2, gpu=0, sms=8, slots=2)],
+                ProximityMatrix.uniform(3), dtype=np.float32)
+    mlp = GpuMLP(layers, machine=m, tile_size=128)
+    xd = torch.as_tensor(x, dtype=torch.float32).cuda()
+    td = torch.as_tensor(t, dtype=torch.float32).cuda()
+    got = [mlp.train_step(xd, td, 0.1) for _ in range(5)]
+    assert all(v > 0 for v in mlp.device_macs), mlp.device_macs
+    mlp.close()
+    ol = [O.OracleLayer(np.array(L.weights, np.float64), np.array(L.bias, np.float64), "sigmoid") for L in layers]
+    ref = [O.train_step(ol, x, t, 0.1, matmul=O.blas_matmul) for _ in range(5)]
+    assert max(abs(g - r) / r for g, r in zip(got, ref)) <= 1e-5, (got, ref)
