@@ -507,8 +507,14 @@ def bench_cfg2(args, tr, torch, machine, gpus, links):
             launches = max(1, s.gpu_launches)
             avg = sum(s.kernel_ms.values()) / launches
             err, nr, nc = band_parity(A, B, C, T, seed=20)
+            launch_tf = flops / launches / (avg / 1e3) / 1e12
+            mp = measured_peaks()
+            passes = 3 if prec == "fp32acc" else 1
             out[prec] = {"tflops": flops / t / 1e12, "ms_per_step": t * 1e3, "steps": args.cfg2_steps,
-                         "avg_launch_ms": avg, "launch_tflops": flops / launches / (avg / 1e3) / 1e12,
+                         "avg_launch_ms": avg, "launch_tflops": launch_tf,
+                         "launch_frac_of_mode_peak_burst": launch_tf / (mp.get("bf16_tflops", 1590.0) / passes),
+                         "launch_frac_of_mode_peak_sustained": launch_tf / (mp.get("bf16_tflops_sustained", 1400.0)
+                                                                            / passes),
                          "tasks_by_device": s.tasks_by_device, "l2_hits": s.cache.l2_hits,
                          "parity": parity_entry(err, prec, f"{nr} rows x {nc} cols (>=8 per tile band)")}
     # cold e2e through run() on pinned host arrays
