@@ -131,7 +131,13 @@ def test_cfg4_full_size_out_of_core_band_sampled():
     from paper_1511_04348_b200 import Runtime
     from paper_1511_04348_b200.matrix import pinned_empty
 
+    from paper_1511_04348_b200 import release_cached_memory
+
     n, T = 131072, 4096
+    # the slab must hold both operands' planes (128 GiB): hand back what earlier
+    # tests left in torch's and the runtime's caches
+    torch.cuda.empty_cache()
+    release_cached_memory()
     torch._C._host_emptyCache()
     a = pinned_empty((n, n), np.float32)
     c = pinned_empty((n, n), np.float32)
