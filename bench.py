@@ -361,6 +361,7 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
         _, s = rt.multiply(a, a, a_uid="A", b_uid="B", c_uid="C", out=c)
         if w == 0:
             first = s
+    rt.lock_stats(reset=True)
     with ClockSampler(gpus) as clk:
         for gg in gpus:
             torch.cuda.synchronize(gg)
@@ -377,6 +378,9 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
     # ev0/ev1 on the first GPU's current stream; every product ends with a host
     # sync of all devices, so the interval covers the K products on all GPUs
     t_step = ev0.elapsed_time(ev1) / 1e3 / args.steps
+    lock = rt.lock_stats(reset=True)
+    lock = {"held_ms_per_step": lock["held_s"] * 1e3 / args.steps, "waited_ms_per_step": lock["waited_s"] * 1e3 /
+            args.steps, "acquisitions_per_step": lock["acquisitions"] // args.steps, "max_hold_us": lock["max_hold_us"]}
     launches = sum(s.gpu_launches for s in stats)
     kms = sum(sum(s.kernel_ms.values()) for s in stats)
     per_launch = flops * args.steps / max(1, launches)
@@ -392,6 +396,7 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
                     "warmup": warm, "gpu_launches": launches,
                     "cache_last_step": cs.as_dict(),
                     "tasks_by_device": last.tasks_by_device,
+                    "directory_lock": lock,
                     "first_warmup_cache": first.cache.as_dict() if first else None,
                     "roofline_time_ms": t_roof_value * 1e3, "frac_of_roofline": t_roof_value / t_step,
                     "frac_of_roofline_burst_peak": t_roof_value_b / t_step,
