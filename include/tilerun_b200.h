@@ -361,6 +361,10 @@ int tr_session_set_async(tr_session* s, int on);
  * 256 x 256 per pair) for tiles taller than 128 rows, 0 = single CTAs
  * (128 x 256, default).  Also settable with TR_GEMM_PAIRS=1 in the environment. */
 int tr_set_gemm_pairs(int32_t on);
+/* Grouped launches as TMA-multicast clusters of two CTA pairs sharing their A
+ * tile (0 = off, the default; TR_GEMM_MC=1).  Measured slower on B200: only 33
+ * such clusters (132 SMs) are co-resident against 74 pairs (148 SMs). */
+int tr_set_gemm_multicast(int32_t on);
 
 /* Split-K policy (process-wide): at most `max_splits` (1..8) K-splits per tile
  * GEMM launch whose output has fewer 128 x 256 blocks than the GPU has SMs

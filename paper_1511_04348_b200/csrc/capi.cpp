@@ -488,6 +488,9 @@ int tr_set_gemm_pairs(int32_t on) {
   return guarded([&] { tr::set_gemm_pairs(on != 0); });
 }
 
+int tr_set_gemm_multicast(int32_t on) {
+  return guarded([&] { tr::set_gemm_multicast(on != 0); });
+}
 int tr_set_task_group(int32_t max_tasks) {
   return guarded([&] {
     if (max_tasks < 1 || max_tasks > tr::kMaxGroup) tr::fail(TR_ERR_VALUE, "task group must be in 1..%d", tr::kMaxGroup);

@@ -991,12 +991,9 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
   }
   const bool host_c = p0->c.location == TR_LOC_HOST;
   if (host_c) wait_on(d, s, sc.gout_free);  // the previous group's writeback has read the buffer
-  BoxKind ba, bb;
-  gemm_boxes(p0->ta, p0->tb, grp.task[0].m_valid, &ba, &bb, /*grouped=*/true);
   auto launch = [&] {
-    TR_CUDA(launch_tile_gemm_group(dc.tmap[ba], dc.tmap[bb], grp, p0->ta, p0->tb,
-                                   persistent_enabled() && !dc.host_fills, sc.stream,
-                                   dc.sms));
+    TR_CUDA(launch_tile_gemm_group_maps(dc.tmap, grp, p0->ta, p0->tb, persistent_enabled() && !dc.host_fills,
+                                        sc.stream, dc.sms));
     if (grp.k_split > 1)
       for (int t = 0; t < grp.n_tasks; ++t) TR_CUDA(launch_splitk_reduce(grp.task[t], sc.stream));
     for (size_t q : cs_pass) {

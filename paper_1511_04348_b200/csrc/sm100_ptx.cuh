@@ -190,6 +190,18 @@ __device__ __forceinline__ void tma_load_3d_cg2(void* smem_dst, const CUtensorMa
       : "memory");
 }
 
+// 2-SM TMA with multicast: the box lands at the same smem offset in every CTA of
+// `mask`; each destination's completion bytes go to the barrier at
+// `bar_cluster_addr`'s offset in that destination's pair leader.
+__device__ __forceinline__ void tma_load_3d_cg2_mc(void* smem_dst, const CUtensorMap* tm, uint32_t bar_cluster_addr,
+                                                   uint16_t mask, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%4, %5, %6}], [%2], %3;" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(bar_cluster_addr), "h"(mask), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 __device__ __forceinline__ void tmem_alloc_cg2(uint32_t* slot_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot_smem)),
                "r"(ncols)

@@ -90,10 +90,13 @@ struct Cfg {
 struct Unit {
   int t, m0, n0, z, nz;
 };
-template <int CG>
+// MC = 2 (TMA multicast, clusters of two CTA pairs): a unit is 256 x 512 --
+// pair p of the cluster computes columns [n0 + 256 p, n0 + 256 p + 256) of the
+// same 256 rows; rank = the CTA's rank in the cluster.
+template <int CG, int MC = 1>
 __device__ __forceinline__ Unit unit_of(const GemmGroup& grp, int u, uint32_t rank) {
   Unit r;
-  const int tiles = grp.cta_begin[grp.n_tasks] / CG;
+  const int tiles = grp.cta_begin[grp.n_tasks] / (CG * MC);
   if (grp.k_split > 1) {
     r.z = u / tiles;
     r.nz = grp.k_split;
@@ -102,14 +105,15 @@ __device__ __forceinline__ Unit unit_of(const GemmGroup& grp, int u, uint32_t ra
     r.z = static_cast<int>(blockIdx.z);
     r.nz = static_cast<int>(gridDim.z);
   }
-  const int cta = u * CG;  // the tile's first CTA index in the flattened (non-persistent) grid
+  const int cta = u * CG * MC;  // the unit's first CTA index in the flattened (non-persistent) grid
   int t = 0;
   while (t + 1 < grp.n_tasks && cta >= grp.cta_begin[t + 1]) ++t;
-  const int local = cta - grp.cta_begin[t];
-  const int m_cta = local % grp.m_blocks[t];
+  const int local_unit = (cta - grp.cta_begin[t]) / (CG * MC);
+  const int mb = grp.m_blocks[t] / CG;  // row blocks of BM * CG rows, fastest
+  const int in_pair = static_cast<int>(rank) % CG, pair = static_cast<int>(rank) / CG;
   r.t = t;
-  r.m0 = (m_cta / CG) * (BM * CG) + static_cast<int>(rank) * BM;
-  r.n0 = (local / grp.m_blocks[t]) * BN;
+  r.m0 = (local_unit % mb) * (BM * CG) + in_pair * BM;
+  r.n0 = ((local_unit / mb) * MC + pair) * BN;
   return r;
 }
 
@@ -133,10 +137,11 @@ __device__ __forceinline__ KRange krange(const GemmArgs& args, int z, int nz) {
 // the MMA issuer run straight across units; the epilogue warps drain unit i's
 // TMEM partial sums while the tensor core already computes unit i+1 into the
 // other TMEM buffer, so the store of one tile overlaps the next tile's k-loop.
-template <bool A_MN, bool B_K, int PLANES, int CG>
+template <bool A_MN, bool B_K, int PLANES, int CG, int MC = 1>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     tile_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                      const __grid_constant__ GemmGroup grp) {
+  static_assert(MC == 1 || CG == 2, "multicast clusters are made of CTA pairs");
   using C = Cfg<PLANES, CG>;
   constexpr int STAGES = C::STAGES;
   constexpr int STAGE_BYTES = C::STAGE_BYTES;
@@ -154,11 +159,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;  // 0 = leader of the pair
-  const bool leader = rank == 0;
-  const int n_units = (grp.cta_begin[grp.n_tasks] / CG) * (grp.k_split > 1 ? grp.k_split : 1);
-  const int first_unit = static_cast<int>(blockIdx.x) / CG;
-  const int unit_stride = static_cast<int>(gridDim.x) / CG;
+  // rank in the cluster; the CTA pair = ranks {2p, 2p + 1}, its leader 2p
+  const uint32_t rank = (CG == 2) ? ptx::cluster_ctarank() : 0u;
+  const uint32_t lead_rank = rank & ~1u;
+  const bool leader = rank == lead_rank;
+  const uint16_t pair_mask = static_cast<uint16_t>(0x3u << lead_rank);
+  const int n_units = (grp.cta_begin[grp.n_tasks] / (CG * MC)) * (grp.k_split > 1 ? grp.k_split : 1);
+  const int first_unit = static_cast<int>(blockIdx.x) / (CG * MC);
+  const int unit_stride = static_cast<int>(gridDim.x) / (CG * MC);
 
   if (warp == 0 && lane == 0) {
     ptx::tma_prefetch_desc(&tmA);
@@ -167,7 +175,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   if (warp == 1 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
-      ptx::mbar_init(&empty[s], 1);
+      ptx::mbar_init(&empty[s], MC);  // MC = 2: a stage is free once BOTH pairs' MMAs read it
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&acc_full[b], 1);
@@ -195,9 +203,9 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = first_unit; u < n_units; u += unit_stride) {
-        const Unit un = unit_of<CG>(grp, u, rank);
+        const Unit un = unit_of<CG, MC>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
-        const int nb0 = un.n0 + static_cast<int>(rank) * BN_LOCAL;  // B columns this CTA stages
+        const int nb0 = un.n0 + static_cast<int>(rank - lead_rank) * BN_LOCAL;  // B columns this CTA stages
         const KRange kr = krange(args, un.z, un.nz);
         int g = 0;  // global k-block index
         for (int ks = 0; ks < args.n_ksteps; ++ks) {
@@ -210,8 +218,8 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             uint8_t* sa = smem + stage * STAGE_BYTES;
             uint8_t* sb = sa + PLANES * A_BYTES;
             const int k0 = kb * BK;
-            // completion bytes of both CTAs go to the leader's full barrier
-            const uint32_t bar = (CG == 2) ? ptx::mapa_shared(full0 + stage * 8, 0) : 0u;
+            // completion bytes of both CTAs go to the pair leader's full barrier
+            const uint32_t bar = (CG == 2) ? ptx::mapa_shared(full0 + stage * 8, lead_rank) : 0u;
             if (leader) ptx::mbar_arrive_expect_tx(&full[stage], CG * STAGE_BYTES);
             auto load = [&](void* dst, const CUtensorMap* tm, int c0, int c1, int c2) {
               if (CG == 2) ptx::tma_load_3d_cg2(dst, tm, bar, c0, c1, c2);
@@ -219,7 +227,19 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             };
 #pragma unroll
             for (int p = 0; p < PLANES; ++p) {
-              if (!A_MN) {
+              if (MC == 2) {
+                // the two pairs need the same A rows: each CTA loads half of its
+                // 128-row A tile (64 rows) and multicasts it to itself and to the
+                // same-position CTA of the other pair (64-row boxes either layout)
+                const int h = static_cast<int>(rank >> 1);  // which half this CTA loads
+                const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank ^ 2u)));
+                if (!A_MN)
+                  ptx::tma_load_3d_cg2_mc(sa + p * A_BYTES + h * (A_BYTES / 2), &tmA, bar, mask, k0, un.m0 + 64 * h,
+                                          az + p);
+                else
+                  ptx::tma_load_3d_cg2_mc(sa + p * A_BYTES + h * MN_GROUP_BYTES, &tmA, bar, mask, un.m0 + 64 * h, k0,
+                                          az + p);
+              } else if (!A_MN) {
                 load(sa + p * A_BYTES, &tmA, k0, un.m0, az + p);
               } else {
 #pragma unroll
@@ -253,7 +273,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       uint32_t phase = 0;
       int seg = 0;  // TMEM partial sums issued so far (all units)
       for (int u = first_unit; u < n_units; u += unit_stride) {
-        const Unit un = unit_of<CG>(grp, u, rank);
+        const Unit un = unit_of<CG, MC>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
         const KRange kr = krange(args, un.z, un.nz);
         const int seg_kb = args.seg_kb > 0 ? args.seg_kb : max(kr.hi - kr.lo, 1);
@@ -299,10 +319,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                   acc = 1;
                 }
               }
-              if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], 0x3);
+              // the stage's smem is released in every CTA that received its data
+              if (CG == 2) ptx::mma_commit_cg2_mc(&empty[stage], MC == 2 ? 0xF : pair_mask);
               else ptx::mma_commit(&empty[stage]);
               if (seg_done) {
-                if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+                if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], pair_mask);
                 else ptx::mma_commit(&acc_full[seg & 1]);
               }
             }
@@ -320,7 +341,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         }
         if (kb_in_seg != 0) {  // the unit's last, partial segment
           if (ptx::elect_one()) {
-            if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], 0x3);
+            if (CG == 2) ptx::mma_commit_cg2_mc(&acc_full[seg & 1], pair_mask);
             else ptx::mma_commit(&acc_full[seg & 1]);
           }
           __syncwarp();
@@ -336,11 +357,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const int half = (warp - EPI_WARP0) >> 2;    // column half of the 256-wide tile
     const int row = q * 32 + lane;
     const uint32_t tlane = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(half * 128);
-    const uint32_t empty_leader = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), 0) : 0u;
+    const uint32_t empty_leader = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), lead_rank) : 0u;
     float* stage = epi_stage + (warp - EPI_WARP0) * (C::STAGE_ROWS * C::STAGE_LD);
     int seg = 0;
     for (int u = first_unit; u < n_units; u += unit_stride) {
-      const Unit un = unit_of<CG>(grp, u, rank);
+      const Unit un = unit_of<CG, MC>(grp, u, rank);
       const GemmArgs& args = grp.task[un.t];
       const KRange kr = krange(args, un.z, un.nz);
       const int my_kb = kr.hi - kr.lo;
@@ -510,14 +531,32 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
-template <bool A_MN, bool B_K, int PLANES, int CG>
+template <bool A_MN, bool B_K, int PLANES, int CG, int MC = 1>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
                            bool persistent, int sm_budget, cudaStream_t stream) {
   using C = Cfg<PLANES, CG>;
-  auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG>;
+  auto kern = tile_gemm_kernel<A_MN, B_K, PLANES, CG, MC>;
+  constexpr int CL = CG * MC;  // CTAs per cluster
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [&] { attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM); });
+  static int max_clusters = 0;  // co-resident clusters of CL CTAs (MC = 2: GPC granularity)
+  std::call_once(once, [&] {
+    attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if (attr_err == cudaSuccess && MC > 1) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(CL * 64);
+      q.blockDim = dim3(NUM_THREADS);
+      q.dynamicSmemBytes = C::SMEM;
+      cudaLaunchAttribute qa[1];
+      qa[0].id = cudaLaunchAttributeClusterDimension;
+      qa[0].val.clusterDim.x = CL;
+      qa[0].val.clusterDim.y = 1;
+      qa[0].val.clusterDim.z = 1;
+      q.attrs = qa;
+      q.numAttrs = 1;
+      attr_err = cudaOccupancyMaxActiveClusters(&max_clusters, kern, &q);
+    }
+  });
   if (attr_err != cudaSuccess) return attr_err;
   // flattened grid: task t owns CTAs [cta_begin[t], cta_begin[t+1]), M-blocks fastest
   g.cta_begin[0] = 0;
@@ -531,7 +570,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
   if (persistent) {
     int dev = 0, sms = sm_budget;
     if (sms <= 0 && cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    ctas = std::min(ctas, std::max(CG, (sms / CG) * CG));
+    ctas = std::min(ctas, MC > 1 ? std::max(CL, max_clusters * CL) : std::max(CG, (sms / CG) * CG));
   }
   dim3 grid(static_cast<unsigned>(ctas), 1, (k_split > 1 && g.k_split <= 1) ? k_split : 1);
   if (CG == 1) {
@@ -545,7 +584,7 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = CL;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
@@ -681,7 +720,10 @@ void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* 
 
 static cudaError_t dispatch(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split, bool a_mn,
                             bool b_kmajor, bool pair, int planes, bool persistent, cudaStream_t stream,
-                            int sm_budget = 0) {
+                            int sm_budget = 0, bool mc = false) {
+  if (mc && pair && !a_mn && !b_kmajor)  // TMA-multicast clusters of two CTA pairs (opt-in; see gemm_multicast)
+    return planes == 2 ? launch_variant<false, false, 2, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream)
+                       : launch_variant<false, false, 1, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
   const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (planes == 2 ? 1 : 0) | (pair ? 8 : 0);
   switch (variant) {
     case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
@@ -736,6 +778,53 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
       return cudaErrorInvalidValue;
   }
   return dispatch(tmA, tmB, g, 1, a_mn, b_kmajor, pair, g.task[0].planes, persistent, stream, sm_budget);
+}
+
+// Whether a grouped launch runs as TMA-multicast clusters (two CTA pairs sharing
+// A: 256 x 512 units, the A tile loaded once per cluster and multicast).  Opt-in
+// (TR_GEMM_MC=1 / set_gemm_multicast): a B200 co-schedules only 33 clusters of
+// four one-CTA-per-SM CTAs (132 SMs) against 74 pairs (148 SMs).
+static std::atomic<int> g_mc{-1};
+
+bool gemm_multicast_enabled() {
+  int v = g_mc.load();
+  if (v < 0) {
+    const char* e = getenv("TR_GEMM_MC");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_mc.store(v);
+  }
+  return v != 0;
+}
+
+void set_gemm_multicast(bool on) { g_mc.store(on ? 1 : 0); }
+
+static bool group_multicast(const GemmGroup& g, bool a_mn, bool b_kmajor, int sm_budget) {
+  if (!gemm_multicast_enabled() || a_mn || b_kmajor || g.k_split > 1 || !group_uses_pairs(g.task[0].m_valid))
+    return false;
+  if (sm_budget > 0) {  // a green-context device: its SM count, not the whole GPU's
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess || sm_budget < sms)
+      return false;
+  }
+  for (int t = 0; t < g.n_tasks; ++t)
+    if (g.task[t].n_valid % (2 * BN) != 0 || g.task[t].k_split > 1) return false;
+  return true;
+}
+
+cudaError_t launch_tile_gemm_group_maps(const CUtensorMap* maps, GemmGroup& g, bool a_mn, bool b_kmajor,
+                                        bool persistent, cudaStream_t stream, int sm_budget) {
+  if (g.n_tasks < 1 || g.n_tasks > kMaxGroup) return cudaErrorInvalidValue;
+  BoxKind ba, bb;
+  gemm_boxes(a_mn, b_kmajor, g.task[0].m_valid, &ba, &bb, /*grouped=*/true);
+  if (!group_multicast(g, a_mn, b_kmajor, sm_budget))
+    return launch_tile_gemm_group(maps[ba], maps[bb], g, a_mn, b_kmajor, persistent, stream, sm_budget);
+  for (int t = 0; t < g.n_tasks; ++t)
+    if (!args_ok(g.task[t]) || g.task[t].planes != g.task[0].planes || !group_uses_pairs(g.task[t].m_valid))
+      return cudaErrorInvalidValue;
+  // each CTA loads (and multicasts) a 64-row half of its A tile
+  return dispatch(maps[BOX_K64], maps[bb], g, 1, a_mn, b_kmajor, /*pair=*/true, g.task[0].planes, persistent, stream,
+                  sm_budget, /*mc=*/true);
 }
 
 cudaError_t launch_splitk_reduce(const GemmArgs& args, cudaStream_t stream) {

@@ -129,6 +129,14 @@ cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tm
 cudaError_t launch_tile_gemm_group(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, bool a_mn,
                                    bool b_kmajor, bool persistent, cudaStream_t stream, int sm_budget = 0);
 void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* box_b, bool grouped = false);
+// A grouped launch given the slab's tensor maps of every box kind (maps[BoxKind]):
+// picks the boxes, and TMA-multicast clusters of two CTA pairs (256 x 512 units,
+// A loaded once per cluster) when gemm_multicast_enabled() and the group allows.
+cudaError_t launch_tile_gemm_group_maps(const CUtensorMap* maps, GemmGroup& g, bool a_mn, bool b_kmajor,
+                                        bool persistent, cudaStream_t stream, int sm_budget = 0);
+// TMA multicast for grouped launches (default off; TR_GEMM_MC=1 enables).
+bool gemm_multicast_enabled();
+void set_gemm_multicast(bool on);
 // Sums the k_split partials of a split-K launch in z order into C, then applies
 // args.epilogue (STORE / ACCUMULATE) and args.post, exactly like the kernel's own
 // epilogue would have (same argument block).

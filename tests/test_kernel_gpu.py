@@ -80,3 +80,34 @@ def test_dense_kernel_accumulate_and_f64_out(variant):
     torch.cuda.synchronize()
     ref = c0 + ref_product(a, b, False, False)
     assert rel_fro(c, ref) <= 1e-5
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+def test_tma_multicast_clusters_match(precision):
+    """The opt-in TMA-multicast K1 (clusters of two CTA pairs sharing their A
+    tile, tr_set_gemm_multicast) against the float64 oracle and against the
+    default CTA-pair kernel, on a grouped warm product with ragged rows."""
+    import numpy as np
+
+    from paper_1511_04348_b200 import Runtime, homogeneous_machine
+    from paper_1511_04348_b200 import _native as N
+
+    T = 1024
+    g = torch.Generator(device="cuda").manual_seed(9)
+    a = torch.randn(3 * T + 300, 2 * T + 64, device="cuda", generator=g)
+    b = torch.randn(2 * T + 64, 4 * T, device="cuda", generator=g)
+    outs = {}
+    for mc in (0, 1):
+        N.call("tr_set_gemm_multicast", mc)
+        try:
+            c = torch.empty(a.shape[0], b.shape[1], device="cuda")
+            with Runtime(homogeneous_machine(1, dtype=np.float32), T, precision=precision) as rt:
+                for _ in range(2):  # the second product is warm: grouped persistent launches
+                    rt.multiply(a, b, a_uid="A", b_uid="B", out=c)
+            outs[mc] = c.double()
+        finally:
+            N.call("tr_set_gemm_multicast", 0)
+    ref = a.double() @ b.double()
+    tol = 1e-5 if precision == "fp32acc" else 1e-2
+    for mc in (0, 1):
+        assert float(torch.linalg.norm(outs[mc] - ref) / torch.linalg.norm(ref)) <= tol
