@@ -685,7 +685,10 @@ def bench_mlp(args, tr, torch, machine, gpus, precision):
     xh[...] = x
     th[...] = t
     torch.cuda.set_device(gpus[0])
-    mlp = tr.GpuMLP(layers, machine=machine, tile_size=args.tile, device=gpus[0], precision=precision)
+    # tile-parallel over N devices: an 8192 x 8192 product is 4 tasks at T = 4096,
+    # so N > 1 uses 2048-wide tiles (16 tasks per product)
+    tile = args.tile if len(gpus) == 1 else min(args.tile, 2048)
+    mlp = tr.GpuMLP(layers, machine=machine, tile_size=tile, device=gpus[0], precision=precision)
     xs, ts = torch.from_numpy(xh), torch.from_numpy(th)
     losses = train_steps(torch, mlp, xs, ts, 2)  # warm-up: slab sizing, kernel attributes
     for gg in gpus:
@@ -701,7 +704,8 @@ def bench_mlp(args, tr, torch, machine, gpus, precision):
     flops = mlp_flops(sizes, batch)
     return {"workload": f"cfg3 MLP {'-'.join(map(str, sizes))} batch {batch}, sigmoid, MSE, SGD lr 0.1 "
                         f"(device-resident GpuMLP; 12 products per step through the tiled runtime over "
-                        f"{machine.n_devices} device(s), fused bias/activation and activation-gradient epilogues)",
+                        f"{machine.n_devices} device(s), T={tile}, fused bias/activation and activation-gradient "
+                        "epilogues)",
             "precision": precision, "samples_per_s": batch / dt, "ms_per_step": dt * 1e3, "tflops": flops / dt / 1e12,
             "algorithmic_tflop_per_step": flops / 1e12, "steps": args.mlp_steps,
             "loss_first": losses[0], "loss_last": losses[-1],
