@@ -191,6 +191,43 @@ def plan(a, b, a_uid: str = "A", b_uid: str = "B", c_uid: str = "C", *, _pinned_
                 completion=Completion(len(tasks)))
 
 
+def _execute_task(machine: Machine, plan_: Plan, directory: CacheDirectory, dev, task: Task):
+    """One task by hand, outside a Runtime (the reference's internal helper,
+    scheduler.py:371-410): the output tile is admitted and pinned for the task;
+    per k-step A then B are acquired through ``directory``, ``c += a @ b`` runs
+    as one GPU tile product (tiles.accumulate_product) and both inputs are
+    released; then the output is written back and released, the completion
+    bitmap marked (a second execution raises) and the task is DONE.  Returns
+    ``(steps, writeback)`` in simulated time units, [(fetch, compute)] per
+    k-step, from the machine's cost model (devices.py:255-283).  Runtime.multiply
+    does all of this natively; this is for callers that drive the pieces."""
+    from .devices import HOST, compute_cost, transfer_cost
+    from .tiles import accumulate_product
+
+    did, eb = dev.device_id, machine.element_bytes
+    task.state = TaskState.RUNNING
+    i, j = task.row, task.col
+    c_key, c_view = plan_.c.key(i, j), plan_.c.tile_view(i, j)
+    directory.admit_output(did, c_key)
+    steps = []
+    for k in range(task.k_steps):
+        keys = (plan_.a.key(i, k), plan_.b.key(k, j))
+        got = (directory.acquire_input(did, keys[0], plan_.a.tile_nbytes(i, k, eb)),
+               directory.acquire_input(did, keys[1], plan_.b.tile_nbytes(k, j, eb)))
+        fetch = sum(transfer_cost(machine, r.source, did, r.nbytes_moved) for r in got)
+        a_view, b_view = plan_.a.tile_view(i, k), plan_.b.tile_view(k, j)
+        accumulate_product(a_view, b_view, c_view)
+        steps.append((fetch, compute_cost(dev, a_view.shape, b_view.shape)))
+        for key in keys:
+            directory.release_input(did, key)
+    nbytes = int(np.prod(np.shape(c_view))) * eb
+    writeback = transfer_cost(machine, did, HOST, nbytes)
+    directory.release_output(did, c_key, nbytes)
+    plan_.completion.mark(task.task_id)
+    task.state = TaskState.DONE
+    return steps, writeback
+
+
 # ----------------------------------------------------------------- stations
 
 

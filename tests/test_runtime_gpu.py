@@ -551,3 +551,31 @@ def test_standalone_rates_follow_sm_counts():
     # contexts follow the boost clock, which a preceding heavy test can lower
     r = standalone_rates(m, T, a, b, out=c, reps=3)
     assert r[0] == r[2] and 0.3 <= r[1] / r[0] <= 0.75, r
+
+
+def test_execute_task_by_hand_state_machine():
+    """scheduler._execute_task (the reference's internal helper, scheduler.py:371-410)
+    driven by hand with plan / ReservationStation / CacheDirectory: every task
+    QUEUED -> RESERVED -> DONE, the product exact, a second mark refused."""
+    from paper_1511_04348_b200 import CacheDirectory, ReservationStation, TaskState, partition, plan, reassemble
+    from paper_1511_04348_b200.scheduler import _execute_task
+
+    rng = np.random.default_rng(16)
+    a, b = int_matrix(rng, 12, 8), int_matrix(rng, 8, 12)
+    machine = homogeneous_machine(1)
+    p = plan(partition(a, 4), partition(b, 4))
+    directory = CacheDirectory(machine, debug=True)
+    st = ReservationStation(0, 4)
+    steps_total = 0
+    while not p.queue.is_empty():
+        for tid in st.refill(p.queue):
+            p.tasks[tid].state = TaskState.RESERVED
+        while (tid := st.pop_for_run()) is not None:
+            steps, wb = _execute_task(machine, p, directory, machine.device(0), p.tasks[tid])
+            steps_total += len(steps)
+            assert wb > 0
+    assert all(t.state is TaskState.DONE for t in p.tasks) and steps_total == 9 * 2
+    assert np.array_equal(reassemble(p.c.tiled), O.reference_gemm(a, b))
+    assert directory.stats().host_fetches == 3 * 2 + 2 * 3
+    with pytest.raises(RuntimeError):
+        p.completion.mark(0)
