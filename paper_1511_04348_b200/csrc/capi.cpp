@@ -1,5 +1,6 @@
 // extern "C" boundary: include/tilerun_b200.h.  Every entry point catches C++
 // exceptions and turns them into a tr_status plus a thread-local message.
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -384,9 +385,33 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     if (K != Kb) tr::fail(TR_ERR_SHAPE, "inner dimensions differ");
     if (C.rows != M || C.cols != N) tr::fail(TR_ERR_SHAPE, "output shape mismatch");
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) tr::fail(TR_ERR_SHAPE, "dimension too large");
-    if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC) tr::fail(TR_ERR_VALUE, "unknown precision");
-    const int planes = precision == TR_PREC_FP32ACC ? 2 : 1;
+    if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT)
+      tr::fail(TR_ERR_VALUE, "unknown precision");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (precision == TR_PREC_EXACT) {  // KX over float64 copies of A and B (one row stride for both)
+      const int64_t ld = (std::max(A.cols, B.cols) + 7) / 8 * 8;
+      double *xa = nullptr, *xb = nullptr;
+      TR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xa), static_cast<size_t>(A.rows * ld * 8), st));
+      TR_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&xb), static_cast<size_t>(B.rows * ld * 8), st));
+      TR_CUDA(tr::launch_exact_convert(A.ptr, A.dtype == TR_DTYPE_F64, A.ld, A.rows, A.cols, xa, ld, st));
+      TR_CUDA(tr::launch_exact_convert(B.ptr, B.dtype == TR_DTYPE_F64, B.ld, B.rows, B.cols, xb, ld, st));
+      tr::GemmArgs x;
+      std::memset(&x, 0, sizeof(x));
+      x.m_valid = static_cast<int32_t>(M);
+      x.n_valid = static_cast<int32_t>(N);
+      x.n_ksteps = 1;
+      x.k_len[0] = static_cast<int32_t>(K);
+      x.c = const_cast<void*>(C.ptr);
+      x.ldc = C.ld;
+      x.c_f64 = C.dtype == TR_DTYPE_F64;
+      x.epilogue = accumulate ? tr::EPI_ACCUMULATE : tr::EPI_STORE;
+      TR_CUDA(tr::launch_exact_gemm(xa, xb, ld, 0, x, ta != 0, tb != 0,
+                                    A.dtype == TR_DTYPE_F32 && B.dtype == TR_DTYPE_F32, st));
+      TR_CUDA(cudaFreeAsync(xa, st));
+      TR_CUDA(cudaFreeAsync(xb, st));
+      return;
+    }
+    const int planes = precision == TR_PREC_FP32ACC ? 2 : 1;
     auto pack = [&](const tr::Mat& m, uint16_t** buf, tr::PlaneGeom* g) {
       const int64_t ld = (m.cols + 7) / 8 * 8;
       const int64_t pe = m.rows * ld;

@@ -114,7 +114,8 @@ void Job::set_error(int status, const std::string& msg) {
 Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t flags, int64_t hbm_budget)
     : tile_(tile), precision_(precision), flags_(flags), hbm_budget_(hbm_budget) {
   if (tile < 1) fail(TR_ERR_SHAPE, "tile_size must be >= 1, got %d", tile);
-  if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC) fail(TR_ERR_VALUE, "unknown precision %d", precision);
+  if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT)
+    fail(TR_ERR_VALUE, "unknown precision %d", precision);
   if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
   sim_ = flags & TR_FLAG_SIM;
   max_group_ = task_group_max();
@@ -127,7 +128,9 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   coherence_ = flags & TR_FLAG_COHERENCE;
   tracing_ = (flags & TR_FLAG_TRACE) && !(flags & TR_FLAG_DRYRUN);
   element_bytes_ = m.element_bytes > 0 ? m.element_bytes : 8;
-  planes_ = precision == TR_PREC_FP32ACC ? 2 : 1;
+  // bf16: one bf16 plane; fp32acc: hi/lo planes; exact: the tile as float64 (4 planes' worth)
+  exact_ = precision == TR_PREC_EXACT;
+  planes_ = exact_ ? 4 : (precision == TR_PREC_FP32ACC ? 2 : 1);
   ld_ = ceil_div(tile, 8) * 8;
   plane_elems_ = static_cast<int64_t>(tile) * ld_;
   slot_elems_ = planes_ * plane_elems_;
@@ -886,7 +889,7 @@ void set_task_group_max(int n) { g_task_group.store(std::max(1, std::min(kMaxGro
 // capacity unbounded) and would not be split along K.  Host outputs land in the
 // stream's group buffer and are written back on the writeback stream.
 bool Session::groupable(int d, Job& job, int64_t gtid) {
-  if (dryrun_ || !coherence_ || devs_[d].capacity >= 0 || max_group_ < 2) return false;
+  if (dryrun_ || exact_ || !coherence_ || devs_[d].capacity >= 0 || max_group_ < 2) return false;
   if (devs_[d].green && devs_[d].sms < 64) return false;  // a slice of a GPU: single tasks stay stealable
   int64_t tid = 0;
   const Product& p = job.prod_of(gtid, &tid);
@@ -1205,19 +1208,24 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     for (int64_t k = 0; k < kc; ++k) k_total += args.k_len[k];
     // narrow C tile (the MLP's 10-wide output layer): Bᵀ·Aᵀ on the tensor cores
     GemmArgs targs;
-    const bool narrow = !dryrun_ && narrow_tc_enabled() && T > kSmallMaxN && args.n_valid <= kSmallMaxN &&
+    // (the exact mode has one kernel: KX, k ascending, never split)
+    const bool narrow = !dryrun_ && !exact_ && narrow_tc_enabled() && T > kSmallMaxN && args.n_valid <= kSmallMaxN &&
                         k_total > kSmallMaxK && plan_narrow(d, *scp, args, targs);
-    const bool small = !dryrun_ && !narrow && small_gemm_enabled() && small_gemm_eligible(args);
-    if (!dryrun_ && !narrow) {
+    const bool small = !dryrun_ && !exact_ && !narrow && small_gemm_enabled() && small_gemm_eligible(args);
+    if (!dryrun_ && !exact_ && !narrow) {
       if (small) plan_split_small(d, *scp, args);
       else plan_split_k(d, *scp, args);
     }
-    const int32_t wt = (!dryrun_ && !narrow && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args) : -1;
+    const int32_t wt = (!dryrun_ && !exact_ && !narrow && k0 == 0 && kc == ks) ? write_through(d, s, p, i, j, args)
+                                                                               : -1;
     const bool reduce = narrow || args.k_split > 1;
     // column sums of the final output: fused into K1's epilogue when it stores the tile, else a pass over it
     const bool cs_pass = !dryrun_ && p.colsum && k0 + kc == ks && (narrow || !fuse_colsum(p, i, j, args, small));
     auto launch = [&] {
-      if (narrow) {  // A' = Bᵀ, B' = Aᵀ: the layouts swap roles
+      if (exact_) {
+        TR_CUDA(launch_exact_gemm(dc.slab, dc.slab, ld_, plane_elems_, args, p.ta, p.tb,
+                                  p.a.dtype == TR_DTYPE_F32 && p.b.dtype == TR_DTYPE_F32, scp->stream));
+      } else if (narrow) {  // A' = Bᵀ, B' = Aᵀ: the layouts swap roles
         BoxKind ba, bb;
         gemm_boxes(!p.tb, !p.ta, targs.m_valid, &ba, &bb);
         TR_CUDA(launch_tile_gemm(dc.tmap[ba], dc.tmap[bb], targs, !p.tb, !p.ta, scp->stream));
@@ -1613,6 +1621,8 @@ void Session::run_products(std::vector<Product> prods, int64_t task_offset, int6
     if (p.post != POST_NONE && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))
       fail(TR_ERR_VALUE, "fused epilogues need a float32 device output");
     if (p.post == POST_ACT_GRAD && !p.aux) fail(TR_ERR_VALUE, "POST_ACT_GRAD needs the activation (aux) matrix");
+    if (exact_ && (p.post != POST_NONE || p.axpy || p.colsum || p.cache_as))
+      fail(TR_ERR_VALUE, "precision 'exact' runs plain products only (no fused epilogue, axpy or write-through)");
     if (p.colsum && (c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32 || T % 32 != 0))
       fail(TR_ERR_VALUE, "fused column sums need a float32 device output and a tile size that is a multiple of 32");
     if (p.axpy && (p.post != POST_NONE || c.location != TR_LOC_DEVICE || c.dtype != TR_DTYPE_F32))

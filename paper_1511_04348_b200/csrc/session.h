@@ -275,6 +275,7 @@ class Session {
 
   int32_t tile_;
   int32_t precision_;
+  bool exact_ = false;  // TR_PREC_EXACT: float64 tiles, the KX kernel only
   int planes_;
   int64_t ld_, plane_elems_, slot_elems_;
   uint32_t flags_;

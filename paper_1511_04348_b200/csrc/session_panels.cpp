@@ -34,7 +34,8 @@ int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // counters keep the reference's values.  Fills are issued up front in arrival
 // order (uncounted, like fetch-ahead); each unit's launch waits for its tiles.
 bool Session::panels_apply(const Job& job) const {
-  if (dryrun_ || sim_ || !coherence_ || n_devices() != 1 || devs_[0].capacity >= 0 || job.prods.size() != 1) return false;
+  if (dryrun_ || sim_ || exact_ || !coherence_ || n_devices() != 1 || devs_[0].capacity >= 0 || job.prods.size() != 1)
+    return false;
   if (!(order_ == -1 || order_ == 4) || (flags_ & TR_FLAG_NO_PREFETCH)) return false;
   const Product& p = job.prods[0];
   if (p.a.location != TR_LOC_HOST || p.b.location != TR_LOC_HOST || p.c.location != TR_LOC_HOST) return false;

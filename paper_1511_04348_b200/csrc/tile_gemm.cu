@@ -924,6 +924,7 @@ void set_group_pairs(bool on) { g_group_pairs.store(on ? 1 : 0); }
 cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols,
                                  uint16_t* dst, int64_t ld_dst, int64_t rows_cap, int64_t plane_stride,
                                  int planes, cudaStream_t stream) {
+  if (planes == 4) return launch_exact_convert(src, src_f64, ld_src, rows, cols, dst, ld_dst, stream);  // exact mode
   if (ld_dst % 8 != 0 || plane_stride % 8 != 0) return cudaErrorInvalidValue;
   // The kernel's TMA boxes never read past the valid extent rounded up to 256
   // (rows or columns), so only that part of the slot is written (zero padded);

@@ -193,6 +193,19 @@ cudaError_t launch_small_gemm(const uint16_t* slab, int64_t ld, int64_t plane_st
 bool small_gemm_enabled();
 void set_small_gemm(bool on);
 
+// KX: precision "exact" (exact_gemm.cu) -- the reference's arithmetic bit for
+// bit: per output element a rounded multiply then a rounded add (float32 when
+// both operands and C are float32, else float64 with C's dtype rounding), k ascending, from 0 (EPI_STORE) or from C's current value
+// (EPI_ACCUMULATE).  Tiles are float64, row-major with `ld` doubles per row; k-step
+// ks of A starts at a_base + (a_z[ks] / 4) * slot_doubles (likewise B).  No
+// post-op, scaling, split-K, write-through or column sums.
+cudaError_t launch_exact_gemm(const void* a_base, const void* b_base, int64_t ld, int64_t slot_doubles,
+                              const GemmArgs& args, bool a_mn, bool b_kmajor, bool f32_operands,
+                              cudaStream_t stream);
+// Tile admission for the exact mode: the rows x cols region as float64 (ld_dst per row).
+cudaError_t launch_exact_convert(const void* src, int src_f64, int64_t ld_src, int64_t rows, int64_t cols, void* dst,
+                                 int64_t ld_dst, cudaStream_t stream);
+
 // K2: tile admission.  Converts a row-major fp32/f64 region (rows x cols, ld_src)
 // into `planes` bf16 planes of a rows_cap x ld_dst slot, zero-filling everything
 // outside the valid region so ragged tiles contribute nothing in K.

@@ -10,10 +10,35 @@ from __future__ import annotations
 from . import _native as N
 from .matrix import describe, is_device_tensor
 
-PRECISIONS = {"bf16": N.TR_PREC_BF16, "fp32acc": N.TR_PREC_FP32ACC}
+# "exact": the reference's own arithmetic (rounded multiply then rounded add per
+# rank-1 update, k ascending, output dtype) on CUDA cores -- bit for bit its results
+PRECISIONS = {"bf16": N.TR_PREC_BF16, "fp32acc": N.TR_PREC_FP32ACC, "exact": N.TR_PREC_EXACT}
+
+_default_precision = None
+
+
+def default_precision() -> str:
+    """The precision used where a call does not name one: set_default_precision(),
+    else the TR_PRECISION environment variable, else "fp32acc"."""
+    import os
+
+    p = _default_precision or os.environ.get("TR_PRECISION") or "fp32acc"
+    if p not in PRECISIONS:
+        raise ValueError(f"unknown precision {p!r} (TR_PRECISION); expected one of {sorted(PRECISIONS)}")
+    return p
+
+
+def set_default_precision(p: str | None) -> None:
+    """Process-wide default precision ("fp32acc", "bf16" or "exact"; None: back to the default)."""
+    global _default_precision
+    if p is not None and p not in PRECISIONS:
+        raise ValueError(f"unknown precision {p!r}; expected one of {sorted(PRECISIONS)}")
+    _default_precision = p
 
 
 def precision_code(p) -> int:
+    if p is None:
+        p = default_precision()
     if isinstance(p, int):
         return p
     try:
@@ -47,7 +72,7 @@ def set_narrow_tc(on: bool) -> None:
     N.call("tr_set_narrow_tc", int(bool(on)))
 
 
-def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision="fp32acc", accumulate=False,
+def dense_gemm(a, b, transpose_a=False, transpose_b=False, out=None, precision=None, accumulate=False,
                stream=None):
     """``out (+)= op(a) @ op(b)`` for torch CUDA tensors (float32/float64).
 

@@ -79,6 +79,9 @@ class GpuMLP:
                  fused_colsum: bool = True):
         import torch
 
+        if precision == "exact" or (runtime is not None and runtime.precision == "exact"):
+            raise ValueError("GpuMLP fuses bias/activation/SGD into the tile GEMMs; precision 'exact' "
+                             "covers plain products only (use 'fp32acc')")
         self.torch = torch
         self.dev = torch.device("cuda", device)
         self.layers: list[DeviceLayer] = []

@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as N
 from .coherence import CacheDirectory, CacheStats, UidTable
-from .dense import precision_code
+from .dense import default_precision, precision_code
 from .devices import Machine
 from .errors import NoDeviceError
 from .matrix import ShapeOnly, describe, is_device_tensor, pinned_empty, pinned_zeros
@@ -416,12 +416,13 @@ class Runtime:
     """A session: one machine, one HBM tile cache, any number of products.
 
     Signature follows scheduler.py:531-533, plus ``precision`` ("fp32acc" |
-    "bf16") and ``hbm_budget_bytes`` (per GPU; 0 = 80% of free HBM).
+    "bf16" | "exact"; None = ``dense.default_precision()``) and
+    ``hbm_budget_bytes`` (per GPU; 0 = 80% of free HBM).
     """
 
     def __init__(self, machine: Machine, tile_size: int, mode: str = "gpu", steal: bool = True,
                  coherence: bool = True, seed: int | None = None, directory_debug: bool = False,
-                 precision: str = "fp32acc", hbm_budget_bytes: int = 0, policy: str = "lru",
+                 precision: str | None = None, hbm_budget_bytes: int = 0, policy: str = "lru",
                  fetch_ahead: bool = True, trace: bool = False, compute: bool = True):
         if mode not in MODES:
             raise ValueError(f"unknown mode {mode!r}")
@@ -433,6 +434,7 @@ class Runtime:
         self.steal = steal
         self.coherence = coherence
         self.seed = seed
+        precision = precision or default_precision()
         self.precision = precision
         flags = (N.TR_FLAG_STEAL if steal else 0) | (N.TR_FLAG_COHERENCE if coherence else 0)
         flags |= N.TR_FLAG_DEBUG if directory_debug else 0
@@ -719,7 +721,7 @@ class Runtime:
 
 
 def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool = True, coherence: bool = True,
-        seed: int | None = None, directory_debug: bool = False, precision: str = "fp32acc", compute: bool = True):
+        seed: int | None = None, directory_debug: bool = False, precision: str | None = None, compute: bool = True):
     """One-shot product through a fresh session with uids "A","B","C" (scheduler.py:615-621)."""
     rt = Runtime(machine, tile_size, mode=mode, steal=steal, coherence=coherence, seed=seed,
                  directory_debug=directory_debug, precision=precision, compute=compute)
@@ -729,7 +731,7 @@ def run(machine: Machine, a, b, tile_size: int, mode: str = "gpu", steal: bool =
         rt.close()
 
 
-def standalone_rates(machine: Machine, tile_size: int, a, b, *, out=None, precision: str = "fp32acc",
+def standalone_rates(machine: Machine, tile_size: int, a, b, *, out=None, precision: str | None = None,
                      reps: int = 2) -> list[float]:
     """Throughput (flop/s) of every logical device of ``machine`` running the
     product ``a @ b`` ALONE: a one-device machine with the device's GPU, green-

@@ -313,3 +313,22 @@ def test_directory_lock_stats_dryrun():
         assert st["acquisitions"] >= 2 * 4 * 5 * 3  # >= one per input request (20 tasks x 3 k-steps x A, B)
         assert st["held_s"] >= 0 and st["waited_s"] >= 0 and st["max_hold_us"] >= 0
         assert rt.lock_stats()["acquisitions"] < st["acquisitions"]
+
+
+def test_default_precision_resolution(monkeypatch):
+    from paper_1511_04348_b200 import dense
+
+    monkeypatch.delenv("TR_PRECISION", raising=False)
+    assert dense.default_precision() == "fp32acc"
+    monkeypatch.setenv("TR_PRECISION", "exact")
+    assert dense.default_precision() == "exact" and dense.precision_code(None) == dense.PRECISIONS["exact"]
+    dense.set_default_precision("bf16")
+    try:
+        assert dense.default_precision() == "bf16"
+    finally:
+        dense.set_default_precision(None)
+    monkeypatch.setenv("TR_PRECISION", "fp16")
+    with pytest.raises(ValueError):
+        dense.default_precision()
+    with pytest.raises(ValueError):
+        dense.set_default_precision("tf32")
