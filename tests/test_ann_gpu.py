@@ -31,7 +31,7 @@ def relerr(x, ref):
 @pytest.mark.parametrize("act", ["sigmoid", "relu"])
 @pytest.mark.parametrize("backend_kind", ["tiled", "dense"])
 def test_gradients_and_trajectory(g, act, backend_kind):
-    backend = TiledBackend(homogeneous_machine(2), tile_size=16) if backend_kind == "tiled" else DenseBackend()
+    backend = TiledBackend(homogeneous_machine(2), tile_size=16, mode="gpu") if backend_kind == "tiled" else DenseBackend()
     net = net_from(g, act)
     loss, grads = loss_gradients(net, g[f"{act}_x"], g[f"{act}_t"], backend)
     assert abs(loss - g[f"{act}_loss0"][0]) <= 1e-5 * abs(g[f"{act}_loss0"][0])
@@ -49,7 +49,7 @@ def test_xor_trajectory_tiled_t2(g):
     net = Network.from_sizes([2, 8, 1], rng, activation="sigmoid")
     assert np.array_equal(net.layers[0].weights, g["xor_w0"])
     x, t = xor_dataset()
-    backend = TiledBackend(homogeneous_machine(2), tile_size=2)
+    backend = TiledBackend(homogeneous_machine(2), tile_size=2, mode="gpu")
     losses = np.array([train_step(net, x, t, 0.5, backend) for _ in range(50)])
     assert np.max(np.abs(losses - g["xor_losses"]) / g["xor_losses"]) <= 1e-5
 
@@ -58,7 +58,25 @@ def test_backward_reuses_forward_tiles():
     rng = np.random.default_rng(5)
     net = Network.from_sizes([8, 8, 4], rng)
     x, t = rng.uniform(-1, 1, (8, 8)), rng.uniform(-1, 1, (8, 4))
-    backend = TiledBackend(homogeneous_machine(1), tile_size=4)
+    backend = TiledBackend(homogeneous_machine(1), tile_size=4, mode="gpu")
     train_step(net, x, t, 0.1, backend)
     assert backend.runtime.directory.stats().l1_hits > 0
     assert len(backend.call_stats) == 3 * 2
+
+
+def test_default_sim_backend_times_improve_with_devices():
+    """TiledBackend in the reference's default mode "sim" (ann.py:85): products from
+    the GPU kernel, bench_pass in simulated time, which falls with more devices
+    (test_ann.py:200-208)."""
+    from paper_1511_04348_b200.ann import bench_pass, random_regression
+
+    rng = np.random.default_rng(6)
+    net = Network.from_sizes([48, 48, 48], rng)
+    x, t = random_regression(rng, 48, 48, 48)
+    times = {}
+    for n in (1, 4):
+        backend = TiledBackend(homogeneous_machine(n), tile_size=8, mode="sim")
+        times[n] = bench_pass(net, x, t, backend, repeats=3)
+        loss, _ = loss_gradients(net, x, t, backend)
+        assert np.isfinite(loss)
+    assert 0 < times[4] < times[1]

@@ -228,6 +228,7 @@ def test_ann_backends_agree(tmp_path):
 @pytest.mark.gpu
 def test_sweep_gpu(tmp_path):
     out = tmp_path / "sweep.csv"
-    assert run_cli("sweep", "--sizes", "256", "--device-counts", "1,2", "--tile-size", 64, "--out", out) == 0
+    assert run_cli("sweep", "--sizes", "256", "--device-counts", "1,2", "--tile-size", 64, "--mode", "gpu",
+                   "--out", out) == 0
     rows = list(csv.DictReader(out.read_text().splitlines()))
     assert len(rows) == 2 and all(float(r["makespan"]) > 0 for r in rows)

@@ -68,7 +68,7 @@ def test_sim_rejects_batches_and_needs_positive_rates():
 
 @pytest.mark.parametrize("name", ["plain", "bypass", "template"])
 def test_cli_sweep_sim_is_byte_identical(tmp_path, name):
-    """`sweep --mode sim` reproduces the reference CLI's table byte for byte."""
+    """`sweep` (default --mode sim, like the reference's) reproduces the reference CLI's table byte for byte."""
     from paper_1511_04348_b200 import cli, save_machine
 
     extra = []
@@ -80,5 +80,24 @@ def test_cli_sweep_sim_is_byte_identical(tmp_path, name):
         extra = ["--devices", str(dev)]
     out = tmp_path / "sweep.csv"
     assert cli.main(["sweep", "--sizes", "8,16,20", "--device-counts", "2,3", "--tile-size", "4", "--seed", "3",
-                     "--mode", "sim", "--out", str(out), *extra]) == 0
+                     "--out", str(out), *extra]) == 0
     assert out.read_text() == G["sweeps"][name]
+
+
+def test_cli_sweep_speedup_curve_shape(tmp_path):
+    """The reference's acceptance criterion 4 (test_acceptance.py:145-168): on the
+    simulated sweep the 4-device speedup rises to its peak and stays within 5 %."""
+    import csv
+
+    from paper_1511_04348_b200 import cli
+
+    dev = tmp_path / "template.json"
+    dev.write_text('{"devices": [{"id": 0, "flops_per_unit": 1000.0, "host_bandwidth": 256.0}]}')
+    out = tmp_path / "sweep.csv"
+    assert cli.main(["sweep", "--sizes", "32,64,128,256,320", "--device-counts", "1,4", "--tile-size", "16",
+                     "--devices", str(dev), "--out", str(out)]) == 0
+    sp = [float(r["speedup"]) for r in csv.DictReader(out.read_text().splitlines()) if r["devices"] == "4"]
+    assert len(sp) == 5
+    peak = int(np.argmax(sp))
+    assert all(sp[i] <= sp[i + 1] + 1e-12 for i in range(peak))
+    assert all(s >= 0.95 * sp[peak] for s in sp[peak:])
