@@ -51,8 +51,11 @@ typedef enum { TR_LOC_HOST = 0, TR_LOC_DEVICE = 1 } tr_location;
  * hi*hi tcgen05 MMAs into an fp32 TMEM accumulator.  BF16: one plane, one MMA. */
 /* TR_PREC_EXACT: the reference's own arithmetic (a rounded multiply then a
  * rounded add per rank-1 update, k ascending, in the output dtype) on CUDA
- * cores: results bit for bit the reference's; tiles cached as float64. */
-typedef enum { TR_PREC_BF16 = 0, TR_PREC_FP32ACC = 1, TR_PREC_EXACT = 2 } tr_precision;
+ * cores: results bit for bit the reference's; tiles cached as float64.
+ * TR_PREC_FP32HI: three bf16 planes (hi, mid, lo: all 24 bits of an fp32
+ * value) and the six MMAs of weight >= 2^-16 per k-block -- about 10x more
+ * accurate than FP32ACC at twice its tensor work. */
+typedef enum { TR_PREC_BF16 = 0, TR_PREC_FP32ACC = 1, TR_PREC_EXACT = 2, TR_PREC_FP32HI = 3 } tr_precision;
 
 typedef enum { TR_POLICY_LRU = 0, TR_POLICY_FIFO = 1 } tr_policy; /* coherence.py:95-99 */
 typedef enum { TR_HIT_L1 = 0, TR_HIT_L2 = 1, TR_HIT_MISS = 2 } tr_hit_level; /* coherence.py:37-40 */

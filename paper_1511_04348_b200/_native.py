@@ -20,7 +20,7 @@ TR_OK, TR_ERR_CONFIG, TR_ERR_SHAPE, TR_ERR_CAPACITY, TR_ERR_RUNTIME, TR_ERR_CUDA
     TR_ERR_INTERNAL, TR_ERR_NODEVICE = range(9)
 TR_DTYPE_F32, TR_DTYPE_F64 = 0, 1
 TR_LOC_HOST, TR_LOC_DEVICE = 0, 1
-TR_PREC_BF16, TR_PREC_FP32ACC, TR_PREC_EXACT = 0, 1, 2
+TR_PREC_BF16, TR_PREC_FP32ACC, TR_PREC_EXACT, TR_PREC_FP32HI = 0, 1, 2, 3
 TR_POLICY_LRU, TR_POLICY_FIFO = 0, 1
 TR_HIT_L1, TR_HIT_L2, TR_HIT_MISS = 0, 1, 2
 TR_SOURCE_HOST = -1

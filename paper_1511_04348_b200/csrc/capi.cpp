@@ -385,7 +385,8 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     if (K != Kb) tr::fail(TR_ERR_SHAPE, "inner dimensions differ");
     if (C.rows != M || C.cols != N) tr::fail(TR_ERR_SHAPE, "output shape mismatch");
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) tr::fail(TR_ERR_SHAPE, "dimension too large");
-    if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT)
+    if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT &&
+      precision != TR_PREC_FP32HI)
       tr::fail(TR_ERR_VALUE, "unknown precision");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (precision == TR_PREC_EXACT) {  // KX over float64 copies of A and B (one row stride for both)
@@ -411,7 +412,7 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
       TR_CUDA(cudaFreeAsync(xb, st));
       return;
     }
-    const int planes = precision == TR_PREC_FP32ACC ? 2 : 1;
+    const int planes = precision == TR_PREC_FP32HI ? 3 : precision == TR_PREC_FP32ACC ? 2 : 1;
     auto pack = [&](const tr::Mat& m, uint16_t** buf, tr::PlaneGeom* g) {
       const int64_t ld = (m.cols + 7) / 8 * 8;
       const int64_t pe = m.rows * ld;
@@ -447,7 +448,7 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     args.ldc = C.ld;
     args.c_f64 = C.dtype == TR_DTYPE_F64;
     args.epilogue = accumulate ? tr::EPI_ACCUMULATE : tr::EPI_STORE;
-    args.seg_kb = planes == 2 ? tr::kSegKbFp32Acc : 0;
+    args.seg_kb = tr::seg_kb_for(planes);
     TR_CUDA(tr::launch_tile_gemm(tma, tmb, args, ta != 0, tb != 0, st));
     TR_CUDA(cudaFreeAsync(pa, st));
     TR_CUDA(cudaFreeAsync(pb, st));

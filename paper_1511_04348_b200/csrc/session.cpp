@@ -114,7 +114,8 @@ void Job::set_error(int status, const std::string& msg) {
 Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t flags, int64_t hbm_budget)
     : tile_(tile), precision_(precision), flags_(flags), hbm_budget_(hbm_budget) {
   if (tile < 1) fail(TR_ERR_SHAPE, "tile_size must be >= 1, got %d", tile);
-  if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT)
+  if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT &&
+      precision != TR_PREC_FP32HI)
     fail(TR_ERR_VALUE, "unknown precision %d", precision);
   if (m.n_devices < 1 || m.n_devices > 64) fail(TR_ERR_CONFIG, "machine needs 1..64 devices, got %d", m.n_devices);
   sim_ = flags & TR_FLAG_SIM;
@@ -130,7 +131,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
   element_bytes_ = m.element_bytes > 0 ? m.element_bytes : 8;
   // bf16: one bf16 plane; fp32acc: hi/lo planes; exact: the tile as float64 (4 planes' worth)
   exact_ = precision == TR_PREC_EXACT;
-  planes_ = exact_ ? 4 : (precision == TR_PREC_FP32ACC ? 2 : 1);
+  planes_ = exact_ ? 4 : precision == TR_PREC_FP32HI ? 3 : precision == TR_PREC_FP32ACC ? 2 : 1;
   ld_ = ceil_div(tile, 8) * 8;
   plane_elems_ = static_cast<int64_t>(tile) * ld_;
   slot_elems_ = planes_ * plane_elems_;
@@ -853,7 +854,7 @@ int Session::group_split(int d, const GemmGroup& grp, bool pair) const {
   // time of one unit's full k-loop (µs; ~1.35 µs per split-bf16x3 k-block under
   // the power cap, a third of that in bf16) and the partials' HBM round trip
   // at ~5 TB/s (µs per byte)
-  const double unit_us = kb * (grp.task[0].planes == 2 ? 1.35 : 0.45);
+  const double unit_us = kb * 0.45 * (grp.task[0].planes == 3 ? 6 : grp.task[0].planes == 2 ? 3 : 1);
   const double us_per_byte = 1.0 / 5e6;
   const bool with_reduce = !(getenv("TR_SPLIT_REDUCE_COST") && getenv("TR_SPLIT_REDUCE_COST")[0] == '0');
   const double base = static_cast<double>(ceil_div(tiles, slots)) * unit_us;
@@ -942,7 +943,7 @@ void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, in
     args.epilogue = p.axpy ? EPI_ACCUMULATE : EPI_STORE;
     args.scaled = p.axpy;
     args.alpha = p.alpha;
-    args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+    args.seg_kb = seg_kb_for(planes_);
     args.k_split = 1;
     if (p.post != POST_NONE) {
       args.post = p.post;
@@ -1180,7 +1181,7 @@ void Session::issue(int d, Job& job, int64_t gtid, int s) {
     args.epilogue = (k0 == 0 && !p.axpy) ? EPI_STORE : EPI_ACCUMULATE;
     args.scaled = p.axpy;
     args.alpha = p.alpha;
-    args.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+    args.seg_kb = seg_kb_for(planes_);
     if (p.post != POST_NONE && k0 + kc == ks) {  // fused post-op on the final chunk only
       args.post = p.post;
       args.act = p.act;

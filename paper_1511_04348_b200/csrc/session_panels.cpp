@@ -189,7 +189,7 @@ bool Session::run_panels(Job& job) {
         a.ldc = nt;
         a.c_f64 = p.c.dtype == TR_DTYPE_F64;
         a.epilogue = u.k0 == 0 ? EPI_STORE : EPI_ACCUMULATE;
-        a.seg_kb = planes_ == 2 ? kSegKbFp32Acc : 0;
+        a.seg_kb = seg_kb_for(planes_);
         a.k_split = 1;
         for (int64_t k = u.k0; k < u.k1; ++k) {
           const auto ak = a_key(i, k), bk = b_key(k, j);

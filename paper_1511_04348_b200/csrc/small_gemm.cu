@@ -351,7 +351,8 @@ bool small_gemm_enabled() {
 void set_small_gemm(bool on) { g_small.store(on ? 1 : 0); }
 
 bool small_gemm_eligible(const GemmArgs& args) {
-  return args.n_valid <= kSmallMaxN || total_k(args) <= kSmallMaxK;
+  // hi + lo planes only: fp32hi's third plane stays on the tensor cores
+  return args.planes <= 2 && (args.n_valid <= kSmallMaxN || total_k(args) <= kSmallMaxK);
 }
 
 int small_gemm_split(const GemmArgs& args, int sms) {

@@ -47,7 +47,9 @@ constexpr int SMEM_BUDGET = 227 * 1024;
 //         each CTA's TMEM holds its 128 x 256 accumulator.  Per SM this halves
 //         the B bytes fetched and the smem bytes the tensor core reads.
 // hi = bf16(v), lo = bf16(v - hi) for 4 consecutive values (the K2 split of a
-// float32 input, bit for bit), stored as 8-byte vectors into 1 or 2 planes.
+// float32 input, bit for bit), stored as 8-byte vectors into 1 or 2 planes; 3
+// planes (fp32hi): hi, mid = bf16(v - hi), lo = bf16(v - hi - mid) -- every
+// difference is exact in float32, so the three planes carry all 24 bits.
 __device__ __forceinline__ void split4(uint16_t* dst, int64_t plane, int planes, float4 v) {
   // packed conversions (one cvt.rn.bf16x2.f32 per pair): the epilogue's store
   // phase is instruction-bound when it also writes the planes
@@ -57,17 +59,44 @@ __device__ __forceinline__ void split4(uint16_t* dst, int64_t plane, int planes,
   hi.x = *reinterpret_cast<const uint32_t*>(&h01);
   hi.y = *reinterpret_cast<const uint32_t*>(&h23);
   *reinterpret_cast<uint2*>(dst) = hi;
-  if (planes == 2) {
+  if (planes >= 2) {
     const float2 f01 = __bfloat1622float2(h01);
     const float2 f23 = __bfloat1622float2(h23);
-    const __nv_bfloat162 l01 = __floats2bfloat162_rn(v.x - f01.x, v.y - f01.y);
-    const __nv_bfloat162 l23 = __floats2bfloat162_rn(v.z - f23.x, v.w - f23.y);
+    const float2 r01 = make_float2(v.x - f01.x, v.y - f01.y);
+    const float2 r23 = make_float2(v.z - f23.x, v.w - f23.y);
+    const __nv_bfloat162 l01 = __floats2bfloat162_rn(r01.x, r01.y);
+    const __nv_bfloat162 l23 = __floats2bfloat162_rn(r23.x, r23.y);
     uint2 lo;
     lo.x = *reinterpret_cast<const uint32_t*>(&l01);
     lo.y = *reinterpret_cast<const uint32_t*>(&l23);
     *reinterpret_cast<uint2*>(dst + plane) = lo;
+    if (planes == 3) {
+      const float2 m01 = __bfloat1622float2(l01);
+      const float2 m23 = __bfloat1622float2(l23);
+      const __nv_bfloat162 t01 = __floats2bfloat162_rn(r01.x - m01.x, r01.y - m01.y);
+      const __nv_bfloat162 t23 = __floats2bfloat162_rn(r23.x - m23.x, r23.y - m23.y);
+      uint2 t;
+      t.x = *reinterpret_cast<const uint32_t*>(&t01);
+      t.y = *reinterpret_cast<const uint32_t*>(&t23);
+      *reinterpret_cast<uint2*>(dst + 2 * plane) = t;
+    }
   }
 }
+
+// The MMA passes of one k-block: plane pairs (a, b), smallest terms first and
+// hi*hi last.  fp32acc (2 planes): the products of (hi+lo)(hi+lo) but lo*lo;
+// fp32hi (3 planes): the six products of (hi+mid+lo)(hi+mid+lo) of weight >= 2^-16.
+__host__ __device__ constexpr int n_passes(int planes) { return planes == 1 ? 1 : (planes == 2 ? 3 : 6); }
+__host__ __device__ constexpr int pass_a(int planes, int pass) {
+  return planes == 2 ? (pass == 1 ? 1 : 0) : planes == 3 ? (pass == 1 ? 2 : pass == 2 || pass == 4 ? 1 : 0) : 0;
+}
+__host__ __device__ constexpr int pass_b(int planes, int pass) {
+  return planes == 2 ? (pass == 0 ? 1 : 0) : planes == 3 ? (pass == 0 ? 2 : pass == 2 || pass == 3 ? 1 : 0) : 0;
+}
+static_assert(pass_a(3, 0) == 0 && pass_b(3, 0) == 2 && pass_a(3, 1) == 2 && pass_b(3, 1) == 0 &&
+                  pass_a(3, 2) == 1 && pass_b(3, 2) == 1 && pass_a(3, 3) == 0 && pass_b(3, 3) == 1 &&
+                  pass_a(3, 4) == 1 && pass_b(3, 4) == 0 && pass_a(3, 5) == 0 && pass_b(3, 5) == 0,
+              "fp32hi pass table");
 
 template <int PLANES, int CG>
 struct Cfg {
@@ -79,6 +108,7 @@ struct Cfg {
   static constexpr int EPI_STAGE_BYTES = EPI_WARPS * STAGE_ROWS * STAGE_LD * 4;
   static constexpr int STAGES = std::min(6, (SMEM_BUDGET - 2048 - EPI_STAGE_BYTES) / STAGE_BYTES);
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_STAGE_BYTES;
+  static_assert(STAGES >= 1, "operand stage does not fit in shared memory");
 };
 
 // Output unit u of a group launch -> (task, row/column origin, split-K share).
@@ -300,11 +330,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             const bool seg_done = kb_in_seg + 1 == seg_kb;
             if (ptx::elect_one()) {
               uint32_t acc = accumulate;
-              // PLANES == 2: small cross terms first, then hi*hi.
+              // small cross terms first, then hi*hi (n_passes / pass_a / pass_b)
 #pragma unroll
-              for (int pass = 0; pass < (PLANES == 2 ? 3 : 1); ++pass) {
-                const int pa = (PLANES == 2) ? (pass == 1 ? 1 : 0) : 0;
-                const int pb = (PLANES == 2) ? (pass == 0 ? 1 : 0) : 0;
+              for (int pass = 0; pass < n_passes(PLANES); ++pass) {
+                const int pa = pass_a(PLANES, pass);
+                const int pb = pass_b(PLANES, pass);
                 // k16 advances the start address field (bits [0,14), 16-byte units)
                 const uint64_t a0 = A_MN ? ptx::sdesc_sw128(a_base + pa * A_BYTES, MN_GROUP_BYTES, 1024)
                                          : ptx::sdesc_sw128(a_base + pa * A_BYTES, 16, 1024);
@@ -603,19 +633,23 @@ __global__ void split_convert_kernel(const T* __restrict__ src, int64_t ld_src, 
        idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = idx / chunks_per_row;
     const int64_t c = (idx - r * chunks_per_row) * 8;
-    uint16_t hi[8], lo[8];
+    uint16_t hi[8], lo[8], lo2[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int64_t cc = c + j;
       const double v = (r < rows && cc < cols) ? static_cast<double>(src[r * ld_src + cc]) : 0.0;
       const __nv_bfloat16 h = __float2bfloat16_rn(static_cast<float>(v));
-      const __nv_bfloat16 l = __float2bfloat16_rn(static_cast<float>(v - static_cast<double>(__bfloat162float(h))));
+      const double rest = v - static_cast<double>(__bfloat162float(h));
+      const __nv_bfloat16 l = __float2bfloat16_rn(static_cast<float>(rest));
+      const __nv_bfloat16 l2 = __float2bfloat16_rn(static_cast<float>(rest - static_cast<double>(__bfloat162float(l))));
       hi[j] = __bfloat16_as_ushort(h);
       lo[j] = __bfloat16_as_ushort(l);
+      lo2[j] = __bfloat16_as_ushort(l2);
     }
     uint16_t* d = dst + r * ld_dst + c;
     *reinterpret_cast<uint4*>(d) = *reinterpret_cast<const uint4*>(hi);
-    if (planes == 2) *reinterpret_cast<uint4*>(d + plane_stride) = *reinterpret_cast<const uint4*>(lo);
+    if (planes >= 2) *reinterpret_cast<uint4*>(d + plane_stride) = *reinterpret_cast<const uint4*>(lo);
+    if (planes == 3) *reinterpret_cast<uint4*>(d + 2 * plane_stride) = *reinterpret_cast<const uint4*>(lo2);
   }
 }
 
@@ -718,30 +752,33 @@ void gemm_boxes(bool a_mn, bool b_kmajor, int m_valid, BoxKind* box_a, BoxKind* 
   *box_b = b_kmajor ? (pair ? BOX_K128 : BOX_K256) : BOX_MN64;
 }
 
+template <int P>
+static cudaError_t dispatch_planes(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
+                                   bool a_mn, bool b_kmajor, bool pair, bool persistent, cudaStream_t stream,
+                                   int sm_budget) {
+  switch ((a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (pair ? 1 : 0)) {
+    case 0: return launch_variant<false, false, P, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 1: return launch_variant<false, false, P, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 2: return launch_variant<false, true, P, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 3: return launch_variant<false, true, P, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 4: return launch_variant<true, false, P, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 5: return launch_variant<true, false, P, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    case 6: return launch_variant<true, true, P, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+    default: return launch_variant<true, true, P, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+  }
+}
+
 static cudaError_t dispatch(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split, bool a_mn,
                             bool b_kmajor, bool pair, int planes, bool persistent, cudaStream_t stream,
                             int sm_budget = 0, bool mc = false) {
-  if (mc && pair && !a_mn && !b_kmajor)  // TMA-multicast clusters of two CTA pairs (opt-in; see gemm_multicast)
+  if (mc && pair && !a_mn && !b_kmajor && planes <= 2)  // TMA-multicast clusters of two CTA pairs (opt-in)
     return planes == 2 ? launch_variant<false, false, 2, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream)
                        : launch_variant<false, false, 1, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-  const int variant = (a_mn ? 4 : 0) | (b_kmajor ? 2 : 0) | (planes == 2 ? 1 : 0) | (pair ? 8 : 0);
-  switch (variant) {
-    case 0: return launch_variant<false, false, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 1: return launch_variant<false, false, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 2: return launch_variant<false, true, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 3: return launch_variant<false, true, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 4: return launch_variant<true, false, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 5: return launch_variant<true, false, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 6: return launch_variant<true, true, 1, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 7: return launch_variant<true, true, 2, 1>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 8: return launch_variant<false, false, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 9: return launch_variant<false, false, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 10: return launch_variant<false, true, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 11: return launch_variant<false, true, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 12: return launch_variant<true, false, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 13: return launch_variant<true, false, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    case 14: return launch_variant<true, true, 1, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
-    default: return launch_variant<true, true, 2, 2>(tmA, tmB, g, k_split, persistent, sm_budget, stream);
+  switch (planes) {
+    case 1: return dispatch_planes<1>(tmA, tmB, g, k_split, a_mn, b_kmajor, pair, persistent, stream, sm_budget);
+    case 2: return dispatch_planes<2>(tmA, tmB, g, k_split, a_mn, b_kmajor, pair, persistent, stream, sm_budget);
+    case 3: return dispatch_planes<3>(tmA, tmB, g, k_split, a_mn, b_kmajor, pair, persistent, stream, sm_budget);
+    default: return cudaErrorInvalidValue;
   }
 }
 
@@ -799,7 +836,8 @@ bool gemm_multicast_enabled() {
 void set_gemm_multicast(bool on) { g_mc.store(on ? 1 : 0); }
 
 static bool group_multicast(const GemmGroup& g, bool a_mn, bool b_kmajor, int sm_budget) {
-  if (!gemm_multicast_enabled() || a_mn || b_kmajor || g.k_split > 1 || !group_uses_pairs(g.task[0].m_valid))
+  if (!gemm_multicast_enabled() || a_mn || b_kmajor || g.k_split > 1 || !group_uses_pairs(g.task[0].m_valid) ||
+      g.task[0].planes > 2)
     return false;
   if (sm_budget > 0) {  // a green-context device: its SM count, not the whole GPU's
     int dev = 0, sms = 0;

@@ -37,7 +37,7 @@ struct GemmArgs {
   int32_t m_valid;               // output rows actually stored
   int32_t n_valid;               // output cols actually stored
   int32_t n_ksteps;              // number of k-steps in this launch
-  int32_t planes;                // 1 = bf16, 2 = hi/lo split (fp32-accurate)
+  int32_t planes;                // 1 = bf16, 2 = hi/lo split (fp32acc), 3 = hi/mid/lo (fp32hi)
   int32_t a_z[kMaxKSteps];       // TMA dim-2 index of A's hi plane per k-step (lo = +1)
   int32_t b_z[kMaxKSteps];       // same for B
   int32_t k_len[kMaxKSteps];     // contraction extent of each k-step
@@ -97,6 +97,10 @@ struct GemmGroup {
 // the partial sum into fp32 registers with round-to-nearest (double-buffered
 // TMEM, so the tensor pipe never waits).  FP32-accurate mode uses seg_kb = 4.
 constexpr int kSegKbFp32Acc = 4;
+// fp32hi (3 planes, 6 MMA passes per k-block): the same TMEM additions per
+// partial sum as fp32acc, so half the k-blocks
+constexpr int kSegKbFp32Hi = 2;
+inline int seg_kb_for(int planes) { return planes == 3 ? kSegKbFp32Hi : planes == 2 ? kSegKbFp32Acc : 0; }
 
 // Geometry of a 3-D bf16 tensor map: dim0 = columns (contiguous), dim1 = rows,
 // dim2 = plane index.  Used for both tile-cache slabs and dense matrices.

@@ -10,9 +10,12 @@ from __future__ import annotations
 from . import _native as N
 from .matrix import describe, is_device_tensor
 
+# "fp32acc": split-bf16x3 on the tensor cores (<= 1e-5); "fp32hi": split-bf16x6
+# (three planes, ~10x more accurate, twice the tensor work); "bf16": one plane;
 # "exact": the reference's own arithmetic (rounded multiply then rounded add per
 # rank-1 update, k ascending, output dtype) on CUDA cores -- bit for bit its results
-PRECISIONS = {"bf16": N.TR_PREC_BF16, "fp32acc": N.TR_PREC_FP32ACC, "exact": N.TR_PREC_EXACT}
+PRECISIONS = {"bf16": N.TR_PREC_BF16, "fp32acc": N.TR_PREC_FP32ACC, "fp32hi": N.TR_PREC_FP32HI,
+              "exact": N.TR_PREC_EXACT}
 
 _default_precision = None
 
@@ -29,7 +32,7 @@ def default_precision() -> str:
 
 
 def set_default_precision(p: str | None) -> None:
-    """Process-wide default precision ("fp32acc", "bf16" or "exact"; None: back to the default)."""
+    """Process-wide default precision (a PRECISIONS key; None: back to the default)."""
     global _default_precision
     if p is not None and p not in PRECISIONS:
         raise ValueError(f"unknown precision {p!r}; expected one of {sorted(PRECISIONS)}")

@@ -14,7 +14,7 @@ from paper_1511_04348_b200.dense import set_gemm_pairs
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32acc": 1e-5, "bf16": 1e-2}
+TOL = {"fp32acc": 1e-5, "bf16": 1e-2, "fp32hi": 2e-6}
 
 
 def rel_fro(c, ref):
@@ -47,7 +47,7 @@ def variant(request):
     set_gemm_pairs(False)
 
 
-@pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
+@pytest.mark.parametrize("precision", ["fp32acc", "bf16", "fp32hi"])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 @pytest.mark.parametrize("shape", SHAPES)
 def test_dense_kernel_normal(shape, ta, tb, precision, variant):
@@ -65,7 +65,7 @@ def test_dense_kernel_integers_exact(ta, tb, variant):
     gen = torch.Generator().manual_seed(7)
     for (m, n, k) in [(33, 65, 17), (300, 260, 700)]:
         a, b = make(m, k, n, ta, tb, torch.float64, gen, kind="int")
-        for precision in ("bf16", "fp32acc"):
+        for precision in ("bf16", "fp32acc", "fp32hi"):
             c = dense_gemm(a, b, ta, tb, precision=precision)
             torch.cuda.synchronize()
             assert torch.equal(c, ref_product(a, b, ta, tb)), precision
