@@ -416,7 +416,7 @@ class Runtime:
     """A session: one machine, one HBM tile cache, any number of products.
 
     Signature follows scheduler.py:531-533, plus ``precision`` ("fp32acc" |
-    "bf16" | "exact"; None = ``dense.default_precision()``) and
+    "fp32hi" | "bf16" | "exact"; None = ``dense.default_precision()``) and
     ``hbm_budget_bytes`` (per GPU; 0 = 80% of free HBM).
     """
 
