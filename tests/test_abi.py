@@ -40,6 +40,20 @@ def test_every_declared_symbol_has_a_python_prototype():
     assert set(declared_functions()) <= protos
 
 
+def test_enum_constants_match_the_header():
+    """Every TR_* enumerator of include/tilerun_b200.h that the Python mirror
+    names has the header's value (precisions, dtypes, locations, ...)."""
+    text = re.sub(r"/\*.*?\*/", "", (ROOT / "include" / "tilerun_b200.h").read_text(), flags=re.S)
+    values = {}
+    for body in re.findall(r"typedef\s+enum\s*\{(.*?)\}", text, flags=re.S):
+        for name, val in re.findall(r"(TR_\w+)\s*=\s*(-?\w+)", body):
+            values[name] = int(val, 0)
+    assert values["TR_PREC_FP32HI"] == 3 and values["TR_PREC_EXACT"] == 2
+    mirrored = {k: v for k, v in vars(N).items() if k in values}
+    assert len(mirrored) >= 8
+    assert {k: values[k] for k in mirrored} == mirrored
+
+
 def test_abi_version_and_error_channel():
     assert N.ABI_VERSION == 1
     h = ctypes.c_void_p()
