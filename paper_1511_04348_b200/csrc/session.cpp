@@ -583,7 +583,10 @@ void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level
     cudaStream_t xs = dc.streams[X].stream;
     TimedLaunch tt{};
     trace_begin(d, X, &tt);
-    if (devs_[o].gpu == dc.gpu) {
+    // TR_FORCE_PEER_COPY=1: the cross-GPU call even between logical devices of one
+    // GPU, so single-GPU tests exercise the multi-GPU fill path
+    static const bool force_peer = getenv("TR_FORCE_PEER_COPY") && getenv("TR_FORCE_PEER_COPY")[0] == '1';
+    if (devs_[o].gpu == dc.gpu && !force_peer) {
       TR_CUDA(cudaMemcpyAsync(slot_ptr(d, phys), slot_ptr(o, src_phys), bytes, cudaMemcpyDeviceToDevice, xs));
     } else {
       TR_CUDA(cudaMemcpyPeerAsync(slot_ptr(d, phys), dc.gpu, slot_ptr(o, src_phys), devs_[o].gpu, bytes, xs));

@@ -94,3 +94,29 @@ def test_cross_device_steals_and_exactly_once():
                 assert ev.thief != ev.victim
     ref = (A.double() @ B.double())
     assert float(torch.linalg.norm(C.double() - ref) / torch.linalg.norm(ref)) <= 1e-5
+
+
+def test_peer_copy_api_path_on_one_gpu():
+    """TR_FORCE_PEER_COPY=1 routes L2 fills between logical devices of one GPU
+    through cudaMemcpyPeerAsync -- the call the multi-GPU path makes -- so the
+    cross-GPU fill branch runs (and stays exact) on a single B200.  Separate
+    process: the switch is read once per process."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np\n"
+        "from paper_1511_04348_b200 import homogeneous_machine, run\n"
+        "rng = np.random.default_rng(7)\n"
+        "a = rng.integers(-4, 5, (2048, 1536)).astype(np.float32)\n"
+        "b = rng.integers(-4, 5, (1536, 2048)).astype(np.float32)\n"
+        "c, s = run(homogeneous_machine(3, dtype=np.float32, gpus=[0, 0, 0]), a, b, 512)\n"
+        "assert np.array_equal(c, a.astype(np.float64) @ b.astype(np.float64))\n"
+        "served = sum(d.peer_copies_served for d in s.devices.values())\n"
+        "assert s.cache.l2_hits > 0 and served > 0, (s.cache.l2_hits, served)\n"
+        "print('peer path ok', s.cache.l2_hits, served)\n")
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, TR_FORCE_PEER_COPY="1", PYTHONPATH=str(root))
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600)
+    assert out.returncode == 0 and "peer path ok" in out.stdout, out.stdout[-2000:] + out.stderr[-3000:]
