@@ -371,6 +371,12 @@ int tr_set_gemm_pairs(int32_t on);
  * tile (0 = off, the default; TR_GEMM_MC=1).  Measured slower on B200: only 33
  * such clusters (132 SMs) are co-resident against 74 pairs (148 SMs). */
 int tr_set_gemm_multicast(int32_t on);
+/* K1's die map of GPU `gpu` (measured once per process, at the first session on
+ * that GPU, or here): *n0 / *n1 = CTA-pair clusters expected on each die of a
+ * persistent launch; both 0 when not measured or not usable (TR_K1_DIE=0
+ * disables it).  Grouped persistent launches then give each die a compact block
+ * of output units. */
+int tr_k1_die_map(int32_t gpu, int32_t* n0, int32_t* n1);
 
 /* Split-K policy (process-wide): at most `max_splits` (1..8) K-splits per tile
  * GEMM launch whose output has fewer 128 x 256 blocks than the GPU has SMs

@@ -145,6 +145,7 @@ _PROTOS = {
     "tr_dense_gemm": [P(MatrixC), i32, P(MatrixC), i32, P(MatrixC), i32, i32, vp],
     "tr_set_gemm_pairs": [i32],
     "tr_set_gemm_multicast": [i32],
+    "tr_k1_die_map": [i32, C.POINTER(C.c_int32), C.POINTER(C.c_int32)],
     "tr_set_splitk": [i32],
     "tr_set_small_gemm": [i32],
     "tr_set_narrow_tc": [i32],

@@ -517,6 +517,18 @@ int tr_set_gemm_pairs(int32_t on) {
 int tr_set_gemm_multicast(int32_t on) {
   return guarded([&] { tr::set_gemm_multicast(on != 0); });
 }
+int tr_k1_die_map(int32_t gpu, int32_t* n0, int32_t* n1) {
+  return guarded([&] {
+    if (!n0 || !n1) tr::fail(TR_ERR_VALUE, "null output");
+    *n0 = *n1 = 0;
+    tr::die_map_prepare(gpu);
+    int a = 0, b = 0;
+    if (tr::die_map_ready(gpu, &a, &b)) {
+      *n0 = a;
+      *n1 = b;
+    }
+  });
+}
 int tr_set_task_group(int32_t max_tasks) {
   return guarded([&] {
     if (max_tasks < 1 || max_tasks > tr::kMaxGroup) tr::fail(TR_ERR_VALUE, "task group must be in 1..%d", tr::kMaxGroup);

@@ -246,6 +246,7 @@ Session::Session(const tr_machine& m, int32_t tile, int32_t precision, uint32_t 
       TR_CUDA(cudaSetDevice(dc.gpu));
       TR_CUDA(cudaDeviceGetAttribute(&dc.sms, cudaDevAttrMultiProcessorCount, dc.gpu));
       if (dc.green) dc.sms = dc.green_sms;
+      die_map_prepare(dc.gpu);  // once per GPU and process: K1's die-aware unit order
       size_t free_b = 0;
       TR_CUDA(DevPool::get().free_bytes(dc.gpu, &free_b));
       const double reusable = static_cast<double>(free_b) + static_cast<double>(DevPool::get().cached_bytes());

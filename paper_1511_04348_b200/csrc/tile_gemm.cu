@@ -13,7 +13,10 @@
 // All k-steps of a task (each a separate tile-cache slot, i.e. a different TMA
 // dim-2 coordinate) stream through the same ring; C is written exactly once.
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <vector>
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
@@ -147,6 +150,48 @@ __device__ __forceinline__ Unit unit_of(const GemmGroup& grp, int u, uint32_t ra
   return r;
 }
 
+// The it-th output unit of cluster `cl` (of n_cl), or -1 when it has no more.
+// Default: units cl, cl + n_cl, ... (row blocks fastest inside a task).  Die
+// mode (grp.die_mode): the units are listed task by task, the upper half of
+// the row blocks column by column, then the lower half; die 0's clusters take
+// the first n0 / (n0 + n1) of the list and die 1's the rest, each die striding
+// through its share by its clusters' ranks -- so at any time a die works on
+// ~half the row blocks of a few columns (its own A and B panels) instead of
+// both dies reading every panel of the wave.
+template <int CG, int MC>
+__device__ __forceinline__ int unit_for(const GemmGroup& grp, int cl, int n_cl, int it, int n_units) {
+  if (MC != 1 || CG != 2 || !grp.die_mode) {
+    const int u = cl + it * n_cl;
+    return u < n_units ? u : -1;
+  }
+  const int dr = grp.die_rank[cl];
+  const int d = dr >> 8, r = dr & 0xFF;
+  const int q0 = static_cast<int>(static_cast<int64_t>(n_units) * grp.die_n[0] / (grp.die_n[0] + grp.die_n[1]));
+  const int q = (d ? q0 : 0) + r + it * grp.die_n[d];
+  if (q >= (d ? n_units : q0)) return -1;
+  int t = 0, base = 0;
+  while (t + 1 < grp.n_tasks) {
+    const int nt = (grp.cta_begin[t + 1] - grp.cta_begin[t]) / CG;
+    if (q < base + nt) break;
+    base += nt;
+    ++t;
+  }
+  const int mb = grp.m_blocks[t] / CG;                                    // row blocks (256 rows)
+  const int nb = (grp.cta_begin[t + 1] - grp.cta_begin[t]) / grp.m_blocks[t];  // column blocks
+  const int ql = q - base;
+  const int h0 = (mb + 1) / 2;
+  int row, col;
+  if (ql < h0 * nb) {
+    col = ql / h0;
+    row = ql % h0;
+  } else {
+    const int q2 = ql - h0 * nb, h1 = mb - h0;
+    col = q2 / h1;
+    row = h0 + q2 % h1;
+  }
+  return grp.cta_begin[t] / CG + col * mb + row;  // that tile's index in the default order (unit_of)
+}
+
 // k-blocks of a task and share z of nz of them
 struct KRange {
   int total, lo, hi;
@@ -232,7 +277,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       const uint32_t full0 = ptx::smem_u32(&full[0]);
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = first_unit; u < n_units; u += unit_stride) {
+      for (int it = 0, u; (u = unit_for<CG, MC>(grp, first_unit, unit_stride, it, n_units)) >= 0; ++it) {
         const Unit un = unit_of<CG, MC>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
         const int nb0 = un.n0 + static_cast<int>(rank - lead_rank) * BN_LOCAL;  // B columns this CTA stages
@@ -302,7 +347,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       int seg = 0;  // TMEM partial sums issued so far (all units)
-      for (int u = first_unit; u < n_units; u += unit_stride) {
+      for (int it = 0, u; (u = unit_for<CG, MC>(grp, first_unit, unit_stride, it, n_units)) >= 0; ++it) {
         const Unit un = unit_of<CG, MC>(grp, u, rank);
         const GemmArgs& args = grp.task[un.t];
         const KRange kr = krange(args, un.z, un.nz);
@@ -390,7 +435,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t empty_leader = (CG == 2) ? ptx::mapa_shared(ptx::smem_u32(&acc_empty[0]), lead_rank) : 0u;
     float* stage = epi_stage + (warp - EPI_WARP0) * (C::STAGE_ROWS * C::STAGE_LD);
     int seg = 0;
-    for (int u = first_unit; u < n_units; u += unit_stride) {
+    for (int it = 0, u; (u = unit_for<CG, MC>(grp, first_unit, unit_stride, it, n_units)) >= 0; ++it) {
       const Unit un = unit_of<CG, MC>(grp, u, rank);
       const GemmArgs& args = grp.task[un.t];
       const KRange kr = krange(args, un.z, un.nz);
@@ -561,6 +606,172 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   }
 }
 
+// ---------------------------------------------------------------- die map
+// Which die each SM sits on (B200: two dies, each with half the L2; addresses
+// are homed on one die at fine grain and an L2 hit costs more from the far
+// die): every SM times dependent L2-only loads of kDieLines lines 2 KB apart;
+// its near/far pattern over the lines is its die's signature.
+constexpr int kDieLines = 256, kDieReps = 32, kDieStride = 2048 / 8;
+
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__global__ void die_probe_kernel(const uint64_t* buf, float* lat, int nsm_cap) {
+  if (threadIdx.x != 0) return;
+  const uint32_t sm = sm_id();
+  if (static_cast<int>(sm) >= nsm_cap) return;
+  for (int j = 0; j < kDieLines; ++j) {
+    uint64_t a = reinterpret_cast<uint64_t>(buf + j * kDieStride);
+    asm volatile("ld.global.cg.u64 %0, [%0];" : "+l"(a));  // into L2 (the line holds its own address)
+    a = reinterpret_cast<uint64_t>(buf + j * kDieStride);
+    const long long t0 = clock64();
+#pragma unroll 1
+    for (int r = 0; r < kDieReps; ++r) asm volatile("ld.global.cg.u64 %0, [%0];" : "+l"(a));
+    const long long t1 = clock64();
+    lat[sm * kDieLines + j] = a == 0 ? -1.f : static_cast<float>(t1 - t0) / kDieReps;
+  }
+}
+
+__global__ void die_where_kernel(int* sm_of_block) {
+  if (threadIdx.x == 0) sm_of_block[blockIdx.x] = static_cast<int>(sm_id());
+}
+
+struct DieMap {
+  int n_clusters = 0;
+  int n[2] = {0, 0};
+  uint16_t rank[kMaxDieClusters] = {};
+};
+std::mutex g_die_mu;
+DieMap* g_die[64] = {};     // per device: null = not measured / not usable
+bool g_die_tried[64] = {};
+
+const DieMap* die_lookup(int gpu) {
+  if (gpu < 0 || gpu >= 64) return nullptr;
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  return g_die[gpu];
+}
+
+DieMap* die_measure() {
+  int dev = 0, nsm = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) !=
+                                                 cudaSuccess)
+    return nullptr;
+  if (nsm < 8 || nsm / 2 > kMaxDieClusters || nsm > 256) return nullptr;
+  const size_t words = static_cast<size_t>(kDieLines) * kDieStride;
+  std::vector<uint64_t> h(words, 0);
+  uint64_t* buf = nullptr;
+  float* lat = nullptr;
+  int* where = nullptr;
+  if (cudaMalloc(&buf, words * 8) != cudaSuccess) return nullptr;
+  bool ok = cudaMalloc(&lat, sizeof(float) * 256 * kDieLines) == cudaSuccess &&
+            cudaMalloc(&where, sizeof(int) * 512) == cudaSuccess;
+  std::vector<float> L(static_cast<size_t>(256) * kDieLines, 0.f);
+  std::vector<int> so(nsm, -1);
+  const int smem = 200 * 1024;  // one CTA per SM
+  if (ok) {
+    for (int j = 0; j < kDieLines; ++j) h[static_cast<size_t>(j) * kDieStride] = reinterpret_cast<uint64_t>(buf + j * kDieStride);
+    ok = cudaMemcpy(buf, h.data(), words * 8, cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemset(lat, 0, sizeof(float) * 256 * kDieLines) == cudaSuccess &&
+         cudaFuncSetAttribute(die_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess &&
+         cudaFuncSetAttribute(die_where_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+  }
+  if (ok) {
+    die_probe_kernel<<<nsm, 32, smem>>>(buf, lat, 256);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(static_cast<unsigned>(nsm / 2 * 2));
+    cfg.blockDim = dim3(32);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeClusterDimension;
+    a[0].val.clusterDim.x = 2;
+    a[0].val.clusterDim.y = 1;
+    a[0].val.clusterDim.z = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = 1;
+    ok = cudaLaunchKernelEx(&cfg, die_where_kernel, where) == cudaSuccess && cudaDeviceSynchronize() == cudaSuccess &&
+         cudaMemcpy(L.data(), lat, L.size() * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+         cudaMemcpy(so.data(), where, sizeof(int) * nsm / 2 * 2, cudaMemcpyDeviceToHost) == cudaSuccess;
+  }
+  cudaGetLastError();
+  if (buf) cudaFree(buf);
+  if (lat) cudaFree(lat);
+  if (where) cudaFree(where);
+  if (!ok) return nullptr;
+  // two-means over the SMs' latency vectors: start from agreement with SM 0's
+  // near/far pattern (per-line midpoint threshold), then re-assign each SM by
+  // its projection on the per-line contrast between the two groups' means
+  // (noisy lines carry little weight); every SM must sit clearly on one side
+  const auto at = [&](int s, int j) { return L[static_cast<size_t>(s) * kDieLines + j]; };
+  std::vector<int> die(nsm, 0);
+  std::vector<double> mu0(kDieLines), mu1(kDieLines);
+  for (int j = 0; j < kDieLines; ++j) {
+    float lo = 1e30f, hi = 0.f;
+    for (int s = 0; s < nsm; ++s) {
+      if (at(s, j) <= 0.f) return nullptr;
+      lo = std::min(lo, at(s, j));
+      hi = std::max(hi, at(s, j));
+    }
+    mu0[j] = 0.5 * (lo + hi);  // threshold, reused below
+  }
+  for (int s = 0; s < nsm; ++s) {
+    int agree = 0;
+    for (int j = 0; j < kDieLines; ++j) agree += (at(s, j) > mu0[j]) == (at(0, j) > mu0[j]);
+    die[s] = agree * 2 > kDieLines ? 0 : 1;
+  }
+  double min_margin = 0.0, gap = 0.0;
+  for (int iter = 0; iter < 4; ++iter) {
+    int c0 = 0, c1 = 0;
+    std::fill(mu0.begin(), mu0.end(), 0.0);
+    std::fill(mu1.begin(), mu1.end(), 0.0);
+    for (int s = 0; s < nsm; ++s) {
+      (die[s] ? c1 : c0) += 1;
+      for (int j = 0; j < kDieLines; ++j) (die[s] ? mu1 : mu0)[j] += at(s, j);
+    }
+    if (c0 == 0 || c1 == 0) return nullptr;
+    double wsum = 0.0;
+    for (int j = 0; j < kDieLines; ++j) {
+      mu0[j] /= c0;
+      mu1[j] /= c1;
+      wsum += std::fabs(mu1[j] - mu0[j]);
+    }
+    gap = wsum / kDieLines;  // mean |latency difference| between the groups per line
+    min_margin = 1e30;
+    for (int s = 0; s < nsm; ++s) {
+      double score = 0.0;
+      for (int j = 0; j < kDieLines; ++j) score += (at(s, j) - 0.5 * (mu0[j] + mu1[j])) * (mu1[j] - mu0[j]);
+      // +-1 when the SM's vector equals its group's mean
+      double half = 0.0;
+      for (int j = 0; j < kDieLines; ++j) half += 0.5 * (mu1[j] - mu0[j]) * (mu1[j] - mu0[j]);
+      const double z = half > 0 ? score / half : 0.0;
+      die[s] = z > 0 ? 1 : 0;
+      min_margin = std::min(min_margin, std::fabs(z));
+    }
+  }
+  if (getenv("TR_K1_DIE_DEBUG")) fprintf(stderr, "die map: mean gap %.1f cycles, min margin %.2f\n", gap, min_margin);
+  if (gap < 8.0 || min_margin < 0.3) return nullptr;  // no clean two-way split
+  auto* m = new DieMap;
+  m->n_clusters = nsm / 2;
+  for (int c = 0; c < m->n_clusters; ++c) {
+    const int s0 = so[2 * c], s1 = so[2 * c + 1];
+    if (s0 < 0 || s0 >= nsm || s1 < 0 || s1 >= nsm || die[s0] != die[s1]) {
+      if (getenv("TR_K1_DIE_DEBUG")) fprintf(stderr, "die map: cluster %d on sms %d / %d\n", c, s0, s1);
+      delete m;
+      return nullptr;
+    }
+    const int d = die[s0];
+    m->rank[c] = static_cast<uint16_t>((d << 8) | m->n[d]);
+    m->n[d] += 1;
+  }
+  if (m->n[0] < m->n_clusters / 4 || m->n[1] < m->n_clusters / 4) {
+    delete m;
+    return nullptr;
+  }
+  return m;
+}
+
 template <bool A_MN, bool B_K, int PLANES, int CG, int MC = 1>
 cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmGroup& g, int k_split,
                            bool persistent, int sm_budget, cudaStream_t stream) {
@@ -603,6 +814,18 @@ cudaError_t launch_variant(const CUtensorMap& tmA, const CUtensorMap& tmB, GemmG
     ctas = std::min(ctas, MC > 1 ? std::max(CL, max_clusters * CL) : std::max(CG, (sms / CG) * CG));
   }
   dim3 grid(static_cast<unsigned>(ctas), 1, (k_split > 1 && g.k_split <= 1) ? k_split : 1);
+  // die-aware unit order: a persistent pair grid over the whole GPU, >= 2 waves of units
+  g.die_mode = 0;
+  if (CG == 2 && MC == 1 && persistent && g.k_split <= 1 && grid.z == 1) {
+    int dev = 0;
+    const DieMap* dm = cudaGetDevice(&dev) == cudaSuccess ? die_lookup(dev) : nullptr;
+    if (dm && ctas == 2 * dm->n_clusters && g.cta_begin[g.n_tasks] / 2 >= 2 * dm->n_clusters) {
+      g.die_mode = 1;
+      g.die_n[0] = dm->n[0];
+      g.die_n[1] = dm->n[1];
+      std::memcpy(g.die_rank, dm->rank, sizeof(g.die_rank));
+    }
+  }
   if (CG == 1) {
     kern<<<grid, NUM_THREADS, C::SMEM, stream>>>(tmA, tmB, g);
     return cudaGetLastError();
@@ -981,6 +1204,31 @@ cudaError_t launch_split_convert(const void* src, int src_f64, int64_t ld_src, i
     split_convert_kernel<float><<<static_cast<unsigned>(blocks), threads, 0, stream>>>(
         static_cast<const float*>(src), ld_src, rows, cols, dst, ld_dst, rows_cap, cols_fill, plane_stride, planes);
   return cudaGetLastError();
+}
+
+void die_map_prepare(int gpu) {
+  if (gpu < 0 || gpu >= 64) return;
+  if (const char* e = getenv("TR_K1_DIE"); e && e[0] == '0') return;
+  {
+    std::lock_guard<std::mutex> lk(g_die_mu);
+    if (g_die_tried[gpu]) return;
+    g_die_tried[gpu] = true;
+  }
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (cudaSetDevice(gpu) != cudaSuccess) return;
+  DieMap* m = die_measure();
+  if (prev >= 0) cudaSetDevice(prev);
+  std::lock_guard<std::mutex> lk(g_die_mu);
+  g_die[gpu] = m;
+}
+
+bool die_map_ready(int gpu, int* n0, int* n1) {
+  const DieMap* m = die_lookup(gpu);
+  if (!m) return false;
+  if (n0) *n0 = m->n[0];
+  if (n1) *n1 = m->n[1];
+  return true;
 }
 
 }  // namespace tr

@@ -82,13 +82,30 @@ struct GemmArgs {
 // wave-quantisation loss of a 512-CTA task grid (3.46 waves of 148 SMs), and
 // keeps CTA pairs from competing with a concurrent kernel for SM pairs.
 constexpr int kMaxGroup = 8;
+constexpr int kMaxDieClusters = 80;
 struct GemmGroup {
   int32_t n_tasks;
   int32_t k_split;  // > 1: every task split into k_split k-shares (units z * tiles + tile; partials to task.ws)
   int32_t cta_begin[kMaxGroup + 1];
   int32_t m_blocks[kMaxGroup];
+  // Die-aware unit order (persistent CTA-pair launches over a whole B200; see
+  // die_map_prepare): cluster c is expected on die die_rank[c] >> 8 as that
+  // die's (die_rank[c] & 0xFF)-th cluster.  A performance hint only -- the
+  // cluster -> unit assignment stays a bijection whatever the real placement.
+  int32_t die_mode;
+  int32_t die_n[2];
+  uint16_t die_rank[kMaxDieClusters];
   GemmArgs task[kMaxGroup];
 };
+
+// Measures, once per GPU, which SMs share a die (L2 latency signatures) and
+// where a persistent CTA-pair launch places each cluster; afterwards grouped
+// K1 launches on that GPU give each die a compact block of output units (a
+// row half of the tasks' tiles) so the two dies' L2 halves stop caching the
+// same panels.  Synchronous (runs small kernels on the current device); call
+// before any stream work, e.g. at session creation.  TR_K1_DIE=0 disables.
+void die_map_prepare(int gpu);
+bool die_map_ready(int gpu, int* n0, int* n1);
 
 // Accumulation-precision note (measured on B200, tools/probe_accum.py): the
 // tcgen05 fp32 accumulator rounds toward zero, so a long K accumulated in TMEM

@@ -70,6 +70,16 @@ def set_small_gemm(on: bool) -> None:
     N.call("tr_set_small_gemm", int(bool(on)))
 
 
+def k1_die_map(gpu: int = 0) -> tuple[int, int]:
+    """CTA-pair clusters of a persistent K1 launch expected on each die of GPU
+    ``gpu`` (measured once per process); (0, 0) when unavailable or TR_K1_DIE=0."""
+    import ctypes as C
+
+    n0, n1 = C.c_int32(), C.c_int32()
+    N.call("tr_k1_die_map", int(gpu), C.byref(n0), C.byref(n1))
+    return n0.value, n1.value
+
+
 def set_narrow_tc(on: bool) -> None:
     """Narrow output tiles (<= 32 columns) as the transposed product on the tensor cores (default on)."""
     N.call("tr_set_narrow_tc", int(bool(on)))

@@ -113,3 +113,44 @@ def test_tma_multicast_clusters_match(precision):
         assert float(torch.linalg.norm(outs[mc] - ref) / torch.linalg.norm(ref)) <= tol
     # every output element goes through the same MMA sequence either way
     assert torch.equal(outs[0], outs[1])
+
+
+def test_die_aware_unit_order_is_measured_and_bitwise_neutral(tmp_path):
+    """K1's die map (L2 latency signatures of every SM + the pair grid's
+    placement) splits the 74 pair clusters between the two dies, and the
+    die-aware unit order changes only which cluster computes which tile: the
+    grouped warm product is bit-identical with it off (TR_K1_DIE=0)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    import numpy as np
+
+    from paper_1511_04348_b200.dense import k1_die_map
+
+    n0, n1 = k1_die_map(0)
+    assert n0 + n1 == torch.cuda.get_device_properties(0).multi_processor_count // 2
+    assert min(n0, n1) >= (n0 + n1) // 4
+    code = (
+        "import sys, numpy as np, torch\n"
+        "import paper_1511_04348_b200 as tr\n"
+        "g = torch.Generator(device='cuda').manual_seed(5)\n"
+        "A = torch.randn(8192, 4096, device='cuda', generator=g)\n"
+        "B = torch.randn(4096, 8192, device='cuda', generator=g)\n"
+        "C = torch.empty(8192, 8192, device='cuda')\n"
+        "with tr.Runtime(tr.homogeneous_machine(1, dtype=np.float32), 2048) as rt:\n"
+        "    for _ in range(2):\n"
+        "        rt.multiply(A, B, a_uid='A', b_uid='B', out=C)\n"
+        "np.save(sys.argv[1], C.cpu().numpy())\n"
+        "print('dies', tr.dense.k1_die_map(0))\n")
+    root = Path(__file__).resolve().parents[1]
+    outs = {}
+    for flag in ("1", "0"):
+        f = tmp_path / f"c{flag}.npy"
+        env = dict(os.environ, TR_K1_DIE=flag, PYTHONPATH=str(root))
+        r = subprocess.run([sys.executable, "-c", code, str(f)], capture_output=True, text=True, env=env, timeout=600)
+        assert r.returncode == 0, r.stderr[-3000:]
+        outs[flag] = (np.load(f), r.stdout)
+    assert "dies (0, 0)" in outs["0"][1] and "dies (0, 0)" not in outs["1"][1]
+    assert np.array_equal(outs["1"][0], outs["0"][0])
