@@ -65,7 +65,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "out-of-core GEMM TFLOPS & MLP train samples/s at 1/2/4/8 B200 vs CPU ref"
 UNIT = "TFLOP/s"
-TOL = {"fp32acc": 1e-5, "bf16": 1e-2, "fp32hi": 2e-6}
+TOL = {"fp32acc": 1e-5, "bf16": 1e-2, "fp32hi": 2e-6, "exact": 0.0}
 LEGS = ("cfg4", "cfg2", "cfg1", "mlp", "mlp_parity", "wide", "wide_hetero", "inhomogeneous", "coherence", "ooc",
         "cpu")
 
@@ -617,6 +617,18 @@ def bench_cfg1(args, tr, machine):
         e["ok"] = e["ok"] and stats_ok
         e["counters_equal_reference"] = stats_ok
         res[prec] = e
+    # precision "exact": the reference's own float32 run, bit for bit (its sampled
+    # block and its per-tile sums, tests/golden/make_golden.py gen_cfg1)
+    c, s = tr.run(machine, a, b, 512, precision="exact")
+    blk = c[np.ix_(g["rows"], g["cols"])]
+    sums = np.array([[c[i * 512:(i + 1) * 512, j * 512:(j + 1) * 512].astype(np.float64).sum(dtype=np.float64)
+                      for j in range(4)] for i in range(4)])
+    bitwise = bool(np.array_equal(blk, g["c32_block"]) and np.array_equal(sums, g["c32_tiles"]))
+    err = float(np.linalg.norm(blk.astype(np.float64) - g["c32_block"]) / np.linalg.norm(g["c32_block"]))
+    e = parity_entry(err, "exact", "the reference's own float32 run: its 8x8 block and 16 tile sums, bit for bit")
+    e["ok"] = e["ok"] and bitwise
+    e["bitwise_equal_reference"] = bitwise
+    res["exact"] = e
     return res
 
 

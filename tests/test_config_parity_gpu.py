@@ -68,6 +68,21 @@ def test_cfg1_against_reference_run(cfg1, n_dev, precision):
         assert cs.l2_hits == 0 and cs.l1_hits == hits
 
 
+@pytest.mark.parametrize("n_dev", [1, 3])
+def test_cfg1_exact_is_the_reference_run_bit_for_bit(cfg1, n_dev):
+    """Precision "exact": cfg1 through run() reproduces the reference's own float32
+    threaded run (4 devices) bit for bit -- its sampled 8x8 block and all 16 tile
+    sums (tests/golden/make_golden.py gen_cfg1) -- on any device count."""
+    g, a, b, _ = cfg1
+    c, s = run(homogeneous_machine(n_dev, dtype=np.float32, gpus=[0] * n_dev), a, b, 512, precision="exact")
+    assert c.dtype == np.float32
+    assert np.array_equal(c[np.ix_(g["rows"], g["cols"])], g["c32_block"])
+    sums = np.array([[c[i * 512:(i + 1) * 512, j * 512:(j + 1) * 512].astype(np.float64).sum(dtype=np.float64)
+                      for j in range(4)] for i in range(4)])
+    assert np.array_equal(sums, g["c32_tiles"])
+    assert s.cache.host_fetches == int(g["stats"][0]) and s.cache.writebacks == int(g["stats"][3])
+
+
 @pytest.mark.parametrize("precision", ["fp32acc", "bf16"])
 def test_band_sampled_ragged_product(precision):
     """>= 8 sampled rows and columns in every tile band, ragged last bands in M,
