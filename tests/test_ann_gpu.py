@@ -80,3 +80,22 @@ def test_default_sim_backend_times_improve_with_devices():
         loss, _ = loss_gradients(net, x, t, backend)
         assert np.isfinite(loss)
     assert 0 < times[4] < times[1]
+
+
+@pytest.mark.parametrize("act", ["sigmoid", "relu"])
+@pytest.mark.parametrize("backend_kind", ["tiled", "dense"])
+def test_exact_precision_reproduces_the_reference_bitwise(g, act, backend_kind):
+    """Precision "exact": the reference's DenseBackend trajectories (ann.npz, made
+    by the reference itself) bit for bit -- gradients, 10 losses, final weights --
+    through the tiled runtime on 2 devices or the dense GPU path."""
+    backend = (TiledBackend(homogeneous_machine(2), tile_size=16, mode="gpu", precision="exact")
+               if backend_kind == "tiled" else DenseBackend(precision="exact"))
+    net = net_from(g, act)
+    loss, grads = loss_gradients(net, g[f"{act}_x"], g[f"{act}_t"], backend)
+    assert loss == g[f"{act}_loss0"][0]
+    for i, (gw, gb) in enumerate(grads):
+        assert np.array_equal(gw, g[f"{act}_gw{i}"]) and np.array_equal(gb, g[f"{act}_gb{i}"])
+    traj = [train_step(net, g[f"{act}_x"], g[f"{act}_t"], 0.1, backend) for _ in range(10)]
+    assert np.array_equal(np.array(traj), g[f"{act}_losses"])
+    for i, layer in enumerate(net.layers):
+        assert np.array_equal(layer.weights, g[f"{act}_final_w{i}"])
