@@ -1330,6 +1330,9 @@ def summarize(line):
         s["inhomog_max_rel_share_err"] = round(line["inhomogeneous"]["max_rel_share_error"], 3)
     if "ooc" in line:
         s["ooc_capped_tflops"] = round(line["ooc"]["tflops"], 1)
+    ex = line.get("parity", {}).get("cfg1", {}).get("exact")
+    if ex:
+        s["cfg1_exact_bitwise_reference"] = ex.get("bitwise_equal_reference")
     s["parity_ok"] = line.get("parity_ok")
     return s
 
