@@ -8,6 +8,7 @@
 #include <string>
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/tilerun_b200.h"
 
@@ -35,5 +36,19 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 #define TR_CUDA(call) ::tr::cuda_check((call), #call, __FILE__, __LINE__)
 
 void set_last_error(const char* msg);
+
+// NVTX range on the calling thread (products, device jobs, tasks, fills): named
+// host-side intervals for nsys / Nsight timelines; a no-op unless a tool is attached.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, long long a) {
+    char buf[96];
+    snprintf(buf, sizeof(buf), fmt, a);
+    nvtxRangePushA(buf);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace tr

@@ -564,6 +564,7 @@ int32_t Session::acquire(int d, int s, Job& job, const Mat& src, uint64_t uid, b
 // of device d, on stream s.  Caller holds the directory lock.
 void Session::load_slot(int d, int /*task stream*/, int32_t phys, HitLevel level, int32_t source,
                         const TileKey& key, const Mat& src, int64_t r, int64_t c, Job& job) {
+  NvtxRange nv(level == HIT_L2 ? "tr.fill peer" : "tr.fill host");
   DeviceCtx& dc = devs_[d];
   SlotState& st = dc.slots[phys];
   const int F = dc.width;      // high-priority convert stream (writes slots)
@@ -908,6 +909,7 @@ bool Session::groupable(int d, Job& job, int64_t gtid) {
 // reference's (admit C, acquire A then B per k, release, release C); the
 // arithmetic of all of them is ONE launch on stream s.
 void Session::issue_group(int d, Job& job, const std::vector<int64_t>& gtids, int s) {
+  NvtxRange nv("tr.task_group x%lld", static_cast<long long>(gtids.size()));
   DeviceCtx& dc = devs_[d];
   StreamCtx& sc = dc.streams[s];
   const int64_t T = tile_;
@@ -1141,6 +1143,7 @@ int32_t Session::write_through(int d, int s, const Product& p, int64_t i, int64_
 // _execute_task (scheduler.py:371-410), asynchronous: the host sequence of
 // directory operations is identical; the arithmetic is enqueued on stream s.
 void Session::issue(int d, Job& job, int64_t gtid, int s) {
+  NvtxRange nv("tr.task %lld", static_cast<long long>(gtid));
   DeviceCtx& dc = devs_[d];
   int64_t tid = 0;
   const Product& p = job.prod_of(gtid, &tid);
@@ -1340,6 +1343,7 @@ void Session::reap(int d, Job& job, bool block_oldest) {
 
 // The device worker (scheduler.py:475-505): refill -> pop -> steal -> issue.
 void Session::run_job(int d, Job& job) {
+  NvtxRange nv("tr.device %lld", static_cast<long long>(d));
   DeviceCtx& dc = devs_[d];
   Station& st = *dc.station;
   uint64_t seq = 0;
@@ -1604,6 +1608,7 @@ static std::vector<int64_t> product_order(const Product& p, int order, int64_t r
 
 void Session::run_products(std::vector<Product> prods, int64_t task_offset, int64_t task_stride,
                            tr_gemm_report* rep) {
+  NvtxRange nv("tr.products x%lld", static_cast<long long>(prods.size()));
   if (prods.empty()) fail(TR_ERR_VALUE, "empty product batch");
   if (task_stride < 1 || task_offset < 0 || task_offset >= task_stride) fail(TR_ERR_VALUE, "bad task shard");
   const int64_t T = tile_;

@@ -49,6 +49,7 @@ bool Session::panels_apply(const Job& job) const {
 }
 
 bool Session::run_panels(Job& job) {
+  NvtxRange nv("tr.k_panels");
   const int d = 0;
   DeviceCtx& dc = devs_[d];
   const Product& p = job.prods[0];
