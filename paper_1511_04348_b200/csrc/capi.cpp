@@ -384,6 +384,10 @@ int tr_dense_gemm(const tr_matrix* a, int32_t ta, const tr_matrix* b, int32_t tb
     const int64_t Kb = tb ? B.cols : B.rows, N = tb ? B.rows : B.cols;
     if (K != Kb) tr::fail(TR_ERR_SHAPE, "inner dimensions differ");
     if (C.rows != M || C.cols != N) tr::fail(TR_ERR_SHAPE, "output shape mismatch");
+    // as the reference's matrices (tiles.py as_matrix): every dimension >= 1
+    if (M < 1 || N < 1 || K < 1)
+      tr::fail(TR_ERR_SHAPE, "matrix dimensions must be >= 1, got %lld x %lld x %lld", static_cast<long long>(M),
+               static_cast<long long>(K), static_cast<long long>(N));
     if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) tr::fail(TR_ERR_SHAPE, "dimension too large");
     if (precision != TR_PREC_BF16 && precision != TR_PREC_FP32ACC && precision != TR_PREC_EXACT &&
       precision != TR_PREC_FP32HI)

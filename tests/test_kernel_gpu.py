@@ -154,3 +154,19 @@ def test_die_aware_unit_order_is_measured_and_bitwise_neutral(tmp_path):
         outs[flag] = (np.load(f), r.stdout)
     assert "dies (0, 0)" in outs["0"][1] and "dies (0, 0)" not in outs["1"][1]
     assert np.array_equal(outs["1"][0], outs["0"][0])
+
+
+@pytest.mark.parametrize("shape", [(0, 5, 4), (4, 5, 0), (4, 0, 3)])
+def test_empty_dimensions_are_a_value_error(shape):
+    """As the reference's matrices (tiles.py as_matrix): a zero dimension is a
+    ValueError, on the dense path and through run()."""
+    import numpy as np
+
+    from paper_1511_04348_b200 import homogeneous_machine, run
+
+    m, k, n = shape
+    a, b = np.zeros((m, k)), np.zeros((k, n))
+    with pytest.raises(ValueError):
+        run(homogeneous_machine(1), a, b, 4)
+    with pytest.raises(ValueError):
+        dense_gemm(torch.zeros((m, k), device="cuda"), torch.zeros((k, n), device="cuda"))
