@@ -63,7 +63,9 @@ __device__ __forceinline__ void unpack8(const uint4& h, const uint4& l, float (&
 __device__ __forceinline__ void split_store(uint16_t* dst, int64_t plane, int planes, float v) {
   const __nv_bfloat16 h = __float2bfloat16_rn(v);
   dst[0] = __bfloat16_as_ushort(h);
-  if (planes == 2) dst[plane] = __bfloat16_as_ushort(__float2bfloat16_rn(v - __bfloat162float(h)));
+  // an infinite hi carries the value alone (lo = 0, not inf - inf = NaN)
+  const float hf = __bfloat162float(h);
+  if (planes == 2) dst[plane] = __bfloat16_as_ushort(__float2bfloat16_rn(isinf(hf) ? 0.f : v - hf));
 }
 
 // 4 consecutive values into the planes (8-byte stores; dst 4-element aligned)
@@ -74,7 +76,8 @@ __device__ __forceinline__ void split_store4(uint16_t* dst, int64_t plane, int p
   for (int i = 0; i < 4; ++i) {
     const __nv_bfloat16 b = __float2bfloat16_rn(x[i]);
     h[i] = __bfloat16_as_ushort(b);
-    l[i] = __bfloat16_as_ushort(__float2bfloat16_rn(x[i] - __bfloat162float(b)));
+    const float bf = __bfloat162float(b);
+    l[i] = __bfloat16_as_ushort(__float2bfloat16_rn(isinf(bf) ? 0.f : x[i] - bf));
   }
   *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
   if (planes == 2) *reinterpret_cast<uint2*>(dst + plane) = *reinterpret_cast<const uint2*>(l);

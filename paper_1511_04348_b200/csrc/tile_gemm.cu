@@ -65,8 +65,9 @@ __device__ __forceinline__ void split4(uint16_t* dst, int64_t plane, int planes,
   if (planes >= 2) {
     const float2 f01 = __bfloat1622float2(h01);
     const float2 f23 = __bfloat1622float2(h23);
-    const float2 r01 = make_float2(v.x - f01.x, v.y - f01.y);
-    const float2 r23 = make_float2(v.z - f23.x, v.w - f23.y);
+    // an infinite hi carries the value alone (lo = 0, not inf - inf = NaN)
+    const float2 r01 = make_float2(isinf(f01.x) ? 0.f : v.x - f01.x, isinf(f01.y) ? 0.f : v.y - f01.y);
+    const float2 r23 = make_float2(isinf(f23.x) ? 0.f : v.z - f23.x, isinf(f23.y) ? 0.f : v.w - f23.y);
     const __nv_bfloat162 l01 = __floats2bfloat162_rn(r01.x, r01.y);
     const __nv_bfloat162 l23 = __floats2bfloat162_rn(r23.x, r23.y);
     uint2 lo;
@@ -862,7 +863,8 @@ __global__ void split_convert_kernel(const T* __restrict__ src, int64_t ld_src, 
       const int64_t cc = c + j;
       const double v = (r < rows && cc < cols) ? static_cast<double>(src[r * ld_src + cc]) : 0.0;
       const __nv_bfloat16 h = __float2bfloat16_rn(static_cast<float>(v));
-      const double rest = v - static_cast<double>(__bfloat162float(h));
+      const float hf = __bfloat162float(h);
+      const double rest = isinf(hf) ? 0.0 : v - static_cast<double>(hf);  // inf carried by hi alone
       const __nv_bfloat16 l = __float2bfloat16_rn(static_cast<float>(rest));
       const __nv_bfloat16 l2 = __float2bfloat16_rn(static_cast<float>(rest - static_cast<double>(__bfloat162float(l))));
       hi[j] = __bfloat16_as_ushort(h);

@@ -170,3 +170,34 @@ def test_empty_dimensions_are_a_value_error(shape):
         run(homogeneous_machine(1), a, b, 4)
     with pytest.raises(ValueError):
         dense_gemm(torch.zeros((m, k), device="cuda"), torch.zeros((k, n), device="cuda"))
+
+
+@pytest.mark.parametrize("precision", ["fp32acc", "fp32hi", "bf16", "exact"])
+def test_inf_and_nan_propagate_like_numpy(precision):
+    """Non-finite inputs give non-finite outputs exactly where the reference's
+    are, and NaN where it has NaN, in every mode.  An inf stays inf in the bf16
+    and exact modes; the split modes (fp32acc, fp32hi) keep inf in the hi plane
+    (lo = 0, not inf - inf) but the cross product inf x lo of the other operand
+    is -inf wherever that lo is negative, so about half of such outputs become
+    NaN.  Every finite element stays within tolerance."""
+    import numpy as np
+
+    from paper_1511_04348_b200 import homogeneous_machine, run
+
+    rng = np.random.default_rng(2)
+    a = rng.standard_normal((300, 200)).astype(np.float32)
+    b = np.abs(rng.standard_normal((200, 260))).astype(np.float32) + 0.1
+    a[5, 7] = np.inf
+    a[9, 3] = np.nan
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    for c in (run(homogeneous_machine(1, dtype=np.float32), a, b, 128, precision=precision)[0],
+              dense_gemm(torch.as_tensor(a).cuda(), torch.as_tensor(b).cuda(), precision=precision).cpu().numpy()):
+        assert np.array_equal(np.isfinite(c), np.isfinite(ref)) and np.isnan(c[np.isnan(ref)]).all()
+        if precision in ("bf16", "exact"):
+            assert np.array_equal(np.isinf(c), np.isinf(ref))
+            assert np.array_equal(np.sign(c[np.isinf(ref)]), np.sign(ref[np.isinf(ref)]))
+        else:
+            assert np.isinf(c[np.isinf(ref)]).any()
+        fin = np.isfinite(ref)
+        tol = {"fp32acc": 1e-5, "fp32hi": 2e-6, "bf16": 1e-2, "exact": 1e-6}[precision]
+        assert np.linalg.norm(c[fin] - ref[fin]) <= tol * np.linalg.norm(ref[fin])
