@@ -16,7 +16,7 @@ from dataclasses import dataclass, fields
 from enum import Enum
 
 from . import _native as N
-from .devices import HOST, Machine
+from .devices import HOST, Machine, closest_owner  # noqa: F401 (tilerun.coherence names)
 from .errors import CapacityError
 from .tiles import TileKey
 

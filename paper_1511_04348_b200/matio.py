@@ -21,6 +21,8 @@ from pathlib import Path
 
 import numpy as np
 
+from .tiles import as_matrix  # noqa: F401 (tilerun.matio name)
+
 _HDR = struct.Struct("<QQ")  # rows, cols
 
 

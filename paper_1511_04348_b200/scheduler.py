@@ -30,13 +30,13 @@ from enum import Enum
 import numpy as np
 
 from . import _native as N
-from .coherence import CacheDirectory, CacheStats, UidTable
+from .coherence import AcquireResult, CacheDirectory, CacheStats, UidTable  # noqa: F401 (tilerun.scheduler names)
 from .dense import default_precision, precision_code
-from .devices import Machine
+from .devices import HOST, DeviceSpec, Machine, compute_cost, transfer_cost  # noqa: F401 (tilerun.scheduler names)
 from .errors import NoDeviceError
 from .matrix import ShapeOnly, describe, is_device_tensor, pinned_empty, pinned_zeros
 from .msqueue import MichaelScottQueue
-from .tiles import TiledMatrix, TileKey, decode_task, partition
+from .tiles import TiledMatrix, TileKey, accumulate_product, decode_task, partition, reassemble  # noqa: F401
 
 SCHEMA_VERSION = 1
 MODES = ("gpu", "threaded", "dryrun", "sim")

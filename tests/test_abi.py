@@ -134,3 +134,31 @@ def test_pure_c_client_runs_on_the_gpu(tmp_path):
     exe = _build_c_client(tmp_path)
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "c client ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_reference_module_namespaces_are_mirrored():
+    """Every public name the reference's modules expose (tilerun/{scheduler,
+    tiles,coherence,devices,ann,msqueue,matio}.py, including the names they
+    import for their callers) resolves in the same module here."""
+    import importlib
+
+    expected = {
+        "scheduler": ["Runtime", "run", "plan", "Plan", "Task", "TaskState", "Operand", "Completion", "RunStats",
+                      "DeviceStats", "StealEvent", "ReservationStation", "steal_task", "write_report_json",
+                      "write_report_csv", "AcquireResult", "DeviceSpec", "HOST", "accumulate_product", "compute_cost",
+                      "reassemble", "transfer_cost"],
+        "tiles": ["TileKey", "TiledMatrix", "partition", "reassemble", "accumulate_product", "gemm_tile",
+                  "reference_gemm", "as_matrix", "encode_task", "decode_task"],
+        "coherence": ["CacheDirectory", "CacheStats", "AcquireResult", "HitLevel", "closest_owner"],
+        "devices": ["DeviceSpec", "Machine", "ProximityMatrix", "homogeneous_machine", "load_machine", "save_machine",
+                    "compute_cost", "transfer_cost", "closest_owner", "HOST"],
+        "ann": ["Layer", "Network", "DenseBackend", "TiledBackend", "train_step", "loss_gradients", "bench_pass",
+                "finite_difference_gradients", "xor_dataset", "random_regression", "reference_gemm"],
+        "msqueue": ["MichaelScottQueue"],
+        "matio": ["save_matrix", "load_matrix", "as_matrix"],
+    }
+    missing = []
+    for mod, names in expected.items():
+        m = importlib.import_module(f"paper_1511_04348_b200.{mod}")
+        missing += [f"{mod}.{n}" for n in names if not hasattr(m, n)]
+    assert not missing, missing
