@@ -31,6 +31,19 @@ def default_precision() -> str:
     return p
 
 
+def reference_api_precision() -> str:
+    """Default of the reference-semantics entry points -- tiles.accumulate_product /
+    gemm_tile / reference_gemm (whose contract is the fixed k-ascending order,
+    tiles.py:154-212) and the ANN backends (the reference's ANN is float64 end to
+    end, ann.py:119-121): "exact", the reference's bits, unless TR_PRECISION or
+    set_default_precision() names another precision."""
+    import os
+
+    if _default_precision or os.environ.get("TR_PRECISION"):
+        return default_precision()
+    return "exact"
+
+
 def set_default_precision(p: str | None) -> None:
     """Process-wide default precision (a PRECISIONS key; None: back to the default)."""
     global _default_precision

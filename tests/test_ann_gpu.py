@@ -31,7 +31,10 @@ def relerr(x, ref):
 @pytest.mark.parametrize("act", ["sigmoid", "relu"])
 @pytest.mark.parametrize("backend_kind", ["tiled", "dense"])
 def test_gradients_and_trajectory(g, act, backend_kind):
-    backend = TiledBackend(homogeneous_machine(2), tile_size=16, mode="gpu") if backend_kind == "tiled" else DenseBackend()
+    """The fp32-accurate tensor-core path through the reference's ANN API (the
+    backends' own default is exact, tested bitwise below)."""
+    backend = (TiledBackend(homogeneous_machine(2), tile_size=16, mode="gpu", precision="fp32acc")
+               if backend_kind == "tiled" else DenseBackend(precision="fp32acc"))
     net = net_from(g, act)
     loss, grads = loss_gradients(net, g[f"{act}_x"], g[f"{act}_t"], backend)
     assert abs(loss - g[f"{act}_loss0"][0]) <= 1e-5 * abs(g[f"{act}_loss0"][0])
@@ -99,3 +102,20 @@ def test_exact_precision_reproduces_the_reference_bitwise(g, act, backend_kind):
     assert np.array_equal(np.array(traj), g[f"{act}_losses"])
     for i, layer in enumerate(net.layers):
         assert np.array_equal(layer.weights, g[f"{act}_final_w{i}"])
+
+
+def test_backends_default_to_exact_like_the_reference_float64_ann(monkeypatch):
+    from paper_1511_04348_b200 import dense
+    from paper_1511_04348_b200.ann import ann_default_precision
+
+    monkeypatch.delenv("TR_PRECISION", raising=False)
+    assert ann_default_precision() == "exact" and DenseBackend().precision == "exact"
+    assert TiledBackend(homogeneous_machine(1), tile_size=8).runtime.precision == "exact"
+    monkeypatch.setenv("TR_PRECISION", "fp32acc")
+    assert DenseBackend().precision == "fp32acc"
+    monkeypatch.delenv("TR_PRECISION")
+    dense.set_default_precision("bf16")
+    try:
+        assert DenseBackend().precision == "bf16"
+    finally:
+        dense.set_default_precision(None)

@@ -129,3 +129,22 @@ def test_exact_rejects_fused_epilogues():
 
     with pytest.raises(ValueError, match="exact"):
         GpuMLP([], tile_size=32, precision="exact")
+
+
+def test_tiles_reference_entry_points_default_to_exact():
+    """tiles.reference_gemm / accumulate_product / gemm_tile promise the reference's
+    fixed k-ascending order (tiles.py:154-212): by default they return its bits;
+    precision="fp32acc" gives the tensor-core product."""
+    from paper_1511_04348_b200 import accumulate_product, gemm_tile, reference_gemm
+
+    rng = np.random.default_rng(12)
+    a, b = rng.standard_normal((90, 70)), rng.standard_normal((70, 50))
+    c0 = rng.standard_normal((90, 50))
+    assert np.array_equal(reference_gemm(a, b), O.reference_gemm(a, b))
+    out = c0.copy()
+    accumulate_product(a, b, out)
+    assert np.array_equal(out, O.accumulate_product(a, b, c0.copy()))
+    assert np.array_equal(gemm_tile(a, b, c0), O.accumulate_product(a, b, c0.copy()))
+    fast = reference_gemm(a, b, precision="fp32acc")
+    ref = a @ b
+    assert np.linalg.norm(fast - ref) <= 1e-5 * np.linalg.norm(ref)
