@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _native as N
 from .coherence import AcquireResult, CacheDirectory, CacheStats, UidTable  # noqa: F401 (tilerun.scheduler names)
-from .dense import default_precision, precision_code
+from .dense import default_precision, precision_code, reference_api_precision
 from .devices import HOST, DeviceSpec, Machine, compute_cost, transfer_cost  # noqa: F401 (tilerun.scheduler names)
 from .errors import NoDeviceError
 from .matrix import ShapeOnly, describe, is_device_tensor, pinned_empty, pinned_zeros
@@ -416,7 +416,8 @@ class Runtime:
     """A session: one machine, one HBM tile cache, any number of products.
 
     Signature follows scheduler.py:531-533, plus ``precision`` ("fp32acc" |
-    "fp32hi" | "bf16" | "exact"; None = ``dense.default_precision()``) and
+    "fp32hi" | "bf16" | "exact"; None = ``dense.default_precision()``, or
+    ``dense.reference_api_precision()`` ("exact") in mode "sim") and
     ``hbm_budget_bytes`` (per GPU; 0 = 80% of free HBM).
     """
 
@@ -434,7 +435,9 @@ class Runtime:
         self.steal = steal
         self.coherence = coherence
         self.seed = seed
-        precision = precision or default_precision()
+        # the simulated engine is the reference's (scheduler.py:432-464): its numbers
+        # default to the reference's bits too; the hardware modes default to fp32acc
+        precision = precision or (reference_api_precision() if mode == "sim" else default_precision())
         self.precision = precision
         flags = (N.TR_FLAG_STEAL if steal else 0) | (N.TR_FLAG_COHERENCE if coherence else 0)
         flags |= N.TR_FLAG_DEBUG if directory_debug else 0
