@@ -413,7 +413,10 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
                        else "tile_gemm_kernel (tcgen05 2-CTA 256x256, bf16)",
                        "per_launch": f"{per_launch / (2.0 * T * T * n):g} task(s) of 2*{T}*{T}*{n} flops",
                        "avg_launch_ms": avg_launch_ms, "launches": launches,
-                       "timing": "CUDA events around every K1 launch on its stream, inside the timed value steps"}
+                       "timing": "CUDA events around every K1 launch on its stream, inside the timed value steps",
+                       "mode_note": ("achieved counts algorithmic flops (2MNK); the FP32-accurate mode issues "
+                                     f"{passes} bf16 MMAs per algorithmic MAC, so its ceiling is peak/{passes} "
+                                     "(mode_peak) and frac <= 1/{passes}") if passes > 1 else "one bf16 MMA per MAC"}
     out["clocks"] = clk.summary()
     rt.close()
     del rt
