@@ -416,7 +416,7 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
                        "timing": "CUDA events around every K1 launch on its stream, inside the timed value steps",
                        "mode_note": ("achieved counts algorithmic flops (2MNK); the FP32-accurate mode issues "
                                      f"{passes} bf16 MMAs per algorithmic MAC, so its ceiling is peak/{passes} "
-                                     "(mode_peak) and frac <= 1/{passes}") if passes > 1 else "one bf16 MMA per MAC"}
+                                     f"(mode_peak) and frac <= 1/{passes}") if passes > 1 else "one bf16 MMA per MAC"}
     out["clocks"] = clk.summary()
     rt.close()
     del rt
