@@ -93,7 +93,7 @@ def parse(argv=None):
     p.add_argument("--wide-sizes", default="784,65536,65536,65536")
     p.add_argument("--wide-steps", type=int, default=2)
     p.add_argument("--wide-cache-gib", type=float, default=24.0)
-    p.add_argument("--hetero-steps", type=int, default=4, help="timed steps of the cfg5 8-device leg")
+    p.add_argument("--hetero-steps", type=int, default=8, help="timed steps of the cfg5 8-device leg (shares: +1 warm-up)")
     a = p.parse_args(argv)
     a.legs = [x for x in a.legs.split(",") if x]
     bad = set(a.legs) - set(LEGS)
