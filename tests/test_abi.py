@@ -162,3 +162,13 @@ def test_reference_module_namespaces_are_mirrored():
         m = importlib.import_module(f"paper_1511_04348_b200.{mod}")
         missing += [f"{mod}.{n}" for n in names if not hasattr(m, n)]
     assert not missing, missing
+
+
+def test_die_map_query_without_a_gpu_is_empty_not_an_error():
+    import torch
+
+    from paper_1511_04348_b200.dense import k1_die_map
+
+    if torch.cuda.is_available():
+        pytest.skip("CPU-only check")
+    assert k1_die_map(0) == (0, 0)
