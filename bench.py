@@ -338,14 +338,32 @@ def pick_headline_n(n, T, reserve=24 * 2**30):
     return n
 
 
+def pinned_retry(tr, torch, shape, attempts=4, wait_s=15.0):
+    """pinned_empty with retries: locking 64 GiB can fail for a while on a box whose
+    previous process (killed) is still releasing its pinned pages."""
+    import gc
+
+    for i in range(attempts):
+        try:
+            return tr.matrix.pinned_empty(shape, np.float32)
+        except RuntimeError as e:  # torch's AcceleratorError (cudaErrorOperatingSystem / OOM) only
+            if i + 1 == attempts:
+                raise
+            print(f"bench: pinned allocation of {shape} failed ({str(e).splitlines()[0][:80]}); retrying",
+                  file=sys.stderr, flush=True)
+            gc.collect()
+            torch._C._host_emptyCache()
+            time.sleep(wait_s)
+
+
 def bench_headline(args, tr, torch, machine, gpus, peaks, links):
     """cfg4: value (warm session), e2e (one-shot run()), K1 roofline, parity."""
     n, T = pick_headline_n(args.n, args.tile), args.tile
     ng = len(gpus)
     flops = 2.0 * n ** 3
     torch._C._host_emptyCache()
-    a = tr.matrix.pinned_empty((n, n), np.float32)
-    c = tr.matrix.pinned_empty((n, n), np.float32)
+    a = pinned_retry(tr, torch, (n, n))
+    c = pinned_retry(tr, torch, (n, n))
     fill_normal(torch, a, seed=4, gpu=gpus[0])
     g = -(-n // T)
     out = {"n": n, "tile": T, "tasks": g * g, "k_steps": g}
