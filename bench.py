@@ -458,7 +458,9 @@ def bench_headline(args, tr, torch, machine, gpus, peaks, links):
         if step == 0:
             continue  # warm-up: pinned output pool, HBM pool
         times.append(e0.elapsed_time(e1) / 1e3)
-        detail.append([round(times[-1] * 1e3, 1), round(s.wall_elapsed * 1e3, 1)])
+        # [event-timed step, run()'s own wall time, device span of the product's GPU work] in ms
+        detail.append([round(times[-1] * 1e3, 1), round(s.wall_elapsed * 1e3, 1),
+                       round(max(s.span_ms.values()) if s.span_ms else 0.0, 1)])
         stats_e2e = s
     t_e2e = float(np.mean(times))
     ce = stats_e2e.cache
