@@ -110,7 +110,9 @@ def test_backends_default_to_exact_like_the_reference_float64_ann(monkeypatch):
 
     monkeypatch.delenv("TR_PRECISION", raising=False)
     assert ann_default_precision() == "exact" and DenseBackend().precision == "exact"
-    assert TiledBackend(homogeneous_machine(1), tile_size=8).runtime.precision == "exact"
+    tb = TiledBackend(homogeneous_machine(1), tile_size=8)
+    assert tb.runtime.precision == "exact" and tb.runtime.mode == "sim"  # the reference's default (ann.py:85)
+    assert TiledBackend(homogeneous_machine(1), tile_size=8, mode="gpu").runtime.precision == "exact"
     monkeypatch.setenv("TR_PRECISION", "fp32acc")
     assert DenseBackend().precision == "fp32acc"
     monkeypatch.delenv("TR_PRECISION")
