@@ -170,8 +170,25 @@ def test_cfg4_full_size_out_of_core_band_sampled():
     torch.cuda.empty_cache()
     release_cached_memory()
     torch._C._host_emptyCache()
-    a = pinned_empty((n, n), np.float32)
-    c = pinned_empty((n, n), np.float32)
+
+    def pinned(shape, attempts=4):
+        # locking 64 GiB can fail for a while on a box still releasing a previous
+        # process's pinned pages (cudaErrorOperatingSystem): retry, as bench.py does
+        import gc
+        import time
+
+        for i in range(attempts):
+            try:
+                return pinned_empty(shape, np.float32)
+            except RuntimeError:
+                if i + 1 == attempts:
+                    raise
+                gc.collect()
+                torch._C._host_emptyCache()
+                time.sleep(15)
+
+    a = pinned((n, n))
+    c = pinned((n, n))
     g = torch.Generator(device="cuda").manual_seed(4)
     at = torch.from_numpy(a)
     for r in range(0, n, 4096):
