@@ -547,8 +547,8 @@ def bench_cfg2(args, tr, torch, machine, gpus, links):
                          "tasks_by_device": s.tasks_by_device, "l2_hits": s.cache.l2_hits,
                          "parity": parity_entry(err, prec, f"{nr} rows x {nc} cols (>=8 per tile band)")}
     # cold e2e through run() on pinned host arrays
-    a_host = tr.matrix.pinned_empty((n, n), np.float32)
-    b_host = tr.matrix.pinned_empty((n, n), np.float32)
+    a_host = pinned_retry(tr, torch, (n, n))
+    b_host = pinned_retry(tr, torch, (n, n))
     a_host[...] = A.cpu().numpy()
     b_host[...] = B.cpu().numpy()
     del A, B, C
@@ -1034,9 +1034,9 @@ def bench_ooc(args, tr, torch, peaks, links, gpu):
     blocked task order, evictions, re-fetches, fetch-ahead into dead slots.
     Each step is a cold one-shot session (host -> HBM -> host inside the timing)."""
     n, T = args.ooc_n, args.tile
-    a = tr.matrix.pinned_empty((n, n), np.float32)
-    b = tr.matrix.pinned_empty((n, n), np.float32)
-    c = tr.matrix.pinned_empty((n, n), np.float32)
+    a = pinned_retry(tr, torch, (n, n))
+    b = pinned_retry(tr, torch, (n, n))
+    c = pinned_retry(tr, torch, (n, n))
     fill_normal(torch, a, 3, gpu)
     fill_normal(torch, b, 5, gpu)
     machine = tr.homogeneous_machine(1, dtype=np.float32, gpus=[gpu])
