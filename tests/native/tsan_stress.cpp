@@ -118,8 +118,23 @@ void station_stress() {
     });
   for (auto& t : th) t.join();
   for (auto& a : taken) CHECK(a.load() == 1);
-  CHECK(steals.load() > 0);
   std::printf("stations: %d tasks, %d steals\n", tasks, steals.load());
+  // deterministic stealing: an owner reserves ids and never runs them; seven
+  // thieves race to steal them from the back -- each id is taken exactly once
+  tr::MSQueue q2;
+  for (int t = 0; t < 64; ++t) q2.enqueue(static_cast<uint64_t>(t));
+  tr::Station owner(0, 64);
+  CHECK(static_cast<int>(owner.refill(q2, 64).size()) == 64);
+  std::vector<std::atomic<int>> got(64);
+  for (auto& a : got) a.store(0);
+  std::vector<std::thread> thieves;
+  for (int d = 1; d < N; ++d)
+    thieves.emplace_back([&] {
+      uint64_t tid;
+      while (owner.try_steal(&tid)) got[tid].fetch_add(1);
+    });
+  for (auto& t : thieves) t.join();
+  for (auto& a : got) CHECK(a.load() == 1);
 }
 
 void directory_stress() {
