@@ -172,3 +172,19 @@ def test_die_map_query_without_a_gpu_is_empty_not_an_error():
     if torch.cuda.is_available():
         pytest.skip("CPU-only check")
     assert k1_die_map(0) == (0, 0)
+
+
+def test_compat_tilerun_alias(monkeypatch):
+    """compat/tilerun makes `import tilerun` (and its submodules) the B200 package."""
+    import importlib
+    import sys
+
+    monkeypatch.syspath_prepend(str(ROOT / "compat"))
+    for k in [k for k in sys.modules if k == "tilerun" or k.startswith("tilerun.")]:
+        monkeypatch.delitem(sys.modules, k)
+    t = importlib.import_module("tilerun")
+    from tilerun.scheduler import Runtime as R2
+    from tilerun.tiles import reference_gemm
+
+    assert t.run is tr.run and R2 is tr.Runtime and reference_gemm is tr.reference_gemm
+    assert t.cli.main is tr.cli.main and set(tr.__all__) <= set(dir(t))
